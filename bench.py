@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 preconditioned Krylov path (one JSON line on rank 0).
+
+Metric (BASELINE.json): solve time to 1e-8 rel. residual; DoF*iter/s; SpMV
+GB/s vs B200 HBM peak.  `value` is DoF*iterations per second of whole solves
+(summed over ranks, each rank an independent replica = weak scaling), with the
+right-hand side already resident in HBM; `e2e` is the same metric through the
+public host-pointer C-ABI call (sdg_bicgstab / sdg_pd_gmres: host->device copy
+of b and device->host copy of x inside the timed region).  One step = one full
+preconditioned solve of the workload's system.
+
+Workload (N=1): BASELINE.json configs[1] = "c2": 160 x 160 cells per
+subdomain (102,720 DoF), log-normal K, BiCGSTAB with td_bgs(Uzawa(AMG_V),
+AMG_D').  Other configs are parity cases (tests/) and can be run with --config.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "solve time to 1e-8 rel. residual; DoF·iter/s; SpMV GB/s vs B200 HBM peak"
+UNIT = "DoF*iter/s"
+FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-solves", type=int, default=1)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def measured_peak_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload_desc(cfg, s):
+    solver = {"bicgstab": "BiCGSTAB", "gmres50": "GMRES(50)", "pdgmres": "PD-GMRES"}[cfg.solver]
+    k = "log-normal K (log10 K ~ N(0,1), seed 13229)" if cfg.lognormal else f"K={cfg.permeability:g}"
+    return (f"{cfg.name}: {cfg.n}x{cfg.n} cells per subdomain, {s.n_total():,} DoF, {k}, {solver} + "
+            f"td_bgs(Uzawa(AMG_V), AMG_D'), AMG levels V{cfg.v_max_levels}/D{cfg.d_max_levels}, tol 1e-8*||b||")
+
+
+def solve_device(sdc, cfg, s, p, b_ptr, x_ptr, tol, ctx):
+    if cfg.solver == "bicgstab":
+        return sdc.bicgstab_device(s.matrix, p, b_ptr, x_ptr, tol, 20000, ctx=ctx)
+    ctrl = sdc.RestartController.fixed(50) if cfg.solver == "gmres50" else sdc.RestartController.defaults()
+    return sdc.pd_gmres_device(s.matrix, p, b_ptr, x_ptr, tol, 4000, ctrl, ctx=ctx)
+
+
+def solve_host(sdc, cfg, s, p, b, tol):
+    if cfg.solver == "bicgstab":
+        return sdc.bicgstab(s.matrix, p, b, tol, 20000)
+    ctrl = sdc.RestartController.fixed(50) if cfg.solver == "gmres50" else sdc.RestartController.defaults()
+    return sdc.pd_gmres(s.matrix, p, b, tol, 4000, ctrl)
+
+
+def reference_solve(R, rs, rtd, cfg, b, tol):
+    if cfg.solver == "bicgstab":
+        return R.bicgstab(rs.a, b, tol, 20000, precond=rtd)
+    if cfg.solver == "gmres50":
+        return R.pd_gmres(rs.a, b, tol, 4000, precond=rtd, m_init=50, m_min=50, m_max=50)
+    return R.pd_gmres(rs.a, b, tol, 4000, precond=rtd)
+
+
+def ref_system(s):
+    from oracle.refpy import Csr, System
+    return System(s.n_total(), s.n_u, s.n_vel, s.n_pff, s.n_ppm,
+                  Csr(s.n_total(), s.n_total(), s.matrix.row_offsets, s.matrix.col_indices, s.matrix.values), s.rhs)
+
+
+def cpu_baseline(cfg, s, tol, solves):
+    """The reference's own CPU solver (oracle/_ref) on the same system, 1 core."""
+    try:
+        from oracle.refpy import RefLib
+        R = RefLib()
+    except Exception as e:  # pragma: no cover - only when the oracle was not built
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+    rs = ref_system(s)
+    t0 = time.perf_counter()
+    rtd = R.td(rs, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
+    setup = time.perf_counter() - t0
+    its, secs = 0, 0.0
+    for _ in range(solves):
+        t0 = time.perf_counter()
+        _, rep = reference_solve(R, rs, rtd, cfg, s.rhs, tol)
+        secs += time.perf_counter() - t0
+        its += rep.iterations
+    return {"value": s.n_total() * its / secs, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{solves} full solve(s) of {cfg.name} ({its // solves} iterations each) with the compiled "
+                      f"reference (oracle/_ref, single-threaded), setup {setup:.2f} s excluded",
+            "solve_s": secs / solves, "iterations": its // solves, "setup_s": setup}
+
+
+def run_reference(args):
+    rank, local_rank, world = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2108_13229_b200 import scenarios
+    from oracle.refpy import RefLib
+    cfg = scenarios.CONFIGS[args.config]
+    s = scenarios.build_system(cfg)
+    tol = 1e-8 * float(np.linalg.norm(s.rhs))
+    R = RefLib()
+    rs = ref_system(s)
+    t0 = time.perf_counter()
+    rtd = R.td(rs, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
+    setup = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        reference_solve(R, rs, rtd, cfg, s.rhs, tol)
+    times, its = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, rep = reference_solve(R, rs, rtd, cfg, s.rhs, tol)
+        times.append(time.perf_counter() - t0)
+        its.append(rep.iterations)
+    value = s.n_total() * sum(its) / sum(times)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_desc(cfg, s), "dof": s.n_total(), "nnz": s.matrix.nnz(),
+                       "iterations": its, "setup_s": setup},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                             "sample": f"each step = 1 full solve of {cfg.name} by the compiled reference "
+                                       f"(single-threaded C++; its solver uses one core)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    rank, local_rank, world = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local_rank)
+    from paper_2108_13229_b200 import scenarios, sdc
+
+    cfg = scenarios.CONFIGS[args.config]
+    t0 = time.perf_counter()
+    s = scenarios.build_system(cfg)
+    assembly_s = time.perf_counter() - t0
+    n = s.n_total()
+    tol = 1e-8 * float(np.linalg.norm(s.rhs))
+    ctx = sdc.Context(local_rank)
+    t0 = time.perf_counter()
+    p = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels, ctx=ctx)
+    setup_s = time.perf_counter() - t0
+    hier_v, hier_d = p.hierarchy(0), p.hierarchy(1)
+
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    b_dev = torch.from_numpy(s.rhs).to(dev)
+    x_dev = torch.zeros(n, dtype=torch.float64, device=dev)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        return solve_device(sdc, cfg, s, p, b_dev.data_ptr(), x_dev.data_ptr(), tol, ctx)
+
+    for _ in range(args.warmup):
+        rep = step()
+    if not rep.converged:
+        raise RuntimeError(f"warm-up solve did not converge: {rep}")
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    evs, iters = [], []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush outside the timed pair
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        rep = step()
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        evs.append((e0, e1))
+        iters.append(rep.iterations)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = ctx.launches - launches0
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    work = float(n) * sum(iters)
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        w = torch.tensor([work], dtype=torch.float64, device=dev)
+        dist.all_reduce(w, op=dist.ReduceOp.SUM)
+        total_ms, work = float(t.item()), float(w.item())
+    value = work / (total_ms / 1e3)
+
+    # parity self-check of the timed solve (residual of the returned x)
+    x_host = x_dev.cpu().numpy()
+    true_res = float(np.linalg.norm(s.rhs - sdc.spmv(s.matrix, x_host)))
+
+    # e2e through the public host-pointer C-ABI call
+    e2e = None
+    if not args.no_e2e:
+        b_pin = torch.from_numpy(s.rhs.copy()).pin_memory()
+        b_np = b_pin.numpy()
+        solve_host(sdc, cfg, s, p, b_np, tol)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e_its = 0
+        for _ in range(args.steps):
+            res = solve_host(sdc, cfg, s, p, b_np, tol)
+            e_its += res.report.iterations
+        e_s = time.perf_counter() - t0
+        e_work = float(n) * e_its
+        if dist:
+            t = torch.tensor([e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            w = torch.tensor([e_work], dtype=torch.float64, device=dev)
+            dist.all_reduce(w, op=dist.ReduceOp.SUM)
+            e_s, e_work = float(t.item()), float(w.item())
+        e2e = {"value": e_work / e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+               "ms_per_step": 1e3 * e_s / args.steps, "timing": "host wall clock around the synchronous C-ABI call"}
+
+    # live per-kernel-family profile of one more solve (CUDA events on the library stream)
+    ctx.set_profiling(True)
+    step()
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    peak, peak_kind = measured_peak_gbs()
+
+    def roof(fam):
+        f = prof[fam]
+        per_launch_ms = f["ms"] / f["launches"]
+        per_launch_bytes = f["bytes"] / f["launches"]
+        ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+        return {"kernel": fam, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "peak_source": peak_kind, "traffic": None,
+                "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms, "launches": f["launches"],
+                "share_of_step": f["ms"] / sum(v["ms"] for v in prof.values())}
+
+    dominant = max(prof, key=lambda k: prof[k]["ms"])
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg, s), "dof": n, "nnz": s.matrix.nnz(),
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed between timed solves (256 MiB write, outside the event pair)",
+                   "iterations": iters, "setup_s": setup_s, "assembly_s": assembly_s,
+                   "hierarchy_v": hier_v, "hierarchy_d": hier_d, "omega": p.omega(),
+                   "true_residual_rel": true_res / float(np.linalg.norm(s.rhs))},
+        "solve_ms": total_ms / args.steps,
+        "roofline": roof(dominant),
+        "spmv_roofline": roof("spmv") if "spmv" in prof else None,
+        "kernel_profile": {k: {"launches": v["launches"], "ms": v["ms"], "GBps": v["bytes"] / v["ms"] / 1e6}
+                           for k, v in prof.items()},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, s, tol, args.cpu_sample_solves)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

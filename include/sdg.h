@@ -1,0 +1,265 @@
+/*
+ * sdg.h -- C-ABI of libsdgpu.so, the B200-native (sm_100a, fp64) replacement
+ * for the reference's preconditioned Krylov path (arXiv 2108.13229 reference,
+ * /root/reference/proj/core).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * Every entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/proj/core).  A header-only C++ adapter that
+ * turns these handles back into the reference's own types
+ * (sdc::LinearOperator, sdc::Preconditioner subclasses, sdc::pd_gmres /
+ * sdc::bicgstab signatures) is include/sdc_gpu.hpp; the Python mirror is
+ * paper_2108_13229_b200/sdc.py.
+ *
+ * Memory contract (mirrors operator.hpp:30-33 and SURVEY.md §8(b)):
+ *   - `*_host` pointers are borrowed for the duration of the call only;
+ *   - `*_dev` pointers are device pointers on the handle's device, consumed
+ *     in stream order on the handle's stream (no implicit synchronisation);
+ *   - handles own their device memory; all handles created from one context
+ *     share that context's CUDA stream, and calls on a context are serialised.
+ *
+ * Error contract: every function returning int returns SDG_OK (0) or one of
+ * the codes below; sdg_last_error() returns a thread-local message.  The C++
+ * adapter rethrows SDG_EDIM as std::invalid_argument and SDG_ESINGULAR /
+ * SDG_EBREAKDOWN as std::runtime_error, which is what the reference throws
+ * (krylov.cpp:52-55,126,150,215; precond.cpp:104-105; lu.cpp:141-143).
+ */
+#ifndef SDG_H
+#define SDG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDG_OK 0
+#define SDG_EDIM 1        /* dimension / contract violation (std::invalid_argument) */
+#define SDG_ESINGULAR 2   /* zero diagonal, zero pivot, singular Hessenberg (std::runtime_error) */
+#define SDG_EBREAKDOWN 3  /* repeated BiCGSTAB breakdown (std::runtime_error) */
+#define SDG_ECUDA 4       /* CUDA runtime / library failure */
+#define SDG_ENOMEM 5      /* device allocation failure */
+#define SDG_ENCCL 6       /* NCCL failure (strip-sharded handles) */
+#define SDG_EINVAL 7      /* bad handle / argument */
+
+typedef struct sdg_context sdg_context;
+typedef struct sdg_matrix sdg_matrix;
+typedef struct sdg_precond sdg_precond;
+
+/* Block preconditioner kinds: precond.hpp:162 (BlockPrecondKind). */
+#define SDG_TD_BJ 0
+#define SDG_TD_BGS 1
+#define SDG_PV_BJ 2
+#define SDG_PV_BGS 3
+
+/* RestartController (krylov.hpp:23-47). Updated in place by sdg_pd_gmres
+ * only on the caller's copy semantics of the reference: the reference takes
+ * the controller by value, so sdg_pd_gmres never writes it back. */
+typedef struct sdg_restart {
+    int m_init;
+    int m_min;
+    int m_step;
+    int m_max;
+    int current_m;
+    double previous_rate;
+    int has_rate_sample;
+    double alpha_p;
+    double alpha_d;
+    double stall_threshold;
+} sdg_restart;
+
+/* SolveReport (krylov.hpp:12-18).  residual_history is caller-owned with
+ * capacity history_capacity (may be NULL / 0); history_length reports the
+ * full length the reference would have produced. */
+typedef struct sdg_report {
+    int iterations;
+    int converged;
+    double wall_time;       /* seconds, host clock around the whole call */
+    double final_residual;
+    double* residual_history;
+    int history_capacity;
+    int history_length;
+    int64_t precond_applications; /* applications made by this solve */
+    double device_ms;       /* CUDA-event time of the device-resident part */
+} sdg_report;
+
+/* AmgOptions (precond.hpp:64-72).  components: NULL or one label per row. */
+typedef struct sdg_amg_options {
+    int max_levels;
+    double strength_theta;
+    int coarse_threshold;
+    const int* components;
+} sdg_amg_options;
+
+/* UzawaConfig (precond.hpp:122-129), inexact mode only (exact mode is the
+ * test-only DirectSolvePreconditioner, out of scope per SURVEY.md §2).
+ * omega_override: NaN -> estimate by power iteration as the reference does
+ * (precond.cpp:278-286); otherwise use the given relaxation directly. */
+typedef struct sdg_uzawa_options {
+    sdg_amg_options amg;
+    double power_tol_rel;
+    int power_max_iters;
+    unsigned power_seed;
+    double omega_override;
+} sdg_uzawa_options;
+
+/* Fills the reference defaults: RestartController::defaults(),
+ * AmgOptions{}, UzawaConfig{}. */
+void sdg_restart_defaults(sdg_restart* c);
+void sdg_amg_defaults(sdg_amg_options* o);
+void sdg_uzawa_defaults(sdg_uzawa_options* o);
+
+const char* sdg_last_error(void);
+const char* sdg_version(void);
+
+/* ---- context ----------------------------------------------------------- */
+int sdg_context_create(int device, sdg_context** out);
+int sdg_context_destroy(sdg_context* ctx);
+int sdg_context_synchronize(sdg_context* ctx);
+/* The context's cudaStream_t, as void* (for callers that order their own
+ * copies against the solver, e.g. the e2e bench leg). */
+void* sdg_context_stream(sdg_context* ctx);
+/* Number of this library's kernels launched on the context so far. */
+int64_t sdg_context_launches(sdg_context* ctx);
+
+/* Live kernel profiler.  When enabled, every launch is bracketed by CUDA
+ * events on the context stream and tagged with its algorithmic bytes
+ * (SURVEY.md §8(d) byte model); sdg_context_profile folds them per kernel
+ * family.  Enabling clears previous totals.  Families: 0 spmv, 1 gs,
+ * 2 restrict, 3 prolong, 4 coarse, 5 uzawa, 6 ortho, 7 bicg, 8 vec, 9 setup. */
+#define SDG_PROF_FAMILIES 10
+int sdg_context_set_profiling(sdg_context* ctx, int enable);
+int sdg_context_profile(sdg_context* ctx, int family, int64_t* launches, double* total_ms,
+                        double* total_bytes);
+const char* sdg_profile_family_name(int family);
+
+/* ---- matrices / LinearOperator ------------------------------------------
+ * Replaces SparseMatrix (sparse.hpp:17-46) as the operand and
+ * LinearOperator::from_matrix (operator.hpp:24-27) as the operator.  CSR,
+ * int32 offsets/columns, fp64 values; the host arrays are copied. */
+int sdg_matrix_create(sdg_context* ctx, int n_rows, int n_cols, const int* rowptr,
+                      const int* col, const double* val, sdg_matrix** out);
+int sdg_matrix_destroy(sdg_matrix* a);
+int sdg_matrix_rows(const sdg_matrix* a);
+int sdg_matrix_cols(const sdg_matrix* a);
+int64_t sdg_matrix_nnz(const sdg_matrix* a);
+
+/* spmv (sparse.cpp:81-90): y = A x. */
+int sdg_spmv(sdg_matrix* a, const double* x_host, double* y_host);
+/* spmv_add (sparse.cpp:98-108): y = y + alpha A x. */
+int sdg_spmv_add(sdg_matrix* a, const double* x_host, double* y_host, double alpha);
+int sdg_spmv_device(sdg_matrix* a, const double* x_dev, double* y_dev);
+/* sor_sweep (precond.cpp:92-108): one forward sweep, z updated in place. */
+int sdg_sor_sweep(sdg_matrix* a, double* z_host, const double* r_host, double omega);
+
+/* ---- preconditioners (operator.hpp:34-62) ------------------------------- */
+/* AmgPreconditioner(a, opts) (precond.hpp:101-120): amg_setup
+ * (precond.cpp:189-217) on the host, V(1,1) apply (precond.cpp:233-259) on
+ * the device. */
+int sdg_amg_create(sdg_matrix* a, const sdg_amg_options* opts, sdg_precond** out);
+/* UzawaPreconditioner(v, b, c, cfg) (precond.cpp:264-299). */
+int sdg_uzawa_create(sdg_matrix* v, sdg_matrix* b, sdg_matrix* c, const sdg_uzawa_options* cfg,
+                     sdg_precond** out);
+/* BlockPreconditioner(kind, matrix, n_v, n_pff, n_ppm, first, pm)
+ * (precond.cpp:304-363).  Retains `first` and `pm` (shared ownership, as the
+ * reference's shared_ptr<const Preconditioner>). */
+int sdg_block_create(int kind, sdg_matrix* matrix, int n_v, int n_pff, int n_ppm,
+                     sdg_precond* first, sdg_precond* pm, sdg_precond** out);
+/* IdentityPreconditioner(n) (operator.hpp:64-76). */
+int sdg_identity_create(sdg_context* ctx, int n, sdg_precond** out);
+/* ground_dof (precond.cpp:375-392) applied on the host to a CSR copy. */
+int sdg_ground_dof_host(int n, const int* rowptr, const int* col, double* val_inout, int dof);
+
+/* The whole MonolithicDriver::build_preconditioner wiring (bench.cpp:121-182)
+ * for kind td_bj / td_bgs in one call: D' = ground_dof(A[pm,pm]), V labels
+ * u = 0 / v = 1, Uzawa(AMG_V) on [v | p_ff], AMG on D'.  v_max_levels /
+ * d_max_levels set AmgOptions.max_levels of the two hierarchies (SURVEY.md
+ * §8(d) makes them per-config parity inputs).  omega_override as above. */
+int sdg_td_create(sdg_matrix* a, int n_u, int n_vel, int n_pff, int n_ppm, int kind,
+                  int v_max_levels, int d_max_levels, double omega_override,
+                  sdg_precond** out);
+
+int sdg_precond_destroy(sdg_precond* p);
+int sdg_precond_rows(const sdg_precond* p);
+/* Preconditioner::apply (operator.hpp:40-43). */
+int sdg_precond_apply(sdg_precond* p, const double* r_host, double* z_host);
+int sdg_precond_apply_device(sdg_precond* p, const double* r_dev, double* z_dev);
+/* Preconditioner::applications() (operator.hpp:55). */
+int64_t sdg_precond_applications(const sdg_precond* p);
+/* setup_memory_doubles / work_per_apply (operator.hpp:51-53). */
+int64_t sdg_precond_setup_memory_doubles(const sdg_precond* p);
+int64_t sdg_precond_work_per_apply(const sdg_precond* p);
+/* UzawaPreconditioner::omega() (precond.hpp:141); for a td_* block, the
+ * omega of its Uzawa first block; NaN otherwise. */
+double sdg_precond_omega(const sdg_precond* p);
+/* Host seconds spent in setup (aggregation, Galerkin, coarse factor, omega). */
+double sdg_precond_setup_seconds(const sdg_precond* p);
+/* Hierarchy shape of an AMG handle (or of the V / D' hierarchies of a td_*
+ * handle, which = 0 / 1): number of levels, rows and nnz per level. */
+int sdg_precond_hierarchy(const sdg_precond* p, int which, int* n_levels, int* rows,
+                          int64_t* nnz, int capacity);
+/* Use CUDA-graph capture for device applies (default on). */
+int sdg_precond_set_graphs(sdg_precond* p, int enable);
+
+/* ---- Krylov solvers (krylov.cpp) ----------------------------------------
+ * precond may be NULL (identity, krylov.cpp:19-25).  x starts at zero
+ * (krylov.cpp:58,194).  tol_abs is absolute, as in the reference. */
+/* pd_gmres (krylov.hpp:57-59, krylov.cpp:47-184). */
+int sdg_pd_gmres(sdg_matrix* a, sdg_precond* precond, const double* b_host, double* x_host,
+                 double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep);
+int sdg_pd_gmres_device(sdg_matrix* a, sdg_precond* precond, const double* b_dev,
+                        double* x_dev, double tol_abs, int max_restarts,
+                        const sdg_restart* ctrl, sdg_report* rep);
+/* bicgstab (krylov.hpp:63-65, krylov.cpp:186-292). */
+int sdg_bicgstab(sdg_matrix* a, sdg_precond* precond, const double* b_host, double* x_host,
+                 double tol_abs, int max_iters, sdg_report* rep);
+int sdg_bicgstab_device(sdg_matrix* a, sdg_precond* precond, const double* b_dev,
+                        double* x_dev, double tol_abs, int max_iters, sdg_report* rep);
+/* power_iteration (krylov.hpp:79-80, krylov.cpp:307-339) on y = A x. */
+int sdg_power_iteration(sdg_matrix* a, double tol_rel, int max_iters, unsigned seed,
+                        double* value, int* iterations, int* converged);
+
+/* ---- host-side input producer (stays host C++) ----------
+ * assemble_monolithic (assembly.cpp:327-380) on the n x n free-flow box
+ * over the n x n porous square, restated in this library so the bench can
+ * build inputs without the reference.  k_cell: NULL for the scalar
+ * permeability `permeability` (bitwise identical to the reference), or n*n
+ * per-cell porous permeabilities (row-major, j*n+i; the log-normal
+ * extension of BASELINE.json configs 2/4 -- parity unpinned, see
+ * DESIGN.md).  Two-phase: call with NULL outputs to get sizes. */
+typedef struct sdg_scenario {
+    int n;
+    double permeability;
+    double alpha_bj;
+    double nu;
+    double rho;
+    double dt;      /* +inf -> stationary */
+    double t_end;
+    double dp_max;
+    double t;       /* inflow_pressure(t) = dp_max/2 (1 - cos(pi t / t_end)) */
+} sdg_scenario;
+
+int sdg_assemble_monolithic(const sdg_scenario* sc, const double* k_cell, const double* v_prev,
+                            int* n_total, int64_t* nnz, int* n_u, int* n_vel, int* n_pff,
+                            int* n_ppm, int* rowptr, int* col, double* val, double* rhs);
+
+/* ---- host-side setup inspection (no GPU needed) ----------------------------
+ * The aggregation hierarchy exactly as the device preconditioner builds it
+ * (amg_setup, precond.cpp:189-217, minus the coarse factorization), so the
+ * setup can be checked bit for bit against the reference on a CPU-only box.
+ * sdg_host_hierarchy_level: NULL outputs are skipped; n_sched_levels is the
+ * Gauss-Seidel level-schedule depth of the level (0 on the coarsest). */
+typedef struct sdg_host_hierarchy sdg_host_hierarchy;
+int sdg_host_hierarchy_build(int n, const int* rowptr, const int* col, const double* val,
+                             const sdg_amg_options* opts, sdg_host_hierarchy** out);
+int sdg_host_hierarchy_levels(const sdg_host_hierarchy* h);
+int sdg_host_hierarchy_level(const sdg_host_hierarchy* h, int lev, int* n, int64_t* nnz,
+                             int* n_coarse, int* n_sched_levels, int* rowptr, int* col,
+                             double* val, int* agg);
+void sdg_host_hierarchy_destroy(sdg_host_hierarchy* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SDG_H */

@@ -1,0 +1,207 @@
+// Internal plumbing of libsdgpu.so: errors, device buffers, the per-handle
+// context (device + stream), host/device CSR.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sdg.h"
+
+namespace sdg {
+
+// Internal exception carrying an SDG_* code; the C-ABI layer converts it to
+// a return code + thread-local message.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define SDG_CUDA(call)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            ::sdg::fail(e_ == cudaErrorMemoryAllocation ? SDG_ENOMEM : SDG_ECUDA,        \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));              \
+    } while (0)
+
+// Owning device allocation.
+template <class T>
+class DevBuf {
+public:
+    DevBuf() = default;
+    explicit DevBuf(std::size_t n) { resize(n); }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    void resize(std::size_t n) {
+        release();
+        if (n) SDG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+        n_ = n;
+    }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    std::size_t size() const { return n_; }
+    void upload(const T* h, std::size_t n, cudaStream_t s) {
+        if (n) SDG_CUDA(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void upload(const std::vector<T>& h, cudaStream_t s) {
+        if (h.size() != n_) resize(h.size());
+        upload(h.data(), h.size(), s);
+    }
+
+private:
+    T* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+// Pinned host scratch for small device->host status reads.
+class PinnedBuf {
+public:
+    explicit PinnedBuf(std::size_t bytes) : n_(bytes) { SDG_CUDA(cudaMallocHost(&p_, bytes)); }
+    ~PinnedBuf() {
+        if (p_) cudaFreeHost(p_);
+    }
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    template <class T>
+    T* as() const { return static_cast<T*>(p_); }
+    std::size_t bytes() const { return n_; }
+
+private:
+    void* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+// Kernel families for the live profiler (sdg_context_profile).
+enum ProfFamily {
+    PF_SPMV = 0,      // operator / block SpMV (incl. spmv_add, residual)
+    PF_GS,            // Gauss-Seidel sweeps
+    PF_RESTRICT,      // fused residual + restriction
+    PF_PROLONG,       // prolongation
+    PF_COARSE,        // dense coarse solve
+    PF_UZAWA,         // Uzawa pressure step
+    PF_ORTHO,         // GMRES multi-dot / multi-axpy / lincomb / scale
+    PF_BICG,          // fused BiCGSTAB update + reduction kernels
+    PF_VEC,           // copies, fills, axpy, dots
+    PF_SETUP,         // setup-only kernels
+    PF_COUNT
+};
+
+// One device + one stream.  Every handle created from a context enqueues on
+// its stream, so calls through one context are ordered like the reference's
+// single-threaded calls.
+struct Context {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::atomic<int64_t> launches{0};
+    std::unique_ptr<PinnedBuf> pinned;   // status words, small host reads
+    void* cusolver = nullptr;            // lazily created cusolverDnHandle_t
+
+    // live profiler: CUDA events bracketing every launch of a family
+    struct ProfRec {
+        int family;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    bool profiling = false;
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> event_pool;
+    int64_t prof_launches[PF_COUNT] = {};
+    double prof_ms[PF_COUNT] = {};
+    double prof_bytes[PF_COUNT] = {};
+    cudaEvent_t take_event();
+    void drain_profile();  // folds recorded events into the per-family sums
+
+    explicit Context(int dev);
+    ~Context();
+    void sync() { SDG_CUDA(cudaStreamSynchronize(stream)); }
+    void count(int n = 1) { launches.fetch_add(n, std::memory_order_relaxed); }
+};
+
+// RAII: when profiling, records an event before and after the launch(es)
+// issued in its scope, tagged with the launch's algorithmic bytes.
+class ProfScope {
+public:
+    ProfScope(Context& c, int family, double bytes) : c_(c) {
+        if (!c_.profiling) return;
+        rec_.family = family;
+        rec_.bytes = bytes;
+        rec_.a = c_.take_event();
+        rec_.b = c_.take_event();
+        cudaEventRecord(rec_.a, c_.stream);
+        on_ = true;
+    }
+    ~ProfScope() {
+        if (!on_) return;
+        cudaEventRecord(rec_.b, c_.stream);
+        c_.prof.push_back(rec_);
+        if (c_.prof.size() >= 4096) c_.drain_profile();
+    }
+
+private:
+    Context& c_;
+    Context::ProfRec rec_{};
+    bool on_ = false;
+};
+
+using CtxPtr = std::shared_ptr<Context>;
+
+// Host CSR, same invariants as the reference SparseMatrix (sparse.hpp:17-46):
+// row_offsets of length n_rows+1, strictly increasing columns per row.
+struct HostCsr {
+    int n_rows = 0;
+    int n_cols = 0;
+    std::vector<int> rp{0};
+    std::vector<int> ci;
+    std::vector<double> v;
+
+    HostCsr() = default;
+    HostCsr(int r, int c) : n_rows(r), n_cols(c), rp(r + 1, 0) {}
+    int64_t nnz() const { return static_cast<int64_t>(v.size()); }
+    void check() const;  // throws SDG_EDIM on structural violations
+};
+
+// Device CSR.
+struct DevCsr {
+    int n_rows = 0;
+    int n_cols = 0;
+    int64_t nnz = 0;
+    DevBuf<int> rp;
+    DevBuf<int> ci;
+    DevBuf<double> v;
+
+    void upload(const HostCsr& h, cudaStream_t s) {
+        n_rows = h.n_rows;
+        n_cols = h.n_cols;
+        nnz = h.nnz();
+        rp.upload(h.rp, s);
+        ci.upload(h.ci, s);
+        v.upload(h.v, s);
+    }
+};
+
+}  // namespace sdg

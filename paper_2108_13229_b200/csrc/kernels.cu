@@ -1,0 +1,707 @@
+// Device kernels of the hot path.  See kernels.cuh for the contracts.
+#include "kernels.cuh"
+
+#include <algorithm>
+
+namespace sdg {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kGsThreads = 1024;
+constexpr int kMaxDotVecs = 64;
+
+inline int blocks_for(int64_t n, int threads = kThreads) {
+    int64_t b = (n + threads - 1) / threads;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, 1 << 30)));
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// Block-wide sum of NV values; result valid in thread 0.  Fixed tree ->
+// deterministic for a fixed block size.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&acc)[NV]) {
+    __shared__ double sm[NV][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = warp_sum(acc[v]);
+    if (lane == 0)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sm[v][warp] = acc[v];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            double x = lane < nwarps ? sm[v][lane] : 0.0;
+            acc[v] = warp_sum(x);
+        }
+    }
+    __syncthreads();
+}
+
+// Stores this block's NV partials; returns true in the block that arrives
+// last, after folding all partials (block order fixed) into acc (thread 0).
+template <int NV>
+__device__ bool finish_reduce(double (&acc)[NV], double* partials, unsigned* ticket) {
+    __shared__ bool am_last;
+    block_sum<NV>(acc);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) partials[blockIdx.x * NV + v] = acc[v];
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        am_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return false;
+    __threadfence();
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] += __ldcg(partials + b * NV + v);
+    block_sum<NV>(acc);
+    if (threadIdx.x == 0) *ticket = 0u;
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// sparse kernels
+
+// BITWISE: sparse.cpp:81-90 / 98-108
+__global__ void k_spmv(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                       const double* __restrict__ v, const double* __restrict__ x,
+                       const double* __restrict__ y_in, double* __restrict__ y, double alpha,
+                       int add) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double sum = 0.0;
+    const int e = rp[i + 1];
+    for (int k = rp[i]; k < e; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], x[ci[k]]));
+    y[i] = add ? __dadd_rn(y_in[i], __dmul_rn(alpha, sum)) : sum;
+}
+
+// BITWISE: precond.cpp:92-108 (sor_sweep), one CTA walking the level
+// schedule.  Lower neighbours (j < i) read the new iterate, upper ones the
+// old, in the reference's column order; the division order of
+// `(1 - omega) * z + omega * s / diag` is kept.
+__global__ void __launch_bounds__(kGsThreads)
+k_gs_levels(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+            const int* __restrict__ lvl_ptr, const int* __restrict__ lvl_rows, int n_levels,
+            const double* __restrict__ r, const double* z_old, double* z_new, double omega) {
+    for (int l = 0; l < n_levels; ++l) {
+        const int b = lvl_ptr[l], e = lvl_ptr[l + 1];
+        for (int idx = b + threadIdx.x; idx < e; idx += blockDim.x) {
+            const int i = lvl_rows[idx];
+            double s = r[i];
+            double diag = 0.0;
+            const int ke = rp[i + 1];
+            for (int k = rp[i]; k < ke; ++k) {
+                const int j = ci[k];
+                const double a = v[k];
+                if (j == i) {
+                    diag = a;
+                } else {
+                    const double zj = j < i ? z_new[j] : (z_old ? z_old[j] : 0.0);
+                    s = __dsub_rn(s, __dmul_rn(a, zj));
+                }
+            }
+            const double zi = z_old ? z_old[i] : 0.0;
+            z_new[i] = __dadd_rn(__dmul_rn(1.0 - omega, zi), __ddiv_rn(__dmul_rn(omega, s), diag));
+        }
+        __syncthreads();
+    }
+}
+
+// BITWISE: precond.cpp:241-244
+__global__ void k_resid_restrict(int n_coarse, const int* __restrict__ pt_ptr,
+                                 const int* __restrict__ pt_rows, const int* __restrict__ rp,
+                                 const int* __restrict__ ci, const double* __restrict__ v,
+                                 const double* __restrict__ r, const double* __restrict__ z,
+                                 double* __restrict__ rc) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_coarse) return;
+    double acc = 0.0;
+    const int qe = pt_ptr[c + 1];
+    for (int q = pt_ptr[c]; q < qe; ++q) {
+        const int i = pt_rows[q];
+        double sum = 0.0;
+        const int ke = rp[i + 1];
+        for (int k = rp[i]; k < ke; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], z[ci[k]]));
+        acc = __dadd_rn(acc, __dadd_rn(r[i], __dmul_rn(-1.0, sum)));
+    }
+    rc[c] = acc;
+}
+
+// BITWISE: precond.cpp:247
+__global__ void k_prolong(int n, const int* __restrict__ agg, const double* __restrict__ z,
+                          const double* __restrict__ zc, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = __dadd_rn(z[i], zc[agg[i]]);
+}
+
+// y = Ainv x, one warp per row.
+__global__ void k_dense_gemv(int n, const double* __restrict__ a, const double* __restrict__ x,
+                             double* __restrict__ y) {
+    const int warps = blockDim.x >> 5;
+    const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const double* ar = a + static_cast<size_t>(row) * n;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(__ldg(ar + j), __ldg(x + j), s);
+    s = warp_sum(s);
+    if (lane == 0) y[row] = s;
+}
+
+// BITWISE: precond.cpp:296-298
+__global__ void k_uzawa_p(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                          const double* __restrict__ v, const double* __restrict__ zv,
+                          const double* __restrict__ r_p, double omega, double* __restrict__ z_p) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double sum = 0.0;
+    const int e = rp[i + 1];
+    for (int k = rp[i]; k < e; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], zv[ci[k]]));
+    z_p[i] = __dmul_rn(omega, __dsub_rn(sum, r_p[i]));
+}
+
+__global__ void k_copy(int64_t n, double* __restrict__ d, const double* __restrict__ s) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+
+__global__ void k_fill(int64_t n, double* __restrict__ d, double val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = val;
+}
+
+__global__ void k_csr_to_dense(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                               const double* __restrict__ v, double* __restrict__ dense) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) dense[static_cast<size_t>(i) * n + ci[k]] = v[k];
+}
+
+__global__ void k_set_identity(int n, double* dense) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dense[static_cast<size_t>(i) * n + i] = 1.0;
+}
+
+// ---------------------------------------------------------------------------
+// Krylov vector kernels
+
+// Block b owns elements [b*chunk, min(n,(b+1)*chunk)); warp w dots vectors
+// w, w+8, ... of X against y over that chunk.
+__global__ void k_multidot(int64_t n, int k, const double* __restrict__ X, int64_t ldx,
+                           const double* __restrict__ y, int64_t chunk, double* partials,
+                           unsigned* ticket, double* __restrict__ out) {
+    __shared__ bool am_last;
+    __shared__ double red[kThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int64_t b0 = blockIdx.x * chunk;
+    const int64_t b1 = min(n, b0 + chunk);
+    for (int vv = warp; vv < k; vv += nwarps) {
+        const double* xv = X + vv * ldx;
+        double s = 0.0;
+        for (int64_t i = b0 + lane; i < b1; i += 32) s = fma(__ldg(xv + i), __ldg(y + i), s);
+        s = warp_sum(s);
+        if (lane == 0) partials[blockIdx.x * kMaxDotVecs + vv] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(ticket, 1u);
+        am_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    for (int vv = 0; vv < k; ++vv) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+            s += __ldcg(partials + b * kMaxDotVecs + vv);
+        s = warp_sum(s);
+        if (lane == 0) red[warp] = s;
+        __syncthreads();
+        if (warp == 0) {
+            double x = lane < nwarps ? red[lane] : 0.0;
+            x = warp_sum(x);
+            if (lane == 0) out[vv] = x;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
+}
+
+template <bool NORM>
+__global__ void k_multi_axpy(int64_t n, int k, const double* __restrict__ X, int64_t ldx,
+                             const double* __restrict__ h, double* __restrict__ w,
+                             double* partials, unsigned* ticket, double* out) {
+    __shared__ double hs[kMaxDotVecs];
+    if (threadIdx.x < k) hs[threadIdx.x] = h[threadIdx.x];
+    __syncthreads();
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double wi = w[i];
+        for (int vv = 0; vv < k; ++vv) wi = fma(-hs[vv], __ldg(X + vv * ldx + i), wi);
+        w[i] = wi;
+        if (NORM) acc[0] = fma(wi, wi, acc[0]);
+    }
+    if (NORM) {
+        if (finish_reduce<1>(acc, partials, ticket) && threadIdx.x == 0) out[0] = acc[0];
+    }
+}
+
+// BITWISE: reference `scale(vi, 1.0 / wn)` (krylov.cpp:115-117)
+__global__ void k_scale_by_inv(int64_t n, const double* __restrict__ src,
+                               const double* __restrict__ den, double* __restrict__ dst) {
+    const double d = *den;
+    if (!(d > 0.0)) return;
+    const double inv = 1.0 / d;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = __dmul_rn(src[i], inv);
+}
+
+// BITWISE: krylov.cpp:153-154 (fill + axpy loop, sequential in v)
+__global__ void k_lincomb(int64_t n, int k, const double* __restrict__ X, int64_t ldx,
+                          const double* __restrict__ y, double* __restrict__ w) {
+    __shared__ double ys[kMaxDotVecs];
+    if (threadIdx.x < k) ys[threadIdx.x] = y[threadIdx.x];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int vv = 0; vv < k; ++vv) s = __dadd_rn(s, __dmul_rn(ys[vv], X[vv * ldx + i]));
+        w[i] = s;
+    }
+}
+
+__global__ void k_add_inplace(int64_t n, double* __restrict__ x, const double* __restrict__ z) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dadd_rn(x[i], z[i]);
+}
+
+__global__ void k_axpy_dev(int64_t n, const double* __restrict__ alpha,
+                           const double* __restrict__ x, double* __restrict__ y) {
+    const double a = *alpha;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __dadd_rn(y[i], __dmul_rn(a, x[i]));
+}
+
+__global__ void k_dot(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                      double* partials, unsigned* ticket, double* out) {
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        acc[0] = fma(x[i], y[i], acc[0]);
+    if (finish_reduce<1>(acc, partials, ticket) && threadIdx.x == 0) out[0] = acc[0];
+}
+
+// BITWISE: krylov.cpp:337
+__global__ void k_div_scalar(int64_t n, const double* __restrict__ y, const double* __restrict__ yn,
+                             double* __restrict__ x) {
+    const double d = *yn;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __ddiv_rn(y[i], d);
+}
+
+// ---------------------------------------------------------------------------
+// BiCGSTAB (krylov.cpp:240-283); element updates keep the reference's
+// expression order, reductions are deterministic tree sums.
+
+__global__ void k_bi_p(int64_t n, BiState* st, const double* __restrict__ r,
+                       const double* __restrict__ v, double* __restrict__ p) {
+    if (st->flag) return;
+    const double rho_new = st->rho_new;
+    if (fabs(rho_new) < 1e-300) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->flag = BI_BREAK_RHO;
+        return;
+    }
+    const double beta = __dmul_rn(__ddiv_rn(rho_new, st->rho), __ddiv_rn(st->alpha, st->omega));
+    const double om = st->omega;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = __dadd_rn(r[i], __dmul_rn(beta, __dsub_rn(p[i], __dmul_rn(om, v[i]))));
+}
+
+__global__ void k_bi_rv(int64_t n, BiState* st, const double* __restrict__ rhat,
+                        const double* __restrict__ v, double* partials, unsigned* ticket) {
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        acc[0] = fma(rhat[i], v[i], acc[0]);
+    if (finish_reduce<1>(acc, partials, ticket) && threadIdx.x == 0) {
+        if (st->flag) return;
+        st->rv = acc[0];
+        if (fabs(acc[0]) < 1e-300)
+            st->flag = BI_BREAK_RV;
+        else
+            st->alpha = st->rho_new / acc[0];
+    }
+}
+
+__global__ void k_bi_s(int64_t n, BiState* st, const double* __restrict__ r,
+                       const double* __restrict__ v, double* __restrict__ s, double* partials,
+                       unsigned* ticket) {
+    const int flag = st->flag;  // uniform for the whole launch
+    double acc[1] = {0.0};
+    if (!flag) {
+        const double alpha = st->alpha;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const double si = __dsub_rn(r[i], __dmul_rn(alpha, v[i]));
+            s[i] = si;
+            acc[0] = fma(si, si, acc[0]);
+        }
+    }
+    if (finish_reduce<1>(acc, partials, ticket) && threadIdx.x == 0) {
+        if (flag) return;
+        st->sn = sqrt(acc[0]);
+        if (st->sn <= st->tol) st->flag = BI_S_CONV;
+    }
+}
+
+__global__ void k_bi_t(int64_t n, BiState* st, const double* __restrict__ t,
+                       const double* __restrict__ s, double* partials, unsigned* ticket) {
+    const int flag = st->flag;
+    double acc[2] = {0.0, 0.0};
+    if (!flag) {
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const double ti = t[i];
+            acc[0] = fma(ti, ti, acc[0]);
+            acc[1] = fma(ti, s[i], acc[1]);
+        }
+    }
+    if (finish_reduce<2>(acc, partials, ticket) && threadIdx.x == 0) {
+        if (flag) return;
+        st->tt = acc[0];
+        st->ts = acc[1];
+        if (acc[0] == 0.0) {
+            st->flag = BI_BREAK_TT;
+            return;
+        }
+        const double om = acc[1] / acc[0];
+        if (fabs(om) < 1e-300)
+            st->flag = BI_BREAK_OMEGA;
+        else
+            st->omega = om;
+    }
+}
+
+__global__ void k_bi_xr(int64_t n, BiState* st, const double* __restrict__ phat,
+                        const double* __restrict__ shat, const double* __restrict__ s,
+                        const double* __restrict__ t, const double* __restrict__ rhat,
+                        double* __restrict__ x, double* __restrict__ r, double* partials,
+                        unsigned* ticket) {
+    const int flag = st->flag;
+    double acc[2] = {0.0, 0.0};
+    if (!flag) {
+        const double alpha = st->alpha, om = st->omega;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            x[i] = __dadd_rn(x[i], __dadd_rn(__dmul_rn(alpha, phat[i]), __dmul_rn(om, shat[i])));
+            const double ri = __dsub_rn(s[i], __dmul_rn(om, t[i]));
+            r[i] = ri;
+            acc[0] = fma(ri, ri, acc[0]);
+            acc[1] = fma(rhat[i], ri, acc[1]);
+        }
+    }
+    if (finish_reduce<2>(acc, partials, ticket) && threadIdx.x == 0) {
+        if (flag) return;
+        st->rho = st->rho_new;
+        st->rn = sqrt(acc[0]);
+        st->rho_new = acc[1];
+    }
+}
+
+__global__ void k_bi_rho(int64_t n, BiState* st, const double* __restrict__ rhat,
+                         const double* __restrict__ r, double* partials, unsigned* ticket) {
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        acc[0] = fma(rhat[i], r[i], acc[0]);
+    if (finish_reduce<1>(acc, partials, ticket) && threadIdx.x == 0) st->rho_new = acc[0];
+}
+
+__global__ void k_bi_x_alpha(int64_t n, const BiState* st, const double* __restrict__ phat,
+                             double* __restrict__ x) {
+    const double a = st->alpha;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dadd_rn(x[i], __dmul_rn(a, phat[i]));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+
+int reduce_blocks(int n, int num_sms) {
+    const int want = (n + 4 * kThreads - 1) / (4 * kThreads);
+    return std::max(1, std::min(want, 2 * num_sms));
+}
+
+void ReduceWs::init(int blocks, int vals, cudaStream_t s) {
+    max_blocks = blocks;
+    max_vals = vals;
+    partials.resize(static_cast<size_t>(blocks) * vals);
+    ticket.resize(1);
+    SDG_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), s));
+}
+
+static inline int stride_blocks(Context& c, int64_t n) {
+    const int64_t want = (n + kThreads - 1) / kThreads;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 8LL * c.num_sms)));
+}
+
+#define SDG_LAUNCHED(ctx)                                                  \
+    do {                                                                   \
+        (ctx).count();                                                     \
+        cudaError_t e_ = cudaGetLastError();                               \
+        if (e_ != cudaSuccess) ::sdg::fail(SDG_ECUDA, cudaGetErrorString(e_)); \
+    } while (0)
+
+void launch_spmv(Context& c, const DevCsr& a, const double* x, double* y) {
+    ProfScope ps_(c, PF_SPMV, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 8.0 * a.n_rows);
+    if (a.n_rows == 0) return;
+    k_spmv<<<blocks_for(a.n_rows), kThreads, 0, c.stream>>>(a.n_rows, a.rp.get(), a.ci.get(),
+                                                            a.v.get(), x, nullptr, y, 0.0, 0);
+    SDG_LAUNCHED(c);
+}
+
+void launch_spmv_add(Context& c, const DevCsr& a, const double* x, const double* y_in,
+                     double* y_out, double alpha) {
+    ProfScope ps_(c, PF_SPMV, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 16.0 * a.n_rows);
+    if (a.n_rows == 0) return;
+    k_spmv<<<blocks_for(a.n_rows), kThreads, 0, c.stream>>>(a.n_rows, a.rp.get(), a.ci.get(),
+                                                            a.v.get(), x, y_in, y_out, alpha, 1);
+    SDG_LAUNCHED(c);
+}
+
+void launch_gs_levels(Context& c, const DevCsr& a, const int* lvl_ptr, const int* lvl_rows,
+                      int n_levels, const double* r, const double* z_old, double* z_new,
+                      double omega) {
+    ProfScope ps_(c, PF_GS, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + (z_old ? 24.0 : 16.0) * a.n_rows + 4.0 * a.n_rows + 4.0 * (n_levels + 1));
+    if (a.n_rows == 0) return;
+    k_gs_levels<<<1, kGsThreads, 0, c.stream>>>(a.rp.get(), a.ci.get(), a.v.get(), lvl_ptr,
+                                                lvl_rows, n_levels, r, z_old, z_new, omega);
+    SDG_LAUNCHED(c);
+}
+
+void launch_resid_restrict(Context& c, const DevCsr& a, const int* pt_ptr, const int* pt_rows,
+                           int n_coarse, const double* r, const double* z, double* rc) {
+    ProfScope ps_(c, PF_RESTRICT, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 16.0 * a.n_rows + 4.0 * a.n_rows + 4.0 * (n_coarse + 1) + 8.0 * n_coarse);
+    if (n_coarse == 0) return;
+    k_resid_restrict<<<blocks_for(n_coarse, 128), 128, 0, c.stream>>>(
+        n_coarse, pt_ptr, pt_rows, a.rp.get(), a.ci.get(), a.v.get(), r, z, rc);
+    SDG_LAUNCHED(c);
+}
+
+void launch_prolong(Context& c, int n, const int* agg, const double* z, const double* zc,
+                    double* out) {
+    ProfScope ps_(c, PF_PROLONG, 20.0 * n + 8.0 * n);
+    if (n == 0) return;
+    k_prolong<<<blocks_for(n), kThreads, 0, c.stream>>>(n, agg, z, zc, out);
+    SDG_LAUNCHED(c);
+}
+
+void launch_dense_gemv(Context& c, int n, const double* ainv, const double* x, double* y) {
+    ProfScope ps_(c, PF_COARSE, 8.0 * n * (double)n + 16.0 * n);
+    if (n == 0) return;
+    const int warps = kThreads / 32;
+    k_dense_gemv<<<(n + warps - 1) / warps, kThreads, 0, c.stream>>>(n, ainv, x, y);
+    SDG_LAUNCHED(c);
+}
+
+void launch_uzawa_pressure(Context& c, const DevCsr& cm, const double* z_v, const double* r_p,
+                           double omega, double* z_p) {
+    ProfScope ps_(c, PF_UZAWA, 12.0 * cm.nnz + 4.0 * (cm.n_rows + 1) + 8.0 * cm.n_cols + 16.0 * cm.n_rows);
+    if (cm.n_rows == 0) return;
+    k_uzawa_p<<<blocks_for(cm.n_rows), kThreads, 0, c.stream>>>(cm.n_rows, cm.rp.get(), cm.ci.get(),
+                                                                cm.v.get(), z_v, r_p, omega, z_p);
+    SDG_LAUNCHED(c);
+}
+
+void launch_copy(Context& c, double* dst, const double* src, int64_t n) {
+    ProfScope ps_(c, PF_VEC, 16.0 * n);
+    if (n == 0 || dst == src) return;
+    k_copy<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, dst, src);
+    SDG_LAUNCHED(c);
+}
+
+void launch_fill(Context& c, double* dst, double v, int64_t n) {
+    ProfScope ps_(c, PF_VEC, 8.0 * n);
+    if (n == 0) return;
+    k_fill<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, dst, v);
+    SDG_LAUNCHED(c);
+}
+
+void launch_csr_to_dense(Context& c, const DevCsr& a, double* dense) {
+    ProfScope ps_(c, PF_SETUP, 12.0 * a.nnz);
+    if (a.n_rows == 0) return;
+    k_csr_to_dense<<<blocks_for(a.n_rows), kThreads, 0, c.stream>>>(a.n_rows, a.rp.get(),
+                                                                    a.ci.get(), a.v.get(), dense);
+    SDG_LAUNCHED(c);
+}
+
+void launch_set_identity(Context& c, int n, double* dense) {
+    ProfScope ps_(c, PF_SETUP, 8.0 * n);
+    if (n == 0) return;
+    k_set_identity<<<blocks_for(n), kThreads, 0, c.stream>>>(n, dense);
+    SDG_LAUNCHED(c);
+}
+
+void launch_multidot(Context& c, ReduceWs& ws, int64_t n, int k, const double* X, int64_t ldx,
+                     const double* y, double* out) {
+    ProfScope ps_(c, PF_ORTHO, 8.0 * (k + 1) * (double)n);
+    if (k <= 0) return;
+    if (k > kMaxDotVecs || ws.max_vals < kMaxDotVecs) fail(SDG_EINVAL, "multidot: too many vectors");
+    int nb = reduce_blocks(static_cast<int>(std::min<int64_t>(n, 1 << 30)), c.num_sms);
+    nb = std::min(nb, ws.max_blocks);
+    const int64_t chunk = std::max<int64_t>(1, (n + nb - 1) / nb);
+    nb = static_cast<int>((n + chunk - 1) / chunk);
+    if (nb < 1) nb = 1;
+    k_multidot<<<nb, kThreads, 0, c.stream>>>(n, k, X, ldx, y, chunk, ws.partials.get(),
+                                              ws.ticket.get(), out);
+    SDG_LAUNCHED(c);
+}
+
+void launch_multi_axpy(Context& c, int64_t n, int k, const double* X, int64_t ldx,
+                       const double* h, double* w) {
+    ProfScope ps_(c, PF_ORTHO, 8.0 * (k + 2) * (double)n);
+    if (k <= 0) return;
+    k_multi_axpy<false><<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, k, X, ldx, h, w,
+                                                                       nullptr, nullptr, nullptr);
+    SDG_LAUNCHED(c);
+}
+
+void launch_multi_axpy_norm2(Context& c, ReduceWs& ws, int64_t n, int k, const double* X,
+                             int64_t ldx, const double* h, double* w, double* out) {
+    ProfScope ps_(c, PF_ORTHO, 8.0 * (k + 2) * (double)n);
+    const int nb = std::min(reduce_blocks(static_cast<int>(std::min<int64_t>(n, 1 << 30)), c.num_sms),
+                            ws.max_blocks);
+    k_multi_axpy<true><<<nb, kThreads, 0, c.stream>>>(n, k, X, ldx, h, w, ws.partials.get(),
+                                                      ws.ticket.get(), out);
+    SDG_LAUNCHED(c);
+}
+
+void launch_scale_by_inv(Context& c, int64_t n, const double* src, const double* den, double* dst) {
+    ProfScope ps_(c, PF_ORTHO, 16.0 * n);
+    k_scale_by_inv<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, src, den, dst);
+    SDG_LAUNCHED(c);
+}
+
+void launch_lincomb(Context& c, int64_t n, int k, const double* X, int64_t ldx, const double* y,
+                    double* w) {
+    ProfScope ps_(c, PF_ORTHO, 8.0 * (k + 1) * (double)n);
+    if (k > kMaxDotVecs) fail(SDG_EINVAL, "lincomb: too many vectors");
+    k_lincomb<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, k, X, ldx, y, w);
+    SDG_LAUNCHED(c);
+}
+
+void launch_add_inplace(Context& c, int64_t n, double* x, const double* z) {
+    ProfScope ps_(c, PF_VEC, 24.0 * n);
+    k_add_inplace<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, x, z);
+    SDG_LAUNCHED(c);
+}
+
+void launch_axpy_dev(Context& c, int64_t n, const double* alpha, const double* x, double* y) {
+    ProfScope ps_(c, PF_VEC, 24.0 * n);
+    k_axpy_dev<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, alpha, x, y);
+    SDG_LAUNCHED(c);
+}
+
+static inline int red_blocks(Context& c, ReduceWs& ws, int64_t n) {
+    return std::min(reduce_blocks(static_cast<int>(std::min<int64_t>(n, 1 << 30)), c.num_sms),
+                    ws.max_blocks);
+}
+
+void launch_norm2sq(Context& c, ReduceWs& ws, int64_t n, const double* x, double* out) {
+    ProfScope ps_(c, PF_VEC, 8.0 * n);
+    k_dot<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, x, x, ws.partials.get(),
+                                                           ws.ticket.get(), out);
+    SDG_LAUNCHED(c);
+}
+
+void launch_dot(Context& c, ReduceWs& ws, int64_t n, const double* x, const double* y, double* out) {
+    ProfScope ps_(c, PF_VEC, 16.0 * n);
+    k_dot<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, x, y, ws.partials.get(),
+                                                           ws.ticket.get(), out);
+    SDG_LAUNCHED(c);
+}
+
+void launch_div_scalar(Context& c, int64_t n, const double* y, const double* yn, double* x) {
+    ProfScope ps_(c, PF_VEC, 16.0 * n);
+    k_div_scalar<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, y, yn, x);
+    SDG_LAUNCHED(c);
+}
+
+void launch_bi_p(Context& c, int64_t n, BiState* st, const double* r, const double* v, double* p) {
+    ProfScope ps_(c, PF_BICG, 32.0 * n);
+    k_bi_p<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, st, r, v, p);
+    SDG_LAUNCHED(c);
+}
+
+void launch_bi_rv(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double* rhat,
+                  const double* v) {
+    ProfScope ps_(c, PF_BICG, 16.0 * n);
+    k_bi_rv<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, rhat, v, ws.partials.get(),
+                                                             ws.ticket.get());
+    SDG_LAUNCHED(c);
+}
+
+void launch_bi_s(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double* r,
+                 const double* v, double* s) {
+    ProfScope ps_(c, PF_BICG, 24.0 * n);
+    k_bi_s<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, r, v, s, ws.partials.get(),
+                                                            ws.ticket.get());
+    SDG_LAUNCHED(c);
+}
+
+void launch_bi_t(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double* t,
+                 const double* s) {
+    ProfScope ps_(c, PF_BICG, 16.0 * n);
+    k_bi_t<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, t, s, ws.partials.get(),
+                                                            ws.ticket.get());
+    SDG_LAUNCHED(c);
+}
+
+void launch_bi_xr(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double* phat,
+                  const double* shat, const double* s, const double* t, const double* rhat,
+                  double* x, double* r) {
+    ProfScope ps_(c, PF_BICG, 64.0 * n);
+    k_bi_xr<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, phat, shat, s, t, rhat, x, r,
+                                                             ws.partials.get(), ws.ticket.get());
+    SDG_LAUNCHED(c);
+}
+
+void launch_bi_rho(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double* rhat,
+                   const double* r) {
+    ProfScope ps_(c, PF_BICG, 16.0 * n);
+    k_bi_rho<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, rhat, r, ws.partials.get(),
+                                                              ws.ticket.get());
+    SDG_LAUNCHED(c);
+}
+
+void launch_bi_x_alpha(Context& c, int64_t n, BiState* st, const double* phat, double* x) {
+    ProfScope ps_(c, PF_BICG, 24.0 * n);
+    k_bi_x_alpha<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, st, phat, x);
+    SDG_LAUNCHED(c);
+}
+
+}  // namespace sdg

@@ -1,0 +1,291 @@
+// Device preconditioners: AMG V(1,1), inexact Uzawa, td_*/pv_* block
+// combinators.  Setup (aggregation, Galerkin, schedules) is host C++
+// (setup.cpp); the coarse factorization is a dense LU on the device
+// followed by an explicit inverse, so each coarse solve is one fully
+// parallel GEMV instead of two sequential triangular solves (SURVEY.md §7
+// hard part 2: at the reference's 3 levels the coarse factor is ~58% dense).
+#include <cusolverDn.h>
+
+#include <chrono>
+#include <cmath>
+#include <string>
+
+#include "power.cuh"
+#include "solver.hpp"
+
+namespace sdg {
+
+// ---------------------------------------------------------------------------
+// context / matrix
+
+Context::Context(int dev) : device(dev) {
+    SDG_CUDA(cudaSetDevice(dev));
+    SDG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    SDG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    pinned = std::make_unique<PinnedBuf>(64 * 1024);
+}
+
+Context::~Context() {
+    for (auto& r : prof) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
+    if (cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(cusolver));
+    if (stream) cudaStreamDestroy(stream);
+}
+
+cudaEvent_t Context::take_event() {
+    if (!event_pool.empty()) {
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    SDG_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void Context::drain_profile() {
+    if (prof.empty()) return;
+    SDG_CUDA(cudaStreamSynchronize(stream));
+    for (auto& r : prof) {
+        float ms = 0.f;
+        SDG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        prof_ms[r.family] += ms;
+        prof_launches[r.family] += 1;
+        prof_bytes[r.family] += r.bytes;
+        event_pool.push_back(r.a);
+        event_pool.push_back(r.b);
+    }
+    prof.clear();
+}
+
+Matrix::Matrix(CtxPtr c, HostCsr h) : ctx(std::move(c)), host(std::move(h)) {
+    host.check();
+    dev.upload(host, ctx->stream);
+}
+
+void Matrix::ensure_schedule() {
+    if (sched_ready) return;
+    if (host.n_rows != host.n_cols) fail(SDG_EDIM, "sor_sweep: matrix must be square");
+    require_diagonal(host, "sor_sweep");
+    LevelSchedule s = lower_schedule(host);
+    lvl_ptr.upload(s.lvl_ptr, ctx->stream);
+    lvl_rows.upload(s.lvl_rows, ctx->stream);
+    n_levels = s.n_levels();
+    sched_ready = true;
+}
+
+void IdentityPrecond::do_apply(const double* r, double* z) { launch_copy(*ctx_, z, r, n_); }
+
+// ---------------------------------------------------------------------------
+// AMG
+
+AmgPrecond::AmgPrecond(CtxPtr c, const HostCsr& a, const AmgOpts& o) : Precond(std::move(c)) {
+    auto t0 = std::chrono::steady_clock::now();
+    Context& cx = *ctx_;
+    std::vector<HostLevel> hl = build_hierarchy(a, o);
+    n_rows_ = a.n_rows;
+    levels_.resize(hl.size());
+    for (size_t l = 0; l < hl.size(); ++l) {
+        Level& L = levels_[l];
+        const HostCsr& A = hl[l].a;
+        L.a.upload(A, cx.stream);
+        if (l > 0) {
+            L.r.resize(A.n_rows);
+            L.z.resize(A.n_rows);
+        }
+        if (l + 1 < hl.size()) {
+            require_diagonal(A, "sor_sweep");
+            LevelSchedule s = lower_schedule(A);
+            L.lvl_ptr.upload(s.lvl_ptr, cx.stream);
+            L.lvl_rows.upload(s.lvl_rows, cx.stream);
+            L.n_sched = s.n_levels();
+            L.agg.upload(hl[l].aggregate_of, cx.stream);
+            std::vector<int> ptr, rows;
+            aggregate_transpose(hl[l].aggregate_of, hl[l].n_coarse, ptr, rows);
+            L.pt_ptr.upload(ptr, cx.stream);
+            L.pt_rows.upload(rows, cx.stream);
+            L.n_coarse = hl[l].n_coarse;
+            L.zt.resize(A.n_rows);
+        }
+    }
+    factor_coarse(hl.back().a);
+    cx.sync();
+    setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void AmgPrecond::factor_coarse(const HostCsr& coarse) {
+    Context& cx = *ctx_;
+    n_c_ = coarse.n_rows;
+    if (n_c_ == 0) return;
+    const size_t nn = static_cast<size_t>(n_c_) * n_c_;
+    DevCsr dc;
+    dc.upload(coarse, cx.stream);
+    // Row-major A is column-major A^T: factor A^T and solve A^T X = I, so X
+    // (column-major) = A^{-T}, i.e. row-major A^{-1}.
+    DevBuf<double> lu(nn);
+    coarse_inv_.resize(nn);
+    SDG_CUDA(cudaMemsetAsync(lu.get(), 0, nn * sizeof(double), cx.stream));
+    SDG_CUDA(cudaMemsetAsync(coarse_inv_.get(), 0, nn * sizeof(double), cx.stream));
+    launch_csr_to_dense(cx, dc, lu.get());
+    launch_set_identity(cx, n_c_, coarse_inv_.get());
+    if (!cx.cusolver) {
+        cusolverDnHandle_t h;
+        if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(SDG_ECUDA, "cusolverDnCreate failed");
+        cx.cusolver = h;
+    }
+    auto h = static_cast<cusolverDnHandle_t>(cx.cusolver);
+    cusolverDnSetStream(h, cx.stream);
+    int lwork = 0;
+    if (cusolverDnDgetrf_bufferSize(h, n_c_, n_c_, lu.get(), n_c_, &lwork) != CUSOLVER_STATUS_SUCCESS)
+        fail(SDG_ECUDA, "cusolverDnDgetrf_bufferSize failed");
+    DevBuf<double> work(std::max(lwork, 1));
+    DevBuf<int> ipiv(n_c_), info(1);
+    if (cusolverDnDgetrf(h, n_c_, n_c_, lu.get(), n_c_, work.get(), ipiv.get(), info.get()) !=
+        CUSOLVER_STATUS_SUCCESS)
+        fail(SDG_ECUDA, "cusolverDnDgetrf failed");
+    int hinfo = 0;
+    SDG_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, cx.stream));
+    cx.sync();
+    if (hinfo > 0)
+        fail(SDG_ESINGULAR, "lu_factor: matrix is singular, zero pivot in row " + std::to_string(hinfo - 1));
+    if (cusolverDnDgetrs(h, CUBLAS_OP_N, n_c_, n_c_, lu.get(), n_c_, ipiv.get(), coarse_inv_.get(),
+                         n_c_, info.get()) != CUSOLVER_STATUS_SUCCESS)
+        fail(SDG_ECUDA, "cusolverDnDgetrs failed");
+    cx.sync();
+}
+
+int64_t AmgPrecond::setup_memory_doubles() const {
+    int64_t s = static_cast<int64_t>(n_c_) * n_c_;
+    for (const auto& l : levels_) s += l.a.nnz;
+    return s;
+}
+
+int64_t AmgPrecond::work_per_apply() const {
+    int64_t s = static_cast<int64_t>(n_c_) * n_c_;
+    for (const auto& l : levels_) s += 5 * l.a.nnz;
+    return s;
+}
+
+void AmgPrecond::vcycle(int lev, const double* r, double* z) {
+    Context& cx = *ctx_;
+    if (lev + 1 == num_levels()) {
+        launch_dense_gemv(cx, n_c_, coarse_inv_.get(), r, z);
+        return;
+    }
+    Level& L = levels_[lev];
+    Level& C = levels_[lev + 1];
+    launch_gs_levels(cx, L.a, L.lvl_ptr.get(), L.lvl_rows.get(), L.n_sched, r, nullptr, z, 1.0);
+    launch_resid_restrict(cx, L.a, L.pt_ptr.get(), L.pt_rows.get(), L.n_coarse, r, z, C.r.get());
+    vcycle(lev + 1, C.r.get(), C.z.get());
+    launch_prolong(cx, L.a.n_rows, L.agg.get(), z, C.z.get(), L.zt.get());
+    launch_gs_levels(cx, L.a, L.lvl_ptr.get(), L.lvl_rows.get(), L.n_sched, r, L.zt.get(), z, 1.0);
+}
+
+void AmgPrecond::do_apply(const double* r, double* z) { vcycle(0, r, z); }
+
+// ---------------------------------------------------------------------------
+// Uzawa
+
+UzawaPrecond::UzawaPrecond(CtxPtr c, const HostCsr& v, const HostCsr& b, const HostCsr& cm,
+                           const AmgOpts& amg, double power_tol, int power_max, unsigned seed,
+                           double omega_override)
+    : Precond(std::move(c)), n_v_(v.n_rows), n_p_(cm.n_rows) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (v.n_rows != v.n_cols || b.n_rows != n_v_ || cm.n_cols != n_v_ || b.n_cols != cm.n_rows)
+        fail(SDG_EDIM, "uzawa: inconsistent block dimensions");
+    Context& cx = *ctx_;
+    inner_ = std::make_shared<AmgPrecond>(ctx_, v, amg);
+    b_.upload(b, cx.stream);
+    c_.upload(cm, cx.stream);
+    if (!std::isnan(omega_override)) {
+        omega_ = omega_override;
+    } else {
+        // omega = 1 / lambda_max(C Vtilde^{-1} B) (precond.cpp:274-286)
+        DevBuf<double> t1(n_v_), t2(n_v_);
+        auto schur = [&](const double* x, double* y) {
+            launch_spmv(cx, b_, x, t1.get());
+            inner_->apply(t1.get(), t2.get());
+            launch_spmv(cx, c_, t2.get(), y);
+        };
+        PowerOut est = power_iteration(cx, n_p_, schur, power_tol, power_max, seed);
+        omega_ = (std::abs(est.value) > 1e-300) ? 1.0 / est.value : 1.0;
+    }
+    cx.sync();
+    setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void UzawaPrecond::do_apply(const double* r, double* z) {
+    inner_->apply(r, z);
+    launch_uzawa_pressure(*ctx_, c_, z, r + n_v_, omega_, z + n_v_);
+}
+
+// ---------------------------------------------------------------------------
+// block combinators
+
+BlockPrecond::BlockPrecond(CtxPtr c, int kind, const HostCsr& matrix, int n_v, int n_pff,
+                           int n_ppm, PrecondPtr first, PrecondPtr pm)
+    : Precond(std::move(c)), kind_(kind), n_v_(n_v), n_pff_(n_pff), n_ppm_(n_ppm),
+      first_(std::move(first)), pm_(std::move(pm)) {
+    const int n = n_v_ + n_pff_ + n_ppm_;
+    if (matrix.n_rows != n || matrix.n_cols != n)
+        fail(SDG_EDIM, "block preconditioner: partition does not cover the matrix");
+    if (kind_ < SDG_TD_BJ || kind_ > SDG_PV_BGS) fail(SDG_EINVAL, "block preconditioner: bad kind");
+    const int n_ff = n_v_ + n_pff_;
+    const bool td = kind_ == SDG_TD_BJ || kind_ == SDG_TD_BGS;
+    const int first_rows = td ? n_ff : n_v_;
+    if (first_ && first_->rows() != first_rows)
+        fail(SDG_EDIM, "block preconditioner: first sub-block size mismatch");
+    if (pm_ && pm_->rows() != n_ppm_)
+        fail(SDG_EDIM, "block preconditioner: pm sub-block size mismatch");
+    if (!first_ || !pm_) fail(SDG_EDIM, "block preconditioner: missing sub-preconditioner");
+    Context& cx = *ctx_;
+    if (kind_ == SDG_TD_BGS) c_prime_.upload(submatrix(matrix, n_ff, n, 0, n_ff), cx.stream);
+    if (kind_ == SDG_PV_BGS) {
+        c_.upload(submatrix(matrix, n_v_, n_ff, 0, n_v_), cx.stream);
+        c1_prime_.upload(submatrix(matrix, n_ff, n, 0, n_v_), cx.stream);
+    }
+    tmp_.resize(std::max(n_ppm_, 1));
+    cx.sync();
+}
+
+int64_t BlockPrecond::setup_memory_doubles() const {
+    return first_->setup_memory_doubles() + pm_->setup_memory_doubles() + c_prime_.nnz + c_.nnz +
+           c1_prime_.nnz;
+}
+
+int64_t BlockPrecond::work_per_apply() const {
+    return first_->work_per_apply() + pm_->work_per_apply() + c_prime_.nnz + c_.nnz +
+           c1_prime_.nnz;
+}
+
+void BlockPrecond::do_apply(const double* r, double* z) {
+    Context& cx = *ctx_;
+    const int n_ff = n_v_ + n_pff_;
+    switch (kind_) {
+    case SDG_TD_BJ:
+        first_->apply(r, z);
+        pm_->apply(r + n_ff, z + n_ff);
+        break;
+    case SDG_TD_BGS:  // precond.cpp:339-345
+        first_->apply(r, z);
+        launch_spmv_add(cx, c_prime_, z, r + n_ff, tmp_.get(), -1.0);
+        pm_->apply(tmp_.get(), z + n_ff);
+        break;
+    case SDG_PV_BJ:
+        first_->apply(r, z);
+        launch_copy(cx, z + n_v_, r + n_v_, n_pff_);
+        pm_->apply(r + n_ff, z + n_ff);
+        break;
+    case SDG_PV_BGS:
+        first_->apply(r, z);
+        launch_spmv_add(cx, c_, z, r + n_v_, z + n_v_, -1.0);
+        launch_spmv_add(cx, c1_prime_, z, r + n_ff, tmp_.get(), -1.0);
+        pm_->apply(tmp_.get(), z + n_ff);
+        break;
+    }
+}
+
+}  // namespace sdg

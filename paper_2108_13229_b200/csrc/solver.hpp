@@ -1,0 +1,185 @@
+// Device-resident objects behind the C-ABI handles: matrices (the
+// LinearOperator of operator.hpp:18-28), preconditioners (the Preconditioner
+// contract of operator.hpp:34-62) and the Krylov drivers (krylov.cpp).
+#pragma once
+
+#include <atomic>
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.cuh"
+#include "setup.hpp"
+
+namespace sdg {
+
+// A device CSR plus its host copy (setup extracts blocks from it) and, on
+// demand, the Gauss-Seidel level schedule.
+struct Matrix {
+    CtxPtr ctx;
+    HostCsr host;
+    DevCsr dev;
+    // lazily built for sdg_sor_sweep
+    bool sched_ready = false;
+    DevBuf<int> lvl_ptr, lvl_rows;
+    int n_levels = 0;
+
+    Matrix(CtxPtr c, HostCsr h);
+    void ensure_schedule();
+};
+using MatrixPtr = std::shared_ptr<Matrix>;
+
+class Precond {
+public:
+    explicit Precond(CtxPtr c) : ctx_(std::move(c)) {}
+    virtual ~Precond() = default;
+    virtual int rows() const = 0;
+    // Preconditioner::apply (operator.hpp:40-43): counts, then applies on
+    // the context stream; r and z are distinct device vectors.
+    void apply(const double* r, double* z) {
+        applications_.fetch_add(1, std::memory_order_relaxed);
+        do_apply(r, z);
+    }
+    int64_t applications() const { return applications_.load(std::memory_order_relaxed); }
+    virtual int64_t setup_memory_doubles() const { return 0; }
+    virtual int64_t work_per_apply() const { return 0; }
+    virtual double omega() const { return std::nan(""); }
+    double setup_seconds = 0.0;
+    Context& ctx() const { return *ctx_; }
+    CtxPtr ctx_ptr() const { return ctx_; }
+
+protected:
+    virtual void do_apply(const double* r, double* z) = 0;
+    CtxPtr ctx_;
+
+private:
+    std::atomic<int64_t> applications_{0};
+};
+using PrecondPtr = std::shared_ptr<Precond>;
+
+class IdentityPrecond final : public Precond {
+public:
+    IdentityPrecond(CtxPtr c, int n) : Precond(std::move(c)), n_(n) {}
+    int rows() const override { return n_; }
+
+protected:
+    void do_apply(const double* r, double* z) override;
+
+private:
+    int n_;
+};
+
+// Aggregation AMG, V(1,1) (precond.hpp:101-120, precond.cpp:233-259).
+class AmgPrecond final : public Precond {
+public:
+    AmgPrecond(CtxPtr c, const HostCsr& a, const AmgOpts& o);
+    int rows() const override { return n_rows_; }
+    int64_t setup_memory_doubles() const override;
+    int64_t work_per_apply() const override;
+    int num_levels() const { return static_cast<int>(levels_.size()); }
+    int level_rows(int l) const { return levels_[l].a.n_rows; }
+    int64_t level_nnz(int l) const { return levels_[l].a.nnz; }
+
+protected:
+    void do_apply(const double* r, double* z) override;
+
+private:
+    struct Level {
+        DevCsr a;
+        DevBuf<int> lvl_ptr, lvl_rows;
+        int n_sched = 0;
+        DevBuf<int> agg;
+        DevBuf<int> pt_ptr, pt_rows;
+        int n_coarse = 0;
+        DevBuf<double> zt;      // z + P zc before post-smoothing
+        DevBuf<double> r, z;    // this level's rhs / solution (levels >= 1)
+    };
+    void vcycle(int lev, const double* r, double* z);
+    void factor_coarse(const HostCsr& coarse);
+
+    int n_rows_ = 0;
+    std::vector<Level> levels_;
+    int n_c_ = 0;
+    DevBuf<double> coarse_inv_;  // row-major inverse of the coarsest matrix
+};
+
+// Inexact Uzawa sweep (precond.cpp:264-299).
+class UzawaPrecond final : public Precond {
+public:
+    UzawaPrecond(CtxPtr c, const HostCsr& v, const HostCsr& b, const HostCsr& cm,
+                 const AmgOpts& amg, double power_tol, int power_max, unsigned seed,
+                 double omega_override);
+    int rows() const override { return n_v_ + n_p_; }
+    double omega() const override { return omega_; }
+    int64_t setup_memory_doubles() const override {
+        return inner_->setup_memory_doubles() + b_.nnz + c_.nnz;
+    }
+    int64_t work_per_apply() const override { return inner_->work_per_apply() + c_.nnz + n_p_; }
+    const AmgPrecond& inner() const { return *inner_; }
+
+protected:
+    void do_apply(const double* r, double* z) override;
+
+private:
+    int n_v_, n_p_;
+    DevCsr b_, c_;
+    std::shared_ptr<AmgPrecond> inner_;
+    double omega_ = 1.0;
+};
+
+// td_* / pv_* block combinators (precond.cpp:304-363).
+class BlockPrecond final : public Precond {
+public:
+    BlockPrecond(CtxPtr c, int kind, const HostCsr& matrix, int n_v, int n_pff, int n_ppm,
+                 PrecondPtr first, PrecondPtr pm);
+    int rows() const override { return n_v_ + n_pff_ + n_ppm_; }
+    double omega() const override { return first_->omega(); }
+    int64_t setup_memory_doubles() const override;
+    int64_t work_per_apply() const override;
+    const PrecondPtr& first() const { return first_; }
+    const PrecondPtr& pm() const { return pm_; }
+
+protected:
+    void do_apply(const double* r, double* z) override;
+
+private:
+    int kind_;
+    int n_v_, n_pff_, n_ppm_;
+    PrecondPtr first_, pm_;
+    DevCsr c_prime_, c_, c1_prime_;
+    DevBuf<double> tmp_;
+};
+
+// Krylov drivers on device vectors; host control flow mirrors krylov.cpp.
+struct SolveOut {
+    int iterations = 0;
+    bool converged = false;
+    double final_residual = 0.0;
+    std::vector<double> history;
+    double device_ms = 0.0;
+};
+
+struct Restart {
+    int m_init = 3, m_min = 3, m_step = 5, m_max = 53, current_m = 3;
+    double previous_rate = 0.0;
+    bool has_rate_sample = false;
+    double alpha_p = -3.0, alpha_d = 5.0, stall_threshold = 0.05;
+    void update(double rate);  // krylov.cpp:37-45
+};
+
+SolveOut pd_gmres(Matrix& a, Precond* p, const double* b_dev, double* x_dev, double tol_abs,
+                  int max_restarts, Restart ctrl);
+SolveOut bicgstab(Matrix& a, Precond* p, const double* b_dev, double* x_dev, double tol_abs,
+                  int max_iters);
+
+struct PowerOut {
+    double value = 0.0;
+    bool converged = false;
+    int iterations = 0;
+};
+// power_iteration (krylov.cpp:307-339) on a device operator y = op(x).
+template <class Op>
+PowerOut power_iteration(Context& c, int n, Op&& op, double tol_rel, int max_iters, unsigned seed);
+
+}  // namespace sdg

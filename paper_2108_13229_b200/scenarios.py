@@ -1,0 +1,102 @@
+"""The BASELINE.json configurations as concrete synthetic inputs.
+
+Geometry: an n x n free-flow box over the n x n porous square (the reference's
+build_grid would make the free-flow box n x 3n, grid.cpp:65).  mu = 1,
+alpha_BJ = 1; the "parabolic inflow" is the reference's pressure inflow
+p_in = inflow_pressure(t_end) = dp_max = 1 (assembly.cpp:338), which gives a
+Poiseuille-type parabolic profile.  Stationary configs use dt = +inf.
+
+The log-normal permeability of configs 2 and 4 is an extension the reference
+cannot express (scalar K, assembly.cpp:330): log10 K ~ N(0, 1) per porous
+cell from a portable generator (SplitMix64 -> Box-Muller, seed 13229), so
+both the GPU path and the CPU oracle read the same field.  Its parity is
+"unpinned": the assembly reduces bitwise to the reference when K
+is uniform, and the solver parity is checked on the extended matrix itself.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+K_SEED = 13229
+_MASK = (1 << 64) - 1
+
+
+def splitmix64(seed: int, count: int) -> np.ndarray:
+    """SplitMix64 stream (Steele, Lea, Flood 2014) as uint64."""
+    with np.errstate(over="ignore"):
+        idx = np.arange(1, count + 1, dtype=np.uint64)
+        z = (np.uint64(seed & _MASK) + idx * np.uint64(0x9E3779B97F4A7C15))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def standard_normals(seed: int, count: int) -> np.ndarray:
+    """Box-Muller on pairs of 53-bit uniforms from SplitMix64."""
+    m = (count + 1) // 2
+    u = (splitmix64(seed, 2 * m) >> np.uint64(11)).astype(np.float64) * (1.0 / (1 << 53))
+    u1, u2 = u[0::2], u[1::2]
+    rad = np.sqrt(-2.0 * np.log1p(-u1))  # 1 - u1 in (0, 1]
+    th = 2.0 * math.pi * u2
+    g = np.empty(2 * m)
+    g[0::2] = rad * np.cos(th)
+    g[1::2] = rad * np.sin(th)
+    return g[:count]
+
+
+def lognormal_k(n: int, seed: int = K_SEED, k_mean: float = 1.0, sigma_log10: float = 1.0) -> np.ndarray:
+    """Per-cell porous permeability, row-major (j*n + i), log10 K ~ N(log10 k_mean, sigma^2)."""
+    g = standard_normals(seed, n * n)
+    return k_mean * np.power(10.0, sigma_log10 * g)
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    n: int
+    permeability: float
+    lognormal: bool
+    solver: str            # "gmres50" | "pdgmres" | "bicgstab"
+    v_max_levels: int
+    d_max_levels: int
+    dt: float = float("inf")
+    steps: int = 1
+    description: str = ""
+
+    @property
+    def dof(self) -> int:
+        return 2 * self.n * (self.n + 1) + 2 * self.n * self.n
+
+    def k_field(self) -> Optional[np.ndarray]:
+        return lognormal_k(self.n) if self.lognormal else None
+
+
+CONFIGS = {
+    "c1": Config("c1", 50, 1.0, False, "gmres50", 3, 3,
+                 description="50x50 per subdomain (10,100 DoF), K=1, block-preconditioned GMRES"),
+    "c2": Config("c2", 160, 1.0, True, "bicgstab", 3, 3,
+                 description="160x160 per subdomain (102,720 DoF), log-normal K, BiCGSTAB + td_bgs, 1 GPU"),
+    "c2u": Config("c2u", 160, 1.0, False, "bicgstab", 3, 3,
+                  description="c2 shape with uniform K=1 (the parity-pinned sub-case)"),
+    "c3": Config("c3", 500, 1e-2, False, "gmres50", 3, 3,
+                 description="500x500 per subdomain (1,001,000 DoF), K=1e-2, GMRES(50)"),
+    "c4": Config("c4", 1000, 1.0, True, "gmres50", 4, 4, dt=0.1, steps=10,
+                 description="1000x1000 per subdomain (4,002,000 DoF), implicit Euler x10, log-normal K"),
+}
+
+
+def scenario(cfg: Config, t: Optional[float] = None):
+    from .sdc import ScenarioConfig
+    return ScenarioConfig(cells_per_unit_square=cfg.n, permeability=cfg.permeability, alpha_bj=1.0,
+                          kinematic_viscosity=1.0, density=1.0, dt=cfg.dt,
+                          t_end=1.0 if not math.isfinite(cfg.dt) else cfg.dt * cfg.steps, dp_max=1.0)
+
+
+def build_system(cfg: Config, t: Optional[float] = None, v_prev=None):
+    from .sdc import assemble_monolithic
+    return assemble_monolithic(scenario(cfg), t=t, v_prev=v_prev, k_cell=cfg.k_field())
