@@ -126,8 +126,9 @@ int64_t sdg_context_launches(sdg_context* ctx);
  * events on the context stream and tagged with its algorithmic bytes
  * (SURVEY.md §8(d) byte model); sdg_context_profile folds them per kernel
  * family.  Enabling clears previous totals.  Families: 0 spmv, 1 gs,
- * 2 restrict, 3 prolong, 4 coarse, 5 uzawa, 6 ortho, 7 bicg, 8 vec, 9 setup. */
-#define SDG_PROF_FAMILIES 10
+ * 2 restrict, 3 prolong, 4 coarse, 5 uzawa, 6 ortho, 7 bicg, 8 vec, 9 setup,
+ * 10 gsprep. */
+#define SDG_PROF_FAMILIES 11
 int sdg_context_set_profiling(sdg_context* ctx, int enable);
 int sdg_context_profile(sdg_context* ctx, int family, int64_t* launches, double* total_ms,
                         double* total_bytes);

@@ -107,6 +107,7 @@ enum ProfFamily {
     PF_BICG,          // fused BiCGSTAB update + reduction kernels
     PF_VEC,           // copies, fills, axpy, dots
     PF_SETUP,         // setup-only kernels
+    PF_GSPREP,        // smoother prep (upper part, fused prolongation)
     PF_COUNT
 };
 

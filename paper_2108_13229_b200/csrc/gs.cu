@@ -1,0 +1,752 @@
+// Fast Gauss-Seidel smoother: plan (host) + prep / lower / restrict kernels.
+// See gs.cuh for the algorithm; this file holds the data layout and kernels.
+//
+// Bands and clusters.  The rows are cut into B bands (B = cluster size, one
+// CTA per band, B <= 8).  Every row's band is its component-relative height
+// (row rank inside its label) raised to the largest band of any of its lower
+// dependencies, so dependencies only ever point to the same or an earlier
+// band.  Values a later band needs are pushed into its shared-memory halo
+// with DSMEM st.async stores that complete single-use "packet" mbarriers
+// there (one packet per upstream band level); a band waits for a packet
+// before the first level that reads it.
+//
+// Packed layout (per band level, contiguous, 16-byte aligned):
+//   [nS small records of 48 B][nL large records of 112 B][nE exports of 16 B]
+// small record (rows with <= 2 lower entries):
+//   { double b; int rowid; int wpos; double val[2]; int src[2]; int pad[2] }
+// large record (rows with 3..8 lower entries):
+//   { double b; int rowid; int wpos; double val[8]; int src[8] }
+// export entry (a value of the PREVIOUS level needed downstream):
+//   { int local ring slot; int destination band | packet << 8; int destination halo index; int pad }
+// b = (r - U z_old)_i / d_i (written by the prep kernels), val = a_ij / d_i,
+// src = slot in [z ring | zero slot | halo], or -(j+1) for the rare in-band
+// dependency older than the ring (read back from global z_new).  48 and 112
+// are odd multiples of 16 bytes, so 16-byte shared loads of consecutive
+// records are bank-conflict free.
+#include "gs.cuh"
+
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+
+namespace cg = cooperative_groups;
+
+namespace sdg {
+
+namespace {
+
+constexpr int kMaxSmem = 227 * 1024;
+constexpr int kSmallBytes = 48;
+constexpr int kLargeBytes = 112;
+constexpr int kExportBytes = 16;
+constexpr int kMaxLower = 8;
+
+__host__ __device__ inline int pad16(int64_t b) { return static_cast<int>((b + 15) / 16 * 16); }
+
+// ---- small PTX helpers (mbarrier, TMA bulk copy, cluster memory) -------------
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// shared::cluster address of `p` (a shared variable of this CTA) in CTA `rank`
+__device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
+    unsigned out;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_addr(p)), "r"(rank));
+    return out;
+}
+
+// asynchronous remote store whose bytes complete a transaction count on an
+// mbarrier in the destination CTA: the DSMEM push needs no fences
+__device__ __forceinline__ void st_async_f64(unsigned addr, double v, unsigned mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr),
+                 "d"(v), "r"(mbar)
+                 : "memory");
+}
+
+// ---- prep kernels ----------------------------------------------------------
+
+__global__ void k_gs_prep_pre(int n, const double* __restrict__ r, const double* __restrict__ dinv,
+                              const int* __restrict__ bidx, double* __restrict__ packed) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) packed[bidx[i]] = r[i] * dinv[i];
+}
+
+__global__ void k_gs_prep_post(int n, const int* __restrict__ urp, const int* __restrict__ uci,
+                               const double* __restrict__ uv, const double* __restrict__ r,
+                               const double* __restrict__ z, const double* __restrict__ zc,
+                               const int* __restrict__ agg, const double* __restrict__ dinv,
+                               const int* __restrict__ bidx, double* __restrict__ packed) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = r[i];
+    const int e = urp[i + 1];
+    if (zc) {
+        for (int k = urp[i]; k < e; ++k) {
+            const int j = uci[k];
+            s = fma(-uv[k], z[j] + zc[agg[j]], s);
+        }
+    } else if (z) {
+        for (int k = urp[i]; k < e; ++k) s = fma(-uv[k], z[uci[k]], s);
+    }
+    packed[bidx[i]] = s * dinv[i];
+}
+
+// ---- the lower solve -------------------------------------------------------
+
+// Load row t of a level segment into registers.  Small records fill the
+// unused entries with the zero slot, so every row can use the same formula.
+__device__ __forceinline__ bool load_row(const unsigned char* seg, int nS, int nL, int t, int zero_slot,
+                                         double& b, int& rowid, int& wpos, double (&v)[kMaxLower],
+                                         int (&sr)[kMaxLower]) {
+    if (t >= nS + nL) return false;
+    if (t < nS) {
+        const unsigned char* q = seg + static_cast<size_t>(t) * kSmallBytes;
+        const int4 h = *reinterpret_cast<const int4*>(q);
+        const double2 vv = *reinterpret_cast<const double2*>(q + 16);
+        const int4 ss = *reinterpret_cast<const int4*>(q + 32);
+        b = __hiloint2double(h.y, h.x);
+        rowid = h.z;
+        wpos = h.w;
+        v[0] = vv.x;
+        v[1] = vv.y;
+        sr[0] = ss.x;
+        sr[1] = ss.y;
+#pragma unroll
+        for (int k = 2; k < kMaxLower; ++k) {
+            v[k] = 0.0;
+            sr[k] = zero_slot;
+        }
+    } else {
+        const unsigned char* q = seg + static_cast<size_t>(nS) * kSmallBytes +
+                                 static_cast<size_t>(t - nS) * kLargeBytes;
+        const int4 h = *reinterpret_cast<const int4*>(q);
+        b = __hiloint2double(h.y, h.x);
+        rowid = h.z;
+        wpos = h.w;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 vv = *reinterpret_cast<const double2*>(q + 16 + 16 * k);
+            v[2 * k] = vv.x;
+            v[2 * k + 1] = vv.y;
+        }
+        const int4 s0 = *reinterpret_cast<const int4*>(q + 80);
+        const int4 s1 = *reinterpret_cast<const int4*>(q + 96);
+        sr[0] = s0.x; sr[1] = s0.y; sr[2] = s0.z; sr[3] = s0.w;
+        sr[4] = s1.x; sr[5] = s1.y; sr[6] = s1.z; sr[7] = s1.w;
+    }
+    return true;
+}
+
+template <bool GLOBAL>
+__device__ __forceinline__ double zref(const double* zring, const double* z_new, int s) {
+    if (GLOBAL) return s >= 0 ? zring[s] : __ldcg(z_new - s - 1);
+    return zring[s];
+}
+
+// z_i = b_i - sum_k v_k z_{src_k}; TWO: the level has only small rows.
+template <bool GLOBAL, bool TWO>
+__device__ __forceinline__ void solve_row(double b, int rowid, int wpos, const double (&v)[kMaxLower],
+                                          const int (&sr)[kMaxLower], double* zring, double* z_new) {
+    double acc;
+    if (TWO) {
+        acc = b - fma(v[1], zref<GLOBAL>(zring, z_new, sr[1]), v[0] * zref<GLOBAL>(zring, z_new, sr[0]));
+    } else {
+        double p[kMaxLower];
+#pragma unroll
+        for (int k = 0; k < kMaxLower; ++k) p[k] = v[k] * zref<GLOBAL>(zring, z_new, sr[k]);
+        acc = b - (((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7])));
+    }
+    zring[wpos] = acc;
+    z_new[rowid] = acc;
+}
+
+// One CTA per band, the bands forming one thread-block cluster.  Shared
+// memory: [D segment mbarriers | meta + req_ptr of the band | packet
+// mbarriers | z ring, zero slot, halo | D segment slots].  Warp 0 lane 0 is
+// the producer (TMA issue D levels ahead, packet waits); warps 1.. are
+// consumers, one row each per level (wider levels loop), with the next
+// level's row pulled into registers before the level barrier.
+__global__ void __launch_bounds__(512, 1)
+k_gs_cluster(const int4* __restrict__ meta_g, const int4* __restrict__ band_info,
+             const int* __restrict__ req_ptr_g, const int* __restrict__ req,
+             const int* __restrict__ packet_bytes, const double* __restrict__ packed, int ring,
+             int halo, int depth, int max_seg, int meta_bytes, int pbar_bytes, double* z_new) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int band = static_cast<int>(cluster.block_rank());
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+    int4* meta = reinterpret_cast<int4*>(sm + 128);
+    int* reqp = reinterpret_cast<int*>(sm + 128 + meta_bytes);
+    uint64_t* pbars = reinterpret_cast<uint64_t*>(sm + 128 + 2 * meta_bytes);
+    double* zring = reinterpret_cast<double*>(sm + 128 + 2 * meta_bytes + pbar_bytes);
+    const int zero_slot = ring;
+    const int zbytes = pad16(static_cast<int64_t>(ring + 1 + halo) * 8);
+    unsigned char* slots = sm + 128 + 2 * meta_bytes + pbar_bytes + zbytes;
+    const int tid = threadIdx.x;
+    const int ct = tid - 32;
+    const int ncons = blockDim.x - 32;
+
+    const int4 bi = band_info[band];  // {meta base, n levels, packet base, n packets}
+    const int mbase = bi.x, n_levels = bi.y;
+    for (int l = tid; l < n_levels; l += blockDim.x) meta[l] = meta_g[mbase + l];
+    for (int l = tid; l <= n_levels; l += blockDim.x) reqp[l] = req_ptr_g[mbase + l];
+    for (int q = tid; q < bi.w; q += blockDim.x) {
+        mbar_init(&pbars[q], 1);
+        mbar_expect_tx(&pbars[q], static_cast<unsigned>(packet_bytes[bi.z + q]));
+    }
+    if (tid == 0) {
+        for (int s = 0; s < depth; ++s) mbar_init(&bars[s], 1);
+        zring[zero_slot] = 0.0;  // zero slot for padded entries
+    }
+    fence_mbar_init();
+    cluster.sync();  // every packet barrier is armed before any remote store
+
+    const unsigned char* gbase = reinterpret_cast<const unsigned char*>(packed);
+    int issue_slot = 0, wait_slot = 0;
+    unsigned wait_parity = 0;
+    auto issue = [&](int L) {
+        const int4 m = meta[L];
+        const unsigned bytes = static_cast<unsigned>(m.y) * 16u;
+        mbar_expect_tx(&bars[issue_slot], bytes);
+        if (bytes)
+            tma_load_1d(slots + static_cast<size_t>(issue_slot) * max_seg,
+                        gbase + static_cast<size_t>(m.x) * 16, bytes, &bars[issue_slot]);
+        issue_slot = issue_slot + 1 == depth ? 0 : issue_slot + 1;
+    };
+    auto wait_next = [&]() {
+        mbar_wait(&bars[wait_slot], wait_parity);
+        if (++wait_slot == depth) {
+            wait_slot = 0;
+            wait_parity ^= 1u;
+        }
+    };
+    // the packets this level imports must have landed
+    auto satisfy = [&](int L) {
+        for (int q = reqp[L]; q < reqp[L + 1]; ++q) mbar_wait(&pbars[req[q]], 0);
+    };
+    if (tid == 0) {
+        for (int L = 0; L < depth && L < n_levels; ++L) issue(L);
+        if (n_levels > 0) {
+            wait_next();
+            satisfy(0);
+        }
+        if (n_levels > 1) wait_next();
+    }
+    __syncthreads();
+
+    double rb = 0.0, v[kMaxLower];
+    int rowid = 0, wpos = 0, sr[kMaxLower];
+    int cur_slot = 0;
+    bool live = false;
+    if (ct >= 0 && n_levels > 0) {
+        const int4 m0 = meta[0];
+        live = load_row(slots, m0.z & 0x7fffffff, m0.w & 0xffff, ct, zero_slot, rb, rowid, wpos, v, sr);
+    }
+
+    for (int L = 0; L < n_levels; ++L) {
+        const int next_slot = cur_slot + 1 == depth ? 0 : cur_slot + 1;
+        if (ct >= 0) {
+            const int4 m = meta[L];
+            const int nS = m.z & 0x7fffffff, nL = m.w & 0xffff, nE = m.w >> 16;
+            const unsigned char* seg = slots + static_cast<size_t>(cur_slot) * max_seg;
+            // exports of the previous level (its values are in the ring)
+            for (int e = ct; e < nE; e += ncons) {
+                const int4 x = *reinterpret_cast<const int4*>(seg + static_cast<size_t>(nS) * kSmallBytes +
+                                                              static_cast<size_t>(nL) * kLargeBytes +
+                                                              static_cast<size_t>(e) * kExportBytes);
+                const unsigned dst = static_cast<unsigned>(x.y) & 0xffu;
+                const unsigned pkt = static_cast<unsigned>(x.y) >> 8;
+                st_async_f64(cluster_addr(zring + zero_slot + 1 + x.z, dst), zring[x.x],
+                             cluster_addr(&pbars[pkt], dst));
+            }
+            if (live) {
+                if (m.z < 0)
+                    solve_row<true, false>(rb, rowid, wpos, v, sr, zring, z_new);
+                else if (nL == 0)
+                    solve_row<false, true>(rb, rowid, wpos, v, sr, zring, z_new);
+                else
+                    solve_row<false, false>(rb, rowid, wpos, v, sr, zring, z_new);
+            }
+            if (nS + nL > ncons) {  // wider than the block
+                for (int t = ct + ncons; t < nS + nL; t += ncons) {
+                    double eb, ev[kMaxLower];
+                    int er, ew, es[kMaxLower];
+                    load_row(seg, nS, nL, t, zero_slot, eb, er, ew, ev, es);
+                    solve_row<true, false>(eb, er, ew, ev, es, zring, z_new);
+                }
+            }
+            if (L + 1 < n_levels) {
+                const int4 mn = meta[L + 1];
+                live = load_row(slots + static_cast<size_t>(next_slot) * max_seg, mn.z & 0x7fffffff,
+                                mn.w & 0xffff, ct, zero_slot, rb, rowid, wpos, v, sr);
+            }
+        } else if (tid == 0) {
+            if (L + 2 < n_levels) wait_next();
+            if (L + 1 < n_levels) satisfy(L + 1);
+        }
+        __syncthreads();
+        if (tid == 0 && L + depth < n_levels) {
+            fence_proxy_async();
+            issue(L + depth);
+        }
+        cur_slot = next_slot;
+    }
+    cluster.sync();  // no CTA leaves while others may still write into it
+}
+
+__device__ __forceinline__ double warp_shfl(double x, int src) {
+    return __shfl_sync(0xffffffffu, x, src);
+}
+
+// BITWISE with precond.cpp:241-244: one warp per aggregate, lanes compute the
+// fine residuals, lane 0 accumulates them in ascending fine-row order.
+__global__ void k_restrict_warp(int n_coarse, const int* __restrict__ pt_ptr,
+                                const int* __restrict__ pt_rows, const int* __restrict__ rp,
+                                const int* __restrict__ ci, const double* __restrict__ v,
+                                const double* __restrict__ r, const double* __restrict__ z,
+                                double* __restrict__ rc, const double* __restrict__ next_dinv,
+                                const int* __restrict__ next_bidx, double* __restrict__ next_packed) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n_coarse) return;
+    const int q0 = pt_ptr[warp], q1 = pt_ptr[warp + 1];
+    double acc = 0.0;
+    for (int base = q0; base < q1; base += 32) {
+        double res = 0.0;
+        if (base + lane < q1) {
+            const int i = pt_rows[base + lane];
+            double sum = 0.0;
+            const int ke = rp[i + 1];
+            for (int k = rp[i]; k < ke; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], z[ci[k]]));
+            res = __dadd_rn(r[i], __dmul_rn(-1.0, sum));
+        }
+        const int cnt = min(32, q1 - base);
+        for (int k = 0; k < cnt; ++k) {
+            const double x = warp_shfl(res, k);
+            acc = __dadd_rn(acc, x);
+        }
+    }
+    if (lane == 0) {
+        rc[warp] = acc;
+        if (next_packed) next_packed[next_bidx[warp]] = acc * next_dinv[warp];
+    }
+}
+
+int smem_budget() {
+    int dev = 0, optin = 0;
+    SDG_CUDA(cudaGetDevice(&dev));
+    SDG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    SDG_CUDA(cudaFuncGetAttributes(&fa, k_gs_cluster));
+    return std::min(kMaxSmem, optin - static_cast<int>(fa.sharedSizeBytes) - 1024);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// plan
+
+void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t s, int bands_hint) {
+    n = a.n_rows;
+    std::vector<double> dinv_h(n);
+    std::vector<int> nlow(n, 0);
+    HostCsr up(n, n);
+    int max_k = 0;
+    for (int i = 0; i < n; ++i) {
+        double d = 0.0;
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k) {
+            if (a.ci[k] == i) d = a.v[k];
+            if (a.ci[k] < i) ++nlow[i];
+            if (a.ci[k] > i) {
+                up.ci.push_back(a.ci[k]);
+                up.v.push_back(a.v[k]);
+            }
+        }
+        dinv_h[i] = 1.0 / d;
+        up.rp[i + 1] = static_cast<int>(up.ci.size());
+        max_k = std::max(max_k, nlow[i]);
+    }
+
+    // ---- bands: one for small systems, more once a single SM's bandwidth
+    // becomes the bound (SDG_GS_BANDS overrides) -----------------------------
+    const int global_depth = lower_schedule(a).n_levels();
+    int nb = bands_hint > 0 ? bands_hint : (n >= 200000 ? 8 : n >= 80000 ? 4 : 1);
+    if (const char* e = std::getenv("SDG_GS_BANDS")) nb = std::max(1, std::atoi(e));
+    nb = std::max(1, std::min({nb, 8, std::max(1, n / 256)}));
+    std::vector<int> rank_in_comp(n), comp_size;
+    for (int i = 0; i < n; ++i) {
+        const int c = comps.empty() ? 0 : comps[i];
+        if (c >= static_cast<int>(comp_size.size())) comp_size.resize(c + 1, 0);
+        rank_in_comp[i] = comp_size[c]++;
+    }
+    std::vector<int> band_of(n);
+    for (int i = 0; i < n; ++i) {
+        const int c = comps.empty() ? 0 : comps[i];
+        int b = static_cast<int>(static_cast<int64_t>(rank_in_comp[i]) * nb / std::max(1, comp_size[c]));
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+            if (a.ci[k] < i) b = std::max(b, band_of[a.ci[k]]);
+        band_of[i] = b;
+    }
+    bands = nb;
+
+    // ---- band-local level schedules --------------------------------------
+    std::vector<int> lev(n, 0), nlev(nb, 0);
+    for (int i = 0; i < n; ++i) {
+        int d = 0;
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k) {
+            const int j = a.ci[k];
+            if (j < i && band_of[j] == band_of[i]) d = std::max(d, lev[j] + 1);
+        }
+        lev[i] = d;
+        nlev[band_of[i]] = std::max(nlev[band_of[i]], d + 1);
+    }
+    // a band that exports gets one extra (row-less) level for its last exports
+    std::vector<int> blev(nb);
+    for (int b = 0; b < nb; ++b) blev[b] = nlev[b] + (nb > 1 ? 1 : 0);
+    std::vector<int> lbase(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) lbase[b + 1] = lbase[b] + blev[b];
+    n_levels = lbase[nb];
+    max_band_levels = *std::max_element(blev.begin(), blev.end());
+
+    std::vector<int> nS_of(n_levels, 0), nr_of(n_levels, 0);
+    for (int i = 0; i < n; ++i) {
+        const int q = lbase[band_of[i]] + lev[i];
+        ++nr_of[q];
+        if (nlow[i] <= 2) ++nS_of[q];
+    }
+    std::vector<int> lptr(n_levels + 1, 0);
+    for (int q = 0; q < n_levels; ++q) lptr[q + 1] = lptr[q] + nr_of[q];
+    std::vector<int> order(n), fillS(n_levels), fillL(n_levels);
+    for (int q = 0; q < n_levels; ++q) {
+        fillS[q] = lptr[q];
+        fillL[q] = lptr[q] + nS_of[q];
+    }
+    for (int i = 0; i < n; ++i) {
+        const int q = lbase[band_of[i]] + lev[i];
+        order[nlow[i] <= 2 ? fillS[q]++ : fillL[q]++] = i;
+    }
+    std::vector<int> pos(n);  // band-local position in level order
+    for (int b = 0; b < nb; ++b)
+        for (int p = lptr[lbase[b]]; p < lptr[lbase[b + 1]]; ++p) pos[order[p]] = p - lptr[lbase[b]];
+
+    // ---- halo imports, packets, exports, requirements ------------------------
+    // A packet = the values band b imports from one level of one upstream
+    // band; it completes a single-use mbarrier in band b.
+    std::vector<std::vector<std::pair<int, int>>> imports(nb);  // (row j, halo index)
+    std::vector<int> halo_n(nb, 0);
+    std::vector<std::vector<int4>> exports(n_levels);  // keyed by the level that executes them
+    std::vector<int> req_ptr_h(n_levels + 1, 0);
+    std::vector<int> req_h;
+    std::vector<int> pkt_base(nb + 1, 0);
+    std::vector<int> pkt_bytes_h;
+    {
+        std::vector<int> halo_band(n, -1);
+        cross_refs = 0;
+        for (int b = 0; b < nb; ++b) {
+            pkt_base[b] = static_cast<int>(pkt_bytes_h.size());
+            std::map<std::pair<int, int>, int> pkt_of;  // (upstream band, its level) -> packet
+            std::vector<char> waited;
+            for (int L = 0; L < blev[b]; ++L) {
+                const int q = lbase[b] + L;
+                for (int p = lptr[q]; p < lptr[q + 1]; ++p) {
+                    const int i = order[p];
+                    for (int k = a.rp[i]; k < a.rp[i + 1]; ++k) {
+                        const int j = a.ci[k];
+                        if (j >= i || band_of[j] == b) continue;
+                        ++cross_refs;
+                        const int bj = band_of[j];
+                        const auto key = std::make_pair(bj, lev[j]);
+                        auto it = pkt_of.find(key);
+                        if (it == pkt_of.end()) {
+                            it = pkt_of.emplace(key, static_cast<int>(pkt_bytes_h.size()) - pkt_base[b]).first;
+                            pkt_bytes_h.push_back(0);
+                            waited.push_back(0);
+                        }
+                        const int pk = it->second;
+                        if (halo_band[j] != b) {  // first import of j into band b
+                            halo_band[j] = b;
+                            const int h = halo_n[b]++;
+                            imports[b].push_back({j, h});
+                            pkt_bytes_h[pkt_base[b] + pk] += 8;
+                            // exported by band bj while it walks level lev[j] + 1
+                            exports[lbase[bj] + lev[j] + 1].push_back(make_int4(0, b | (pk << 8), h, j));
+                        }
+                        if (!waited[pk]) {  // the first level that reads a packet waits for it
+                            waited[pk] = 1;
+                            req_h.push_back(pk);
+                        }
+                    }
+                }
+                req_ptr_h[q + 1] = static_cast<int>(req_h.size());
+            }
+        }
+        pkt_base[nb] = static_cast<int>(pkt_bytes_h.size());
+    }
+    halo = std::max(1, *std::max_element(halo_n.begin(), halo_n.end()));
+    max_packets = 1;
+    for (int b = 0; b < nb; ++b) max_packets = std::max(max_packets, pkt_base[b + 1] - pkt_base[b]);
+
+    // ---- segments ---------------------------------------------------------
+    std::vector<int4> mh(n_levels);
+    int64_t off = 0;
+    int max_rows = 1, max_exp = 0;
+    max_seg = 16;
+    for (int q = 0; q < n_levels; ++q) {
+        const int nS = nS_of[q], nL = nr_of[q] - nS_of[q], nE = static_cast<int>(exports[q].size());
+        if (nL > 0xffff || nE > 0x7fff) fail(SDG_EINVAL, "gs plan: level too wide");
+        const int bytes = nS * kSmallBytes + nL * kLargeBytes + nE * kExportBytes;
+        mh[q] = make_int4(static_cast<int>(off / 16), bytes / 16, nS, nL | (nE << 16));
+        off += bytes;
+        max_seg = std::max(max_seg, bytes);
+        max_rows = std::max(max_rows, nr_of[q]);
+        max_exp = std::max(max_exp, nE);
+    }
+    if (off / 8 + 2 > (static_cast<int64_t>(1) << 31)) fail(SDG_EINVAL, "gs plan: packed buffer too large");
+
+    int max_dist = 2;      // in-band dependency distance in level-order positions
+    int max_exp_dist = 2;  // exports read the ring one level after the value was written
+    for (int b = 0; b < nb; ++b)
+        for (int q = lbase[b]; q < lbase[b + 1]; ++q) {
+            const int band_end = lptr[q + 1] - lptr[lbase[b]];
+            for (int p = lptr[q]; p < lptr[q + 1]; ++p) {
+                const int i = order[p];
+                for (int k = a.rp[i]; k < a.rp[i + 1]; ++k) {
+                    const int j = a.ci[k];
+                    if (j < i && band_of[j] == b) max_dist = std::max(max_dist, band_end - pos[j]);
+                }
+                if (q + 1 < lbase[b + 1])
+                    max_exp_dist = std::max(max_exp_dist, lptr[q + 2] - lptr[lbase[b]] - pos[i]);
+            }
+        }
+
+    const int budget = smem_budget();
+    const int meta_bytes = pad16(static_cast<int64_t>(max_band_levels + 1) * 16);
+    const int pbar_bytes = pad16(static_cast<int64_t>(max_packets) * 8);
+    // z ring: large enough for every in-band dependency when six segment
+    // slots still fit, else the largest power of two that does
+    const int ring_room = (budget - 128 - 2 * meta_bytes - pbar_bytes - (halo + 2) * 8 - 16 - 6 * max_seg) / 8;
+    int min_ring = 64;
+    while (min_ring < max_exp_dist) min_ring <<= 1;  // exports must find their values
+    ring = 1;
+    while (ring < max_dist && ring < 32768) ring <<= 1;
+    while (ring > min_ring && ring > ring_room) ring >>= 1;
+    ring = std::max(ring, min_ring);
+
+    std::vector<double> pk(static_cast<size_t>(off / 8 + 2), 0.0);
+    unsigned char* base = reinterpret_cast<unsigned char*>(pk.data());
+    std::vector<int> bidx_h(n);
+    global_refs = 0;
+    lower_entries = 0;
+    std::vector<int> halo_lookup(n, -1);
+    for (int b = 0; b < nb; ++b) {
+        for (auto& jh : imports[b]) halo_lookup[jh.first] = jh.second;
+        for (int L = 0; L < blev[b]; ++L) {
+            const int q = lbase[b] + L;
+            int4& m = mh[q];
+            const int band_end = lptr[q + 1] - lptr[lbase[b]];
+            const int nS = m.z, nL = m.w & 0xffff;
+            for (int p = lptr[q]; p < lptr[q + 1]; ++p) {
+                const int t = p - lptr[q];
+                const int i = order[p];
+                const bool small = t < nS;
+                unsigned char* rec = base + static_cast<size_t>(m.x) * 16 +
+                                     (small ? static_cast<size_t>(t) * kSmallBytes
+                                            : static_cast<size_t>(nS) * kSmallBytes +
+                                                  static_cast<size_t>(t - nS) * kLargeBytes);
+                double* recd = reinterpret_cast<double*>(rec);
+                int* reci = reinterpret_cast<int*>(rec);
+                bidx_h[i] = static_cast<int>((rec - base) / 8);
+                reci[2] = i;                      // rowid
+                reci[3] = pos[i] & (ring - 1);    // wpos
+                const int kcap = small ? 2 : kMaxLower;
+                double* val = recd + 2;
+                int* src = reci + (small ? 8 : 20);
+                int k2 = 0;
+                for (int k = a.rp[i]; k < a.rp[i + 1] && k2 < kcap; ++k) {
+                    const int j = a.ci[k];
+                    if (j >= i) continue;
+                    val[k2] = a.v[k] * dinv_h[i];
+                    if (band_of[j] != b) {
+                        src[k2] = ring + 1 + halo_lookup[j];
+                    } else if (band_end - pos[j] <= ring) {
+                        src[k2] = pos[j] & (ring - 1);
+                    } else {
+                        src[k2] = -(j + 1);
+                        ++global_refs;
+                        m.z |= static_cast<int>(0x80000000u);
+                    }
+                    ++k2;
+                    ++lower_entries;
+                }
+                for (; k2 < kcap; ++k2) {
+                    val[k2] = 0.0;
+                    src[k2] = ring;  // zero slot
+                }
+            }
+            // export entries executed at this level (values of level L-1)
+            int* ex = reinterpret_cast<int*>(base + static_cast<size_t>(m.x) * 16 +
+                                             static_cast<size_t>(nS) * kSmallBytes +
+                                             static_cast<size_t>(nL) * kLargeBytes);
+            for (size_t e = 0; e < exports[q].size(); ++e) {
+                const int4 x = exports[q][e];
+                ex[4 * e + 0] = pos[x.w] & (ring - 1);  // local ring slot of row j
+                ex[4 * e + 1] = x.y;                    // destination band | packet << 8
+                ex[4 * e + 2] = x.z;                    // destination halo index
+                ex[4 * e + 3] = 0;
+            }
+        }
+        for (auto& jh : imports[b]) halo_lookup[jh.first] = -1;
+    }
+
+    nthreads = 32 + std::min(480, (std::max(max_rows, max_exp) + 31) / 32 * 32);
+    const int fixed = 128 + 2 * meta_bytes + pbar_bytes + pad16(static_cast<int64_t>(ring + 1 + halo) * 8);
+    depth = std::min(8, std::max(0, (budget - fixed) / std::max(max_seg, 16)));
+    usable = depth >= 3 && max_k <= kMaxLower && ring >= max_exp_dist;
+    smem = static_cast<size_t>(fixed) + static_cast<size_t>(std::max(depth, 0)) * max_seg;
+    if (std::getenv("SDG_DEBUG"))
+        std::fprintf(stderr,
+                     "[sdg gs plan] n=%d bands=%d levels(max/band)=%d global_depth=%d threads=%d ring=%d "
+                     "halo=%d depth=%d max_seg=%d smem=%zu cross_refs=%lld global_refs=%lld packets=%zu "
+                     "packed=%.1fKB usable=%d max_k=%d\n",
+                     n, nb, max_band_levels, global_depth, nthreads, ring, halo, depth, max_seg, smem,
+                     (long long)cross_refs, (long long)global_refs, pkt_bytes_h.size(), off / 1024.0,
+                     (int)usable, max_k);
+
+    std::vector<int4> binfo(nb);
+    for (int b = 0; b < nb; ++b)
+        binfo[b] = make_int4(lbase[b], blev[b], pkt_base[b], pkt_base[b + 1] - pkt_base[b]);
+    if (req_h.empty()) req_h.push_back(0);
+    if (pkt_bytes_h.empty()) pkt_bytes_h.push_back(0);
+    meta.upload(mh, s);
+    band_info.upload(binfo, s);
+    req_ptr.upload(req_ptr_h, s);
+    req.upload(req_h, s);
+    packet_bytes.upload(pkt_bytes_h, s);
+    packed.upload(pk, s);
+    bidx.upload(bidx_h, s);
+    dinv.upload(dinv_h, s);
+    upper.upload(up, s);
+    meta_bytes_ = meta_bytes;
+    pbar_bytes_ = pbar_bytes;
+    if (usable) {
+        SDG_CUDA(cudaFuncSetAttribute(k_gs_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+        SDG_CUDA(cudaFuncSetAttribute(k_gs_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+    SDG_CUDA(cudaStreamSynchronize(s));  // host staging vectors die here
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+#define SDG_GS_CHECK()                                                                      \
+    do {                                                                                    \
+        c.count();                                                                          \
+        cudaError_t e_ = cudaGetLastError();                                                \
+        if (e_ != cudaSuccess) fail(SDG_ECUDA, std::string(__func__) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+void launch_gs_prep_pre(Context& c, const GsPlan& g, const double* r) {
+    ProfScope ps_(c, PF_GSPREP, 24.0 * g.n + 8.0 * g.n);
+    if (g.n == 0) return;
+    k_gs_prep_pre<<<(g.n + 255) / 256, 256, 0, c.stream>>>(g.n, r, g.dinv.get(), g.bidx.get(),
+                                                            const_cast<double*>(g.packed.get()));
+    SDG_GS_CHECK();
+}
+
+void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const double* z,
+                         const double* zc, const int* agg) {
+    ProfScope ps_(c, PF_GSPREP,
+                  12.0 * g.upper.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (z ? 2 : 1) + (zc ? 12.0 * g.n : 0.0) +
+                      16.0 * g.n);
+    if (g.n == 0) return;
+    k_gs_prep_post<<<(g.n + 255) / 256, 256, 0, c.stream>>>(
+        g.n, g.upper.rp.get(), g.upper.ci.get(), g.upper.v.get(), r, z, zc, agg, g.dinv.get(),
+        g.bidx.get(), const_cast<double*>(g.packed.get()));
+    SDG_GS_CHECK();
+}
+
+void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
+    ProfScope ps_(c, PF_GS, g.packed_bytes() + 8.0 * g.n);
+    if (g.n == 0) return;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(g.bands);
+    cfg.blockDim = dim3(g.nthreads);
+    cfg.dynamicSmemBytes = g.smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = g.bands;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const double* packed = g.packed.get();
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_gs_cluster, g.meta.get(), g.band_info.get(), g.req_ptr.get(),
+                                       g.req.get(), g.packet_bytes.get(), packed, g.ring, g.halo, g.depth,
+                                       g.max_seg, g.meta_bytes_, g.pbar_bytes_, z_new);
+    if (e != cudaSuccess) fail(SDG_ECUDA, std::string("launch_gs_lower: ") + cudaGetErrorString(e));
+    SDG_GS_CHECK();
+}
+
+void launch_restrict_warp(Context& c, const DevCsr& a, const int* pt_ptr, const int* pt_rows,
+                          int n_coarse, const double* r, const double* z, double* rc,
+                          const GsPlan* next) {
+    ProfScope ps_(c, PF_RESTRICT,
+                  12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 16.0 * a.n_rows + 4.0 * a.n_rows +
+                      4.0 * (n_coarse + 1) + 8.0 * n_coarse);
+    if (n_coarse == 0) return;
+    const int threads = 256;
+    const int blocks = static_cast<int>((static_cast<int64_t>(n_coarse) * 32 + threads - 1) / threads);
+    k_restrict_warp<<<blocks, threads, 0, c.stream>>>(
+        n_coarse, pt_ptr, pt_rows, a.rp.get(), a.ci.get(), a.v.get(), r, z, rc,
+        next ? next->dinv.get() : nullptr, next ? next->bidx.get() : nullptr,
+        next ? const_cast<double*>(next->packed.get()) : nullptr);
+    SDG_GS_CHECK();
+}
+
+}  // namespace sdg

@@ -1,0 +1,88 @@
+// Fast lexicographic Gauss-Seidel for the AMG smoother (precond.cpp:92-108,
+// omega = 1).  One forward sweep  z_new = (D + L)^{-1} (r - U z_old)  is
+// split into
+//   prep  (all SMs, bandwidth-bound): b_i = (r_i - sum_{j>i} a_ij z_old_j) / d_i
+//         written straight into the level-ordered packed buffer; for the
+//         post-smoother z_old = z + P zc, i.e. the prolongation is fused here;
+//   lower (latency-bound): the exact lexicographic recurrence
+//         z_i = b_i - sum_{j<i} (a_ij / d_i) z_j.
+//
+// The lower solve is a banded, pipelined level walk on one thread-block
+// cluster.  Rows are split into B bands (horizontal strips of the grid for
+// the lexicographic MAC / TPFA orderings, cut at the same relative height in
+// every labelled component); CTA b owns band b and walks the dependency
+// levels of the band-local lower triangle.  Values needed by later bands are
+// pushed into their shared memory with DSMEM st.async packets that complete
+// single-use mbarriers there; a band waits for a packet before the level that
+// reads it, so bands run as a skewed pipeline and the whole sweep keeps the
+// lexicographic order exactly.  Inside a CTA each
+// level's packed segment (b, scaled lower coefficients, ring slots, row ids)
+// is streamed into shared memory by TMA bulk copies (cp.async.bulk +
+// mbarrier) several levels ahead by a producer warp, and the band's recent z
+// values live in a shared-memory ring; the per-level critical path is one
+// barrier + shared-memory gathers + a short FMA tree.  Splitting into bands
+// spreads the shared-memory and L2 traffic of a sweep over B SMs, which is
+// what bounds a single-CTA walk (scripts/mb_levels.cu).
+//
+// Arithmetic is reassociated versus the reference (upper part first, 1/d
+// folded into the coefficients), so results agree to rounding; the BITWISE
+// single-CTA kernel (kernels.cu, k_gs_levels) remains the checker path of
+// sdg_sor_sweep and SDG_GS_EXACT=1.
+#pragma once
+
+#include <vector>
+
+#include "common.hpp"
+#include "setup.hpp"
+
+namespace sdg {
+
+struct GsPlan {
+    int n = 0;
+    int bands = 1;          // = cluster size of the lower kernel
+    int n_levels = 0;       // sum over bands of band levels (+1 export level when banded)
+    int max_band_levels = 0;
+    int nthreads = 64;
+    int ring = 0;           // local z ring per band, power of two
+    int halo = 0;           // imported boundary values per band (max)
+    int depth = 0;          // segments in flight (D)
+    int max_seg = 0;        // bytes
+    int max_packets = 1;    // imported DSMEM packets per band (max)
+    size_t smem = 0;        // dynamic shared memory of the lower kernel
+    bool usable = false;    // false -> fall back to the bitwise kernel
+    int64_t lower_entries = 0;
+    int64_t cross_refs = 0;
+    int64_t global_refs = 0;
+    int meta_bytes_ = 0, pbar_bytes_ = 0;
+    DevBuf<int4> meta;         // per (band, level) {off16, bytes16, nS | global flag << 31, nL | nE << 16}
+    DevBuf<int4> band_info;    // per band {meta base, n levels, packet base, n packets}
+    DevBuf<int> req_ptr;       // per (band, level) + 1: CSR into req
+    DevBuf<int> req;           // band-local packet ids a level waits for
+    DevBuf<int> packet_bytes;  // expected bytes per packet (all bands)
+    DevBuf<double> packed;     // all segments, 16-byte aligned
+    DevBuf<int> bidx;          // natural row -> index (in doubles) of its b slot
+    DevBuf<double> dinv;
+    DevCsr upper;              // strict upper triangle (natural order), unscaled
+
+    // components: per-row labels (e.g. u = 0 / v = 1 of the MAC velocity
+    // block) so that bands cut every component at the same relative height.
+    void build(const HostCsr& a, const std::vector<int>& components, cudaStream_t s,
+               int bands_hint = 0);
+    double packed_bytes() const { return static_cast<double>(packed.size()) * 8.0; }
+};
+
+// packed[bidx[i]] = r[i] * dinv[i]                      (pre-smoother, z_old = 0)
+void launch_gs_prep_pre(Context& c, const GsPlan& g, const double* r);
+// packed[bidx[i]] = (r_i - sum_{j>i} a_ij (z_j [+ zc[agg_j]])) * dinv_i
+void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const double* z,
+                         const double* zc, const int* agg);
+// the level walk; writes z_new (natural order)
+void launch_gs_lower(Context& c, const GsPlan& g, double* z_new);
+// fused residual + restriction, one warp per aggregate (bit-identical to
+// precond.cpp:241-244); optionally also seeds the next level's packed b
+// (rc * dinv) for its pre-smoother.
+void launch_restrict_warp(Context& c, const DevCsr& a, const int* pt_ptr, const int* pt_rows,
+                          int n_coarse, const double* r, const double* z, double* rc,
+                          const GsPlan* next);
+
+}  // namespace sdg

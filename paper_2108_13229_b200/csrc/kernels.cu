@@ -2,6 +2,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <string>
 
 namespace sdg {
 
@@ -154,9 +155,17 @@ __global__ void k_dense_gemv(int n, const double* __restrict__ a, const double* 
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
     const double* ar = a + static_cast<size_t>(row) * n;
-    double s = 0.0;
-    for (int j = lane; j < n; j += 32) s = fma(__ldg(ar + j), __ldg(x + j), s);
-    s = warp_sum(s);
+    // four independent accumulators keep four loads in flight per lane
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int j = lane;
+    for (; j + 96 < n; j += 128) {
+        s0 = fma(__ldg(ar + j), __ldg(x + j), s0);
+        s1 = fma(__ldg(ar + j + 32), __ldg(x + j + 32), s1);
+        s2 = fma(__ldg(ar + j + 64), __ldg(x + j + 64), s2);
+        s3 = fma(__ldg(ar + j + 96), __ldg(x + j + 96), s3);
+    }
+    for (; j < n; j += 32) s0 = fma(__ldg(ar + j), __ldg(x + j), s0);
+    double s = warp_sum((s0 + s1) + (s2 + s3));
     if (lane == 0) y[row] = s;
 }
 
@@ -258,7 +267,7 @@ __global__ void k_multi_axpy(int64_t n, int k, const double* __restrict__ X, int
         if (NORM) acc[0] = fma(wi, wi, acc[0]);
     }
     if (NORM) {
-        if (finish_reduce<1>(acc, partials, ticket) && threadIdx.x == 0) out[0] = acc[0];
+        if (finish_reduce<1>(acc, partials, ticket) && threadIdx.x == 0) out[0] = sqrt(acc[0]);  // ||w||, not its square
     }
 }
 
@@ -473,7 +482,8 @@ static inline int stride_blocks(Context& c, int64_t n) {
     do {                                                                   \
         (ctx).count();                                                     \
         cudaError_t e_ = cudaGetLastError();                               \
-        if (e_ != cudaSuccess) ::sdg::fail(SDG_ECUDA, cudaGetErrorString(e_)); \
+        if (e_ != cudaSuccess)                                             \
+            ::sdg::fail(SDG_ECUDA, std::string(__func__) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
 void launch_spmv(Context& c, const DevCsr& a, const double* x, double* y) {

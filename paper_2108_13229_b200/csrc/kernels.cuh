@@ -68,7 +68,7 @@ void launch_multidot(Context& c, ReduceWs& ws, int64_t n, int k, const double* X
 // w -= sum_v h[v] X_v  (h in device memory)
 void launch_multi_axpy(Context& c, int64_t n, int k, const double* X, int64_t ldx,
                        const double* h, double* w);
-// w -= sum_v h[v] X_v, then out[0] = ||w||^2
+// w -= sum_v h[v] X_v, then out[0] = ||w||_2 (the norm itself)
 void launch_multi_axpy_norm2(Context& c, ReduceWs& ws, int64_t n, int k, const double* X,
                              int64_t ldx, const double* h, double* w, double* out);
 // dst = src * (1/den[0]) when den[0] > 0  (reference: scale(v, 1.0 / wn))

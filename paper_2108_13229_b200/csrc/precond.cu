@@ -8,6 +8,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "power.cuh"
@@ -87,6 +88,8 @@ AmgPrecond::AmgPrecond(CtxPtr c, const HostCsr& a, const AmgOpts& o) : Precond(s
     Context& cx = *ctx_;
     std::vector<HostLevel> hl = build_hierarchy(a, o);
     n_rows_ = a.n_rows;
+    const char* ex = std::getenv("SDG_GS_EXACT");
+    exact_ = ex && ex[0] == '1';
     levels_.resize(hl.size());
     for (size_t l = 0; l < hl.size(); ++l) {
         Level& L = levels_[l];
@@ -109,6 +112,10 @@ AmgPrecond::AmgPrecond(CtxPtr c, const HostCsr& a, const AmgOpts& o) : Precond(s
             L.pt_rows.upload(rows, cx.stream);
             L.n_coarse = hl[l].n_coarse;
             L.zt.resize(A.n_rows);
+            if (!exact_) {
+                L.gs.build(A, hl[l].components, cx.stream);
+                L.fast = L.gs.usable;
+            }
         }
     }
     factor_coarse(hl.back().a);
@@ -177,8 +184,19 @@ void AmgPrecond::vcycle(int lev, const double* r, double* z) {
     }
     Level& L = levels_[lev];
     Level& C = levels_[lev + 1];
+    // the next level's pre-smoother input is seeded by the restriction
+    const GsPlan* seed = (lev + 2 < num_levels() && C.fast) ? &C.gs : nullptr;
+    if (L.fast) {
+        if (lev == 0) launch_gs_prep_pre(cx, L.gs, r);
+        launch_gs_lower(cx, L.gs, z);
+        launch_restrict_warp(cx, L.a, L.pt_ptr.get(), L.pt_rows.get(), L.n_coarse, r, z, C.r.get(), seed);
+        vcycle(lev + 1, C.r.get(), C.z.get());
+        launch_gs_prep_post(cx, L.gs, r, z, C.z.get(), L.agg.get());  // fused prolongation
+        launch_gs_lower(cx, L.gs, z);
+        return;
+    }
     launch_gs_levels(cx, L.a, L.lvl_ptr.get(), L.lvl_rows.get(), L.n_sched, r, nullptr, z, 1.0);
-    launch_resid_restrict(cx, L.a, L.pt_ptr.get(), L.pt_rows.get(), L.n_coarse, r, z, C.r.get());
+    launch_restrict_warp(cx, L.a, L.pt_ptr.get(), L.pt_rows.get(), L.n_coarse, r, z, C.r.get(), seed);
     vcycle(lev + 1, C.r.get(), C.z.get());
     launch_prolong(cx, L.a.n_rows, L.agg.get(), z, C.z.get(), L.zt.get());
     launch_gs_levels(cx, L.a, L.lvl_ptr.get(), L.lvl_rows.get(), L.n_sched, r, L.zt.get(), z, 1.0);

@@ -171,7 +171,7 @@ std::vector<HostLevel> build_hierarchy(const HostCsr& a, const AmgOpts& o) {
     if (!o.components.empty() && static_cast<int>(o.components.size()) != a.n_rows)
         fail(SDG_EDIM, "amg_setup: component label length mismatch");
     std::vector<HostLevel> levels;
-    levels.push_back({a, {}, 0});
+    levels.push_back({a, {}, 0, o.components});
     std::vector<int> labels = o.components;
     while (static_cast<int>(levels.size()) < o.max_levels &&
            levels.back().a.n_rows > o.coarse_threshold) {
@@ -186,7 +186,7 @@ std::vector<HostLevel> build_hierarchy(const HostCsr& a, const AmgOpts& o) {
         }
         levels.back().aggregate_of = std::move(agg);
         levels.back().n_coarse = n_coarse;
-        levels.push_back({std::move(coarse), {}, 0});
+        levels.push_back({std::move(coarse), {}, 0, labels});
     }
     return levels;
 }

@@ -27,6 +27,7 @@ struct HostLevel {
     HostCsr a;
     std::vector<int> aggregate_of;  // empty on the coarsest level
     int n_coarse = 0;
+    std::vector<int> components;    // dof labels of this level (empty: scalar)
 };
 
 // amg_setup (precond.cpp:189-217) without the coarse factorization, which

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "common.hpp"
+#include "gs.cuh"
 #include "kernels.cuh"
 #include "setup.hpp"
 
@@ -92,13 +93,16 @@ private:
         DevBuf<int> agg;
         DevBuf<int> pt_ptr, pt_rows;
         int n_coarse = 0;
-        DevBuf<double> zt;      // z + P zc before post-smoothing
+        DevBuf<double> zt;      // z + P zc before post-smoothing (bitwise path)
         DevBuf<double> r, z;    // this level's rhs / solution (levels >= 1)
+        GsPlan gs;              // fast smoother plan
+        bool fast = false;
     };
     void vcycle(int lev, const double* r, double* z);
     void factor_coarse(const HostCsr& coarse);
 
     int n_rows_ = 0;
+    bool exact_ = false;  // SDG_GS_EXACT=1: bitwise smoother path throughout
     std::vector<Level> levels_;
     int n_c_ = 0;
     DevBuf<double> coarse_inv_;  // row-major inverse of the coarsest matrix

@@ -35,8 +35,8 @@ def test_spmv_bitwise_full_c3_size(ref):
     s = sdc.assemble_monolithic(cfg)
     assert s.n_total() == 1001000 and s.matrix.nnz() == 7742002
     from oracle.refpy import Csr
-    a = Csr(s.n, s.n, s.matrix.row_offsets, s.matrix.col_indices, s.matrix.values)
-    x = ref.random_vector(s.n, 11)
+    a = Csr(s.n_total(), s.n_total(), s.matrix.row_offsets, s.matrix.col_indices, s.matrix.values)
+    x = ref.random_vector(s.n_total(), 11)
     assert bitwise_equal(sdc.spmv(s.matrix, x), ref.spmv(a, x))
 
 
