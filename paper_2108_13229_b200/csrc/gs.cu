@@ -206,35 +206,46 @@ __device__ __forceinline__ void solve_row(double b, int rowid, int wpos, const d
 }
 
 // One CTA per band, the bands forming one thread-block cluster.  Shared
-// memory: [D segment mbarriers | meta + req_ptr of the band | packet
-// mbarriers | z ring, zero slot, halo | D segment slots].  Warp 0 lane 0 is
-// the producer (TMA issue D levels ahead, packet waits); warps 1.. are
-// consumers, one row each per level (wider levels loop), with the next
-// level's row pulled into registers before the level barrier.
+// memory: [D chunk mbarriers | per-level meta + req_ptr + chunk table of the
+// band | packet mbarriers | z ring, zero slot, halo | D chunk slots].  The
+// level segments are grouped into chunks of several consecutive levels that
+// one TMA bulk copy brings in, so warp 0 lane 0 (the producer) works once per
+// chunk, keeping D chunks in flight; warps 1.. are consumers, one row each
+// per level (wider levels loop), pulling their next-level row into registers
+// before the level barrier.
 __global__ void __launch_bounds__(512, 1)
 k_gs_cluster(const int4* __restrict__ meta_g, const int4* __restrict__ band_info,
              const int* __restrict__ req_ptr_g, const int* __restrict__ req,
-             const int* __restrict__ packet_bytes, const double* __restrict__ packed, int ring,
-             int halo, int depth, int max_seg, int meta_bytes, int pbar_bytes, double* z_new) {
+             const int* __restrict__ packet_bytes, const int4* __restrict__ chunks_g,
+             const double* __restrict__ packed, int ring, int halo, int depth, int max_chunk,
+             int meta_bytes, int chunk_tab_bytes, int pbar_bytes, double* z_new) {
     extern __shared__ __align__(128) unsigned char sm[];
     cg::cluster_group cluster = cg::this_cluster();
     const int band = static_cast<int>(cluster.block_rank());
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
     int4* meta = reinterpret_cast<int4*>(sm + 128);
     int* reqp = reinterpret_cast<int*>(sm + 128 + meta_bytes);
-    uint64_t* pbars = reinterpret_cast<uint64_t*>(sm + 128 + 2 * meta_bytes);
-    double* zring = reinterpret_cast<double*>(sm + 128 + 2 * meta_bytes + pbar_bytes);
+    int4* chunks = reinterpret_cast<int4*>(sm + 128 + 2 * meta_bytes);
+    uint64_t* pbars = reinterpret_cast<uint64_t*>(sm + 128 + 2 * meta_bytes + chunk_tab_bytes);
+    double* zring = reinterpret_cast<double*>(sm + 128 + 2 * meta_bytes + chunk_tab_bytes + pbar_bytes);
     const int zero_slot = ring;
     const int zbytes = pad16(static_cast<int64_t>(ring + 1 + halo) * 8);
-    unsigned char* slots = sm + 128 + 2 * meta_bytes + pbar_bytes + zbytes;
+    unsigned char* slots = reinterpret_cast<unsigned char*>(zring) + zbytes;
     const int tid = threadIdx.x;
     const int ct = tid - 32;
     const int ncons = blockDim.x - 32;
 
-    const int4 bi = band_info[band];  // {meta base, n levels, packet base, n packets}
-    const int mbase = bi.x, n_levels = bi.y;
-    for (int l = tid; l < n_levels; l += blockDim.x) meta[l] = meta_g[mbase + l];
+    const int4 bi = band_info[band];          // {meta base, n levels, packet base, n packets}
+    const int4 bc = band_info[gridDim.x + band];  // {chunk base, n chunks, -, -}
+    const int mbase = bi.x, n_levels = bi.y, n_chunks = bc.y;
+    const bool has_packets = bi.w > 0;
+    for (int l = tid; l < n_levels; l += blockDim.x) {
+        int4 m = meta_g[mbase + l];
+        m.x = (m.w % depth) * max_chunk + m.x * 16;  // byte offset of the level in the slot area
+        meta[l] = m;
+    }
     for (int l = tid; l <= n_levels; l += blockDim.x) reqp[l] = req_ptr_g[mbase + l];
+    for (int c = tid; c < n_chunks; c += blockDim.x) chunks[c] = chunks_g[bc.x + c];
     for (int q = tid; q < bi.w; q += blockDim.x) {
         mbar_init(&pbars[q], 1);
         mbar_expect_tx(&pbars[q], static_cast<unsigned>(packet_bytes[bi.z + q]));
@@ -247,53 +258,44 @@ k_gs_cluster(const int4* __restrict__ meta_g, const int4* __restrict__ band_info
     cluster.sync();  // every packet barrier is armed before any remote store
 
     const unsigned char* gbase = reinterpret_cast<const unsigned char*>(packed);
-    int issue_slot = 0, wait_slot = 0;
-    unsigned wait_parity = 0;
-    auto issue = [&](int L) {
-        const int4 m = meta[L];
-        const unsigned bytes = static_cast<unsigned>(m.y) * 16u;
-        mbar_expect_tx(&bars[issue_slot], bytes);
-        if (bytes)
-            tma_load_1d(slots + static_cast<size_t>(issue_slot) * max_seg,
-                        gbase + static_cast<size_t>(m.x) * 16, bytes, &bars[issue_slot]);
-        issue_slot = issue_slot + 1 == depth ? 0 : issue_slot + 1;
+    auto slot_of = [&](int chunk) { return slots + static_cast<size_t>(chunk % depth) * max_chunk; };
+    auto seg_of = [&](int L) {
+        return static_cast<const unsigned char*>(slots) + meta[L].x;  // {slot offset, nS | flag, nL | nE << 16, chunk}
     };
-    auto wait_next = [&]() {
-        mbar_wait(&bars[wait_slot], wait_parity);
-        if (++wait_slot == depth) {
-            wait_slot = 0;
-            wait_parity ^= 1u;
-        }
+    auto issue = [&](int c) {
+        const int4 ch = chunks[c];  // {off16, bytes16, first level, levels}
+        uint64_t* bar = &bars[c % depth];
+        const unsigned bytes = static_cast<unsigned>(ch.y) * 16u;
+        mbar_expect_tx(bar, bytes);
+        if (bytes) tma_load_1d(slot_of(c), gbase + static_cast<size_t>(ch.x) * 16, bytes, bar);
     };
-    // the packets this level imports must have landed
+    auto wait_chunk = [&](int c) { mbar_wait(&bars[c % depth], static_cast<unsigned>(c / depth) & 1u); };
     auto satisfy = [&](int L) {
         for (int q = reqp[L]; q < reqp[L + 1]; ++q) mbar_wait(&pbars[req[q]], 0);
     };
     if (tid == 0) {
-        for (int L = 0; L < depth && L < n_levels; ++L) issue(L);
+        for (int c = 0; c < depth && c < n_chunks; ++c) issue(c);
         if (n_levels > 0) {
-            wait_next();
-            satisfy(0);
+            wait_chunk(meta[0].w);
+            if (has_packets) satisfy(0);
         }
-        if (n_levels > 1) wait_next();
+        if (n_levels > 1 && meta[1].w != meta[0].w) wait_chunk(meta[1].w);
     }
     __syncthreads();
 
     double rb = 0.0, v[kMaxLower];
     int rowid = 0, wpos = 0, sr[kMaxLower];
-    int cur_slot = 0;
     bool live = false;
     if (ct >= 0 && n_levels > 0) {
         const int4 m0 = meta[0];
-        live = load_row(slots, m0.z & 0x7fffffff, m0.w & 0xffff, ct, zero_slot, rb, rowid, wpos, v, sr);
+        live = load_row(seg_of(0), m0.y & 0x7fffffff, m0.z & 0xffff, ct, zero_slot, rb, rowid, wpos, v, sr);
     }
 
     for (int L = 0; L < n_levels; ++L) {
-        const int next_slot = cur_slot + 1 == depth ? 0 : cur_slot + 1;
         if (ct >= 0) {
             const int4 m = meta[L];
-            const int nS = m.z & 0x7fffffff, nL = m.w & 0xffff, nE = m.w >> 16;
-            const unsigned char* seg = slots + static_cast<size_t>(cur_slot) * max_seg;
+            const int nS = m.y & 0x7fffffff, nL = m.z & 0xffff, nE = m.z >> 16;
+            const unsigned char* seg = seg_of(L);
             // exports of the previous level (its values are in the ring)
             for (int e = ct; e < nE; e += ncons) {
                 const int4 x = *reinterpret_cast<const int4*>(seg + static_cast<size_t>(nS) * kSmallBytes +
@@ -305,7 +307,7 @@ k_gs_cluster(const int4* __restrict__ meta_g, const int4* __restrict__ band_info
                              cluster_addr(&pbars[pkt], dst));
             }
             if (live) {
-                if (m.z < 0)
+                if (m.y < 0)
                     solve_row<true, false>(rb, rowid, wpos, v, sr, zring, z_new);
                 else if (nL == 0)
                     solve_row<false, true>(rb, rowid, wpos, v, sr, zring, z_new);
@@ -320,21 +322,23 @@ k_gs_cluster(const int4* __restrict__ meta_g, const int4* __restrict__ band_info
                     solve_row<true, false>(eb, er, ew, ev, es, zring, z_new);
                 }
             }
+            // then the next level's row (its segment landed before the last barrier)
             if (L + 1 < n_levels) {
                 const int4 mn = meta[L + 1];
-                live = load_row(slots + static_cast<size_t>(next_slot) * max_seg, mn.z & 0x7fffffff,
-                                mn.w & 0xffff, ct, zero_slot, rb, rowid, wpos, v, sr);
+                live = load_row(seg_of(L + 1), mn.y & 0x7fffffff, mn.z & 0xffff, ct, zero_slot, rb, rowid,
+                                wpos, v, sr);
             }
         } else if (tid == 0) {
-            if (L + 2 < n_levels) wait_next();
-            if (L + 1 < n_levels) satisfy(L + 1);
+            // consumers read level L+2 during level L+1: its chunk must land first
+            if (L + 2 < n_levels && meta[L + 2].w != meta[L + 1].w) wait_chunk(meta[L + 2].w);
+            if (has_packets && L + 1 < n_levels) satisfy(L + 1);
         }
         __syncthreads();
-        if (tid == 0 && L + depth < n_levels) {
+        // chunk(L) is done once level L+1 starts in the next chunk: recycle it
+        if (tid == 0 && L + 1 < n_levels && meta[L + 1].w != meta[L].w && meta[L].w + depth < n_chunks) {
             fence_proxy_async();
-            issue(L + depth);
+            issue(meta[L].w + depth);
         }
-        cur_slot = next_slot;
     }
     cluster.sync();  // no CTA leaves while others may still write into it
 }
@@ -531,21 +535,44 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     max_packets = 1;
     for (int b = 0; b < nb; ++b) max_packets = std::max(max_packets, pkt_base[b + 1] - pkt_base[b]);
 
-    // ---- segments ---------------------------------------------------------
-    std::vector<int4> mh(n_levels);
+    // ---- segments and chunks -------------------------------------------------
+    // level q's segment: [small records][large records][exports]; consecutive
+    // levels of a band are grouped into chunks of about kChunkTarget bytes,
+    // each brought in by one TMA copy
+    constexpr int kChunkTarget = 24 * 1024;
+    std::vector<int> lvl_abs16(n_levels), lvl_bytes(n_levels);
+    std::vector<int4> mh(n_levels);   // {local off16, nS | flag, nL | nE << 16, band-local chunk}
+    std::vector<int4> ch_h;           // {off16, bytes16, first level, levels}
+    std::vector<int> ch_base(nb + 1, 0);
     int64_t off = 0;
     int max_rows = 1, max_exp = 0;
     max_seg = 16;
-    for (int q = 0; q < n_levels; ++q) {
-        const int nS = nS_of[q], nL = nr_of[q] - nS_of[q], nE = static_cast<int>(exports[q].size());
-        if (nL > 0xffff || nE > 0x7fff) fail(SDG_EINVAL, "gs plan: level too wide");
-        const int bytes = nS * kSmallBytes + nL * kLargeBytes + nE * kExportBytes;
-        mh[q] = make_int4(static_cast<int>(off / 16), bytes / 16, nS, nL | (nE << 16));
-        off += bytes;
-        max_seg = std::max(max_seg, bytes);
-        max_rows = std::max(max_rows, nr_of[q]);
-        max_exp = std::max(max_exp, nE);
+    for (int b = 0; b < nb; ++b) {
+        ch_base[b] = static_cast<int>(ch_h.size());
+        int chunk_bytes = 0;
+        for (int L = 0; L < blev[b]; ++L) {
+            const int q = lbase[b] + L;
+            const int nS = nS_of[q], nL = nr_of[q] - nS_of[q], nE = static_cast<int>(exports[q].size());
+            if (nL > 0xffff || nE > 0x7fff) fail(SDG_EINVAL, "gs plan: level too wide");
+            const int bytes = nS * kSmallBytes + nL * kLargeBytes + nE * kExportBytes;
+            if (L == 0 || chunk_bytes + bytes > kChunkTarget) {
+                ch_h.push_back(make_int4(static_cast<int>(off / 16), 0, L, 0));
+                chunk_bytes = 0;
+            }
+            int4& ch = ch_h.back();
+            lvl_abs16[q] = static_cast<int>(off / 16);
+            lvl_bytes[q] = bytes;
+            mh[q] = make_int4(chunk_bytes / 16, nS, nL | (nE << 16), static_cast<int>(ch_h.size()) - 1 - ch_base[b]);
+            chunk_bytes += bytes;
+            ch.y = chunk_bytes / 16;
+            ch.w += 1;
+            off += bytes;
+            max_seg = std::max(max_seg, chunk_bytes);
+            max_rows = std::max(max_rows, nr_of[q]);
+            max_exp = std::max(max_exp, nE);
+        }
     }
+    ch_base[nb] = static_cast<int>(ch_h.size());
     if (off / 8 + 2 > (static_cast<int64_t>(1) << 31)) fail(SDG_EINVAL, "gs plan: packed buffer too large");
 
     int max_dist = 2;      // in-band dependency distance in level-order positions
@@ -564,12 +591,16 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
             }
         }
 
+    int max_band_chunks = 1;
+    for (int b = 0; b < nb; ++b) max_band_chunks = std::max(max_band_chunks, ch_base[b + 1] - ch_base[b]);
     const int budget = smem_budget();
     const int meta_bytes = pad16(static_cast<int64_t>(max_band_levels + 1) * 16);
+    const int chunk_tab_bytes = pad16(static_cast<int64_t>(max_band_chunks) * 16);
     const int pbar_bytes = pad16(static_cast<int64_t>(max_packets) * 8);
-    // z ring: large enough for every in-band dependency when six segment
-    // slots still fit, else the largest power of two that does
-    const int ring_room = (budget - 128 - 2 * meta_bytes - pbar_bytes - (halo + 2) * 8 - 16 - 6 * max_seg) / 8;
+    const int base_bytes = 128 + 2 * meta_bytes + chunk_tab_bytes + pbar_bytes;
+    // z ring: large enough for every in-band dependency when four chunk slots
+    // still fit, else the largest power of two that does
+    const int ring_room = (budget - base_bytes - (halo + 2) * 8 - 16 - 4 * max_seg) / 8;
     int min_ring = 64;
     while (min_ring < max_exp_dist) min_ring <<= 1;  // exports must find their values
     ring = 1;
@@ -589,15 +620,15 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
             const int q = lbase[b] + L;
             int4& m = mh[q];
             const int band_end = lptr[q + 1] - lptr[lbase[b]];
-            const int nS = m.z, nL = m.w & 0xffff;
+            const int nS = m.y, nL = m.z & 0xffff;
+            unsigned char* seg = base + static_cast<size_t>(lvl_abs16[q]) * 16;
             for (int p = lptr[q]; p < lptr[q + 1]; ++p) {
                 const int t = p - lptr[q];
                 const int i = order[p];
                 const bool small = t < nS;
-                unsigned char* rec = base + static_cast<size_t>(m.x) * 16 +
-                                     (small ? static_cast<size_t>(t) * kSmallBytes
-                                            : static_cast<size_t>(nS) * kSmallBytes +
-                                                  static_cast<size_t>(t - nS) * kLargeBytes);
+                unsigned char* rec = seg + (small ? static_cast<size_t>(t) * kSmallBytes
+                                                  : static_cast<size_t>(nS) * kSmallBytes +
+                                                        static_cast<size_t>(t - nS) * kLargeBytes);
                 double* recd = reinterpret_cast<double*>(rec);
                 int* reci = reinterpret_cast<int*>(rec);
                 bidx_h[i] = static_cast<int>((rec - base) / 8);
@@ -618,7 +649,7 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
                     } else {
                         src[k2] = -(j + 1);
                         ++global_refs;
-                        m.z |= static_cast<int>(0x80000000u);
+                        m.y |= static_cast<int>(0x80000000u);
                     }
                     ++k2;
                     ++lower_entries;
@@ -629,8 +660,7 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
                 }
             }
             // export entries executed at this level (values of level L-1)
-            int* ex = reinterpret_cast<int*>(base + static_cast<size_t>(m.x) * 16 +
-                                             static_cast<size_t>(nS) * kSmallBytes +
+            int* ex = reinterpret_cast<int*>(seg + static_cast<size_t>(nS) * kSmallBytes +
                                              static_cast<size_t>(nL) * kLargeBytes);
             for (size_t e = 0; e < exports[q].size(); ++e) {
                 const int4 x = exports[q][e];
@@ -644,22 +674,24 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     }
 
     nthreads = 32 + std::min(480, (std::max(max_rows, max_exp) + 31) / 32 * 32);
-    const int fixed = 128 + 2 * meta_bytes + pbar_bytes + pad16(static_cast<int64_t>(ring + 1 + halo) * 8);
-    depth = std::min(8, std::max(0, (budget - fixed) / std::max(max_seg, 16)));
+    const int fixed = base_bytes + pad16(static_cast<int64_t>(ring + 1 + halo) * 8);
+    depth = std::min(6, std::max(0, (budget - fixed) / std::max(max_seg, 16)));
     usable = depth >= 3 && max_k <= kMaxLower && ring >= max_exp_dist;
     smem = static_cast<size_t>(fixed) + static_cast<size_t>(std::max(depth, 0)) * max_seg;
     if (std::getenv("SDG_DEBUG"))
         std::fprintf(stderr,
                      "[sdg gs plan] n=%d bands=%d levels(max/band)=%d global_depth=%d threads=%d ring=%d "
-                     "halo=%d depth=%d max_seg=%d smem=%zu cross_refs=%lld global_refs=%lld packets=%zu "
-                     "packed=%.1fKB usable=%d max_k=%d\n",
-                     n, nb, max_band_levels, global_depth, nthreads, ring, halo, depth, max_seg, smem,
-                     (long long)cross_refs, (long long)global_refs, pkt_bytes_h.size(), off / 1024.0,
+                     "halo=%d chunks=%zu depth=%d max_chunk=%d smem=%zu cross_refs=%lld global_refs=%lld "
+                     "packets=%zu packed=%.1fKB usable=%d max_k=%d\n",
+                     n, nb, max_band_levels, global_depth, nthreads, ring, halo, ch_h.size(), depth, max_seg,
+                     smem, (long long)cross_refs, (long long)global_refs, pkt_bytes_h.size(), off / 1024.0,
                      (int)usable, max_k);
 
-    std::vector<int4> binfo(nb);
-    for (int b = 0; b < nb; ++b)
+    std::vector<int4> binfo(2 * nb);
+    for (int b = 0; b < nb; ++b) {
         binfo[b] = make_int4(lbase[b], blev[b], pkt_base[b], pkt_base[b + 1] - pkt_base[b]);
+        binfo[nb + b] = make_int4(ch_base[b], ch_base[b + 1] - ch_base[b], 0, 0);
+    }
     if (req_h.empty()) req_h.push_back(0);
     if (pkt_bytes_h.empty()) pkt_bytes_h.push_back(0);
     meta.upload(mh, s);
@@ -667,11 +699,13 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     req_ptr.upload(req_ptr_h, s);
     req.upload(req_h, s);
     packet_bytes.upload(pkt_bytes_h, s);
+    chunk_tab.upload(ch_h, s);
     packed.upload(pk, s);
     bidx.upload(bidx_h, s);
     dinv.upload(dinv_h, s);
     upper.upload(up, s);
     meta_bytes_ = meta_bytes;
+    chunk_tab_bytes_ = chunk_tab_bytes;
     pbar_bytes_ = pbar_bytes;
     if (usable) {
         SDG_CUDA(cudaFuncSetAttribute(k_gs_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
@@ -727,8 +761,9 @@ void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
     cfg.numAttrs = 1;
     const double* packed = g.packed.get();
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_gs_cluster, g.meta.get(), g.band_info.get(), g.req_ptr.get(),
-                                       g.req.get(), g.packet_bytes.get(), packed, g.ring, g.halo, g.depth,
-                                       g.max_seg, g.meta_bytes_, g.pbar_bytes_, z_new);
+                                       g.req.get(), g.packet_bytes.get(), g.chunk_tab.get(), packed, g.ring,
+                                       g.halo, g.depth, g.max_seg, g.meta_bytes_, g.chunk_tab_bytes_,
+                                       g.pbar_bytes_, z_new);
     if (e != cudaSuccess) fail(SDG_ECUDA, std::string("launch_gs_lower: ") + cudaGetErrorString(e));
     SDG_GS_CHECK();
 }

@@ -46,16 +46,17 @@ struct GsPlan {
     int ring = 0;           // local z ring per band, power of two
     int halo = 0;           // imported boundary values per band (max)
     int depth = 0;          // segments in flight (D)
-    int max_seg = 0;        // bytes
+    int max_seg = 0;        // bytes of the largest chunk
     int max_packets = 1;    // imported DSMEM packets per band (max)
     size_t smem = 0;        // dynamic shared memory of the lower kernel
     bool usable = false;    // false -> fall back to the bitwise kernel
     int64_t lower_entries = 0;
     int64_t cross_refs = 0;
     int64_t global_refs = 0;
-    int meta_bytes_ = 0, pbar_bytes_ = 0;
-    DevBuf<int4> meta;         // per (band, level) {off16, bytes16, nS | global flag << 31, nL | nE << 16}
-    DevBuf<int4> band_info;    // per band {meta base, n levels, packet base, n packets}
+    int meta_bytes_ = 0, chunk_tab_bytes_ = 0, pbar_bytes_ = 0;
+    DevBuf<int4> meta;         // per (band, level) {chunk-local off16, nS | global flag << 31, nL | nE << 16, chunk}
+    DevBuf<int4> chunk_tab;    // per (band, chunk) {off16, bytes16, first level, levels}
+    DevBuf<int4> band_info;    // per band {meta base, n levels, packet base, n packets}, then {chunk base, n chunks}
     DevBuf<int> req_ptr;       // per (band, level) + 1: CSR into req
     DevBuf<int> req;           // band-local packet ids a level waits for
     DevBuf<int> packet_bytes;  // expected bytes per packet (all bands)

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 
 #include "solver.hpp"
 
@@ -206,6 +207,38 @@ SolveOut pd_gmres(Matrix& A, Precond* P, const double* b, double* x, double tol_
     return out;
 }
 
+// Per-matrix BiCGSTAB workspace, kept across solves so the captured
+// iteration graph (which bakes in these pointers) can be replayed.
+struct BiWork {
+    int n = 0;
+    DevBuf<double> r, rhat, p, vv, s, phat, shat, t, rt, scal;
+    DevBuf<BiState> st;
+    ReduceWs ws;
+    cudaGraphExec_t exec = nullptr;
+    const Precond* graph_p = nullptr;
+    const double* graph_x = nullptr;
+    int64_t graph_launches = 0;
+    explicit BiWork(int n_, Context& c)
+        : n(n_), r(n_), rhat(n_), p(n_), vv(n_), s(n_), phat(n_), shat(n_), t(n_), rt(n_), scal(4), st(1) {
+        ws.init(reduce_blocks(n_, c.num_sms), 2, c.stream);
+    }
+    ~BiWork() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
+namespace {
+
+bool graphs_enabled(const Context& c) {
+    static const bool env_off = [] {
+        const char* e = std::getenv("SDG_GRAPHS");
+        return e && e[0] == '0';
+    }();
+    return !env_off && !c.profiling;
+}
+
+}  // namespace
+
 SolveOut bicgstab(Matrix& A, Precond* P, const double* b, double* x, double tol_abs,
                   int max_iters) {
     Context& c = *A.ctx;
@@ -218,17 +251,64 @@ SolveOut bicgstab(Matrix& A, Precond* P, const double* b, double* x, double tol_
     double* host = c.pinned->as<double>();
     BiState* hst = reinterpret_cast<BiState*>(host + 512);
 
-    DevBuf<double> r(n), rhat(n), p(n), vv(n), s(n), phat(n), shat(n), t(n), rt(n), scal(4);
-    DevBuf<BiState> st(1);
-    ReduceWs ws;
-    ws.init(reduce_blocks(n, c.num_sms), 2, c.stream);
+    if (!A.bi_work || A.bi_work->n != n) A.bi_work = std::make_shared<BiWork>(n, c);
+    BiWork& W = *A.bi_work;
+    DevBuf<double>&r = W.r, &rhat = W.rhat, &p = W.p, &vv = W.vv, &s = W.s, &phat = W.phat,
+                   &shat = W.shat, &t = W.t, &rt = W.rt, &scal = W.scal;
+    DevBuf<BiState>& st = W.st;
+    ReduceWs& ws = W.ws;
+
+    // one iteration (krylov.cpp:241-283) plus the status read-back
+    auto enqueue_iteration = [&]() {
+        launch_bi_p(c, n, st.get(), r.get(), vv.get(), p.get());
+        precond_apply(c, P, p.get(), phat.get(), n);
+        launch_spmv(c, A.dev, phat.get(), vv.get());
+        launch_bi_rv(c, ws, n, st.get(), rhat.get(), vv.get());
+        launch_bi_s(c, ws, n, st.get(), r.get(), vv.get(), s.get());
+        precond_apply(c, P, s.get(), shat.get(), n);
+        launch_spmv(c, A.dev, shat.get(), t.get());
+        launch_bi_t(c, ws, n, st.get(), t.get(), s.get());
+        launch_bi_xr(c, ws, n, st.get(), phat.get(), shat.get(), s.get(), t.get(), rhat.get(), x, r.get());
+        SDG_CUDA(cudaMemcpyAsync(hst, st.get(), sizeof(BiState), cudaMemcpyDeviceToHost, c.stream));
+    };
+    const bool use_graph = graphs_enabled(c);
+    if (use_graph && (!W.exec || W.graph_p != P || W.graph_x != x)) {
+        if (W.exec) {
+            cudaGraphExecDestroy(W.exec);
+            W.exec = nullptr;
+        }
+        const int64_t l0 = c.launches.load();
+        cudaGraph_t g = nullptr;
+        SDG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_iteration();
+        } catch (...) {
+            cudaStreamEndCapture(c.stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        SDG_CUDA(cudaStreamEndCapture(c.stream, &g));
+        SDG_CUDA(cudaGraphInstantiate(&W.exec, g, 0));
+        cudaGraphDestroy(g);
+        W.graph_launches = c.launches.load() - l0;
+        c.launches.fetch_sub(W.graph_launches);
+        W.graph_p = P;
+        W.graph_x = x;
+    }
+    auto run_iteration = [&]() {
+        if (use_graph) {
+            SDG_CUDA(cudaGraphLaunch(W.exec, c.stream));
+            c.count(static_cast<int>(W.graph_launches));
+        } else {
+            enqueue_iteration();
+        }
+    };
 
     auto upload_state = [&](const BiState& s_) {
         *hst = s_;
         SDG_CUDA(cudaMemcpyAsync(st.get(), hst, sizeof(BiState), cudaMemcpyHostToDevice, c.stream));
     };
-    auto read_state = [&]() -> BiState {
-        SDG_CUDA(cudaMemcpyAsync(hst, st.get(), sizeof(BiState), cudaMemcpyDeviceToHost, c.stream));
+    auto read_state = [&]() -> BiState {  // the iteration already queued the copy
         c.sync();
         return *hst;
     };
@@ -289,16 +369,7 @@ SolveOut bicgstab(Matrix& A, Precond* P, const double* b, double* x, double tol_
     };
 
     for (int iter = 0; iter < max_iters && !done; ++iter) {
-        launch_bi_p(c, n, st.get(), r.get(), vv.get(), p.get());
-        precond_apply(c, P, p.get(), phat.get(), n);
-        launch_spmv(c, A.dev, phat.get(), vv.get());
-        launch_bi_rv(c, ws, n, st.get(), rhat.get(), vv.get());
-        launch_bi_s(c, ws, n, st.get(), r.get(), vv.get(), s.get());
-        precond_apply(c, P, s.get(), shat.get(), n);
-        launch_spmv(c, A.dev, shat.get(), t.get());
-        launch_bi_t(c, ws, n, st.get(), t.get(), s.get());
-        launch_bi_xr(c, ws, n, st.get(), phat.get(), shat.get(), s.get(), t.get(), rhat.get(),
-                     x, r.get());
+        run_iteration();
         BiState cur = read_state();
         switch (cur.flag) {
         case BI_BREAK_RHO:

@@ -15,6 +15,8 @@
 
 namespace sdg {
 
+struct BiWork;  // krylov.cu: cached BiCGSTAB workspace + captured iteration graph
+
 // A device CSR plus its host copy (setup extracts blocks from it) and, on
 // demand, the Gauss-Seidel level schedule.
 struct Matrix {
@@ -25,6 +27,8 @@ struct Matrix {
     bool sched_ready = false;
     DevBuf<int> lvl_ptr, lvl_rows;
     int n_levels = 0;
+
+    std::shared_ptr<BiWork> bi_work;
 
     Matrix(CtxPtr c, HostCsr h);
     void ensure_schedule();
