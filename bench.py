@@ -322,11 +322,21 @@ def run_ours(args):
         per_launch_ms = f["ms"] / f["launches"]
         per_launch_bytes = f["bytes"] / f["launches"]
         ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+        t = traffic.get(fam)
         return {"kernel": fam, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "peak_source": peak_kind, "traffic": None,
+                "frac": ach / peak, "peak_source": peak_kind,
+                "traffic": t["dram_bytes_per_launch"] if t else None,
+                "traffic_note": t["kernel"] + "; " + t["source"] if t else None,
                 "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms, "launches": f["launches"],
                 "share_of_step": f["ms"] / sum(v["ms"] for v in prof.values())}
 
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    traffic = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f)
+    except Exception:
+        pass
     dominant = max(prof, key=lambda k: prof[k]["ms"])
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
