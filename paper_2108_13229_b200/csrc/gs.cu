@@ -24,6 +24,7 @@
 // are odd multiples of 16 bytes, so 16-byte shared loads of consecutive
 // records are bank-conflict free.
 #include "gs.cuh"
+#include "ptx.cuh"
 
 #include <cooperative_groups.h>
 
@@ -39,6 +40,8 @@ namespace cg = cooperative_groups;
 
 namespace sdg {
 
+using namespace ptx;
+
 namespace {
 
 constexpr int kMaxSmem = 227 * 1024;
@@ -48,65 +51,6 @@ constexpr int kExportBytes = 16;
 constexpr int kMaxLower = 8;
 
 __host__ __device__ inline int pad16(int64_t b) { return static_cast<int>((b + 15) / 16 * 16); }
-
-// ---- small PTX helpers (mbarrier, TMA bulk copy, cluster memory) -------------
-
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-// shared::cluster address of `p` (a shared variable of this CTA) in CTA `rank`
-__device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
-    unsigned out;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_addr(p)), "r"(rank));
-    return out;
-}
-
-// asynchronous remote store whose bytes complete a transaction count on an
-// mbarrier in the destination CTA: the DSMEM push needs no fences
-__device__ __forceinline__ void st_async_f64(unsigned addr, double v, unsigned mbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr),
-                 "d"(v), "r"(mbar)
-                 : "memory");
-}
 
 // ---- prep kernels ----------------------------------------------------------
 
@@ -418,10 +362,18 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
 
     // ---- bands: one for small systems, more once a single SM's bandwidth
     // becomes the bound (SDG_GS_BANDS overrides) -----------------------------
-    const int global_depth = lower_schedule(a).n_levels();
     int nb = bands_hint > 0 ? bands_hint : (n >= 200000 ? 8 : n >= 80000 ? 4 : 1);
     if (const char* e = std::getenv("SDG_GS_BANDS")) nb = std::max(1, std::atoi(e));
     nb = std::max(1, std::min({nb, 8, std::max(1, n / 256)}));
+    const char* walk_env = std::getenv("SDG_GS_WALK");
+    if (nb == 1 && !(walk_env && walk_env[0] == '0') && build_walk(a, dinv_h, nlow, max_k, s)) {
+        dinv.upload(dinv_h, s);
+        upper.upload(up, s);
+        SDG_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    walk = false;
+    const int global_depth = lower_schedule(a).n_levels();
     std::vector<int> rank_in_comp(n), comp_size;
     for (int i = 0; i < n; ++i) {
         const int c = comps.empty() ? 0 : comps[i];
@@ -747,6 +699,10 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
 void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
     ProfScope ps_(c, PF_GS, g.packed_bytes() + 8.0 * g.n);
     if (g.n == 0) return;
+    if (g.walk) {
+        launch_gs_walk(c, g, z_new);
+        return;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(g.bands);
     cfg.blockDim = dim3(g.nthreads);

@@ -54,6 +54,11 @@ struct GsPlan {
     int64_t cross_refs = 0;
     int64_t global_refs = 0;
     int meta_bytes_ = 0, chunk_tab_bytes_ = 0, pbar_bytes_ = 0;
+    bool walk = false;         // single-CTA walk (gs_walk.cu) instead of the banded cluster kernel
+    int walk_meta_bytes = 0, walk_chunk_bytes = 0, walk_cfirst_bytes = 0, walk_zbytes = 0, walk_chunks = 0;
+    int walk_w2 = 0;           // consumer warps owning the <= 2-entry rows
+    DevBuf<int4> walk_iss;     // per chunk {global off16, bytes, stage off, issue after level}
+    DevBuf<int> walk_cfirst;   // per chunk: first level
     DevBuf<int4> meta;         // per (band, level) {chunk-local off16, nS | global flag << 31, nL | nE << 16, chunk}
     DevBuf<int4> chunk_tab;    // per (band, chunk) {off16, bytes16, first level, levels}
     DevBuf<int4> band_info;    // per band {meta base, n levels, packet base, n packets}, then {chunk base, n chunks}
@@ -70,6 +75,10 @@ struct GsPlan {
     void build(const HostCsr& a, const std::vector<int>& components, cudaStream_t s,
                int bands_hint = 0);
     double packed_bytes() const { return static_cast<double>(packed.size()) * 8.0; }
+
+private:
+    bool build_walk(const HostCsr& a, const std::vector<double>& dinv_h, const std::vector<int>& nlow, int max_k,
+                    cudaStream_t s);
 };
 
 // packed[bidx[i]] = r[i] * dinv[i]                      (pre-smoother, z_old = 0)
@@ -79,6 +88,8 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
                          const double* zc, const int* agg);
 // the level walk; writes z_new (natural order)
 void launch_gs_lower(Context& c, const GsPlan& g, double* z_new);
+// single-CTA variant (plans with walk == true; gs_walk.cu)
+void launch_gs_walk(Context& c, const GsPlan& g, double* z_new);
 // fused residual + restriction, one warp per aggregate (bit-identical to
 // precond.cpp:241-244); optionally also seeds the next level's packed b
 // (rc * dinv) for its pre-smoother.

@@ -1,0 +1,66 @@
+// Dev harness: the production single-CTA walk (plan + kernel) on a synthetic
+// nx x nx 5-point lower triangle, timed with CUDA events.  Feature knock-outs
+// with -DSDG_WALK_EXP=mask (see gs_walk.cu).
+#define private public
+#include "../paper_2108_13229_b200/csrc/gs_walk.cu"
+
+#include <cmath>
+#include <vector>
+
+using namespace sdg;
+
+int main(int argc, char** argv) {
+    const int nx = argc > 1 ? atoi(argv[1]) : 160, n = nx * nx;
+    HostCsr a(n, n);
+    std::vector<double> dinv(n, 0.25);
+    std::vector<int> nlow(n, 0);
+    for (int j = 0; j < nx; ++j)
+        for (int i = 0; i < nx; ++i) {
+            const int r = j * nx + i;
+            if (j > 0) { a.ci.push_back(r - nx); a.v.push_back(-1.0); nlow[r]++; }
+            if (i > 0) { a.ci.push_back(r - 1); a.v.push_back(-1.0); nlow[r]++; }
+            a.ci.push_back(r); a.v.push_back(4.0);
+            a.rp[r + 1] = static_cast<int>(a.ci.size());
+        }
+    cudaStream_t s;
+    cudaStreamCreate(&s);
+    GsPlan g;
+    if (!g.build_walk(a, dinv, nlow, 2, s)) { printf("plan failed\n"); return 1; }
+    std::vector<int> bidx(n);
+    cudaMemcpy(bidx.data(), g.bidx.get(), n * 4, cudaMemcpyDeviceToHost);
+    std::vector<double> pk(g.packed.size());
+    cudaMemcpy(pk.data(), g.packed.get(), pk.size() * 8, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < n; ++i) pk[bidx[i]] = 0.25 * (1.0 + 1e-3 * (i % 7));
+    cudaMemcpy(g.packed.get(), pk.data(), pk.size() * 8, cudaMemcpyHostToDevice);
+    double* z;
+    cudaMalloc(&z, n * 8);
+    WalkArgs wa{g.meta.get(), g.walk_iss.get(), g.walk_cfirst.get(),
+                reinterpret_cast<const unsigned char*>(g.packed.get()), g.n_levels, g.walk_chunks, g.ring,
+                g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_cfirst_bytes, g.walk_zbytes, g.walk_w2, z};
+    for (int r = 0; r < 3; ++r) k_gs_walk<<<1, g.nthreads, g.smem, s>>>(wa);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < 20; ++r) k_gs_walk<<<1, g.nthreads, g.smem, s>>>(wa);
+    cudaEventRecord(e1, s);
+    cudaError_t e = cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    std::vector<double> hz(n), zc(n);
+    cudaMemcpy(hz.data(), z, n * 8, cudaMemcpyDeviceToHost);
+    double maxd = 0;
+    for (int i = 0; i < n; ++i) {
+        double acc = 0.25 * (1.0 + 1e-3 * (i % 7));
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+            if (a.ci[k] < i) acc += 0.25 * zc[a.ci[k]];
+        zc[i] = acc;
+        maxd = std::max(maxd, std::abs(acc - hz[i]) / std::abs(acc));
+    }
+    int clk;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("nx %d levels %d threads %d: %.2f us/launch, %.0f cycles/level, rel err %.1e (%s)\n",
+           nx, g.n_levels, g.nthreads, ms / 20 * 1e3, ms / 20 * 1e-3 * clk * 1e3 / g.n_levels, maxd,
+           cudaGetErrorString(e));
+    return 0;
+}
