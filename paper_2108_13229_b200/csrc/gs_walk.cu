@@ -40,6 +40,15 @@ using namespace ptx;
 
 namespace {
 
+#ifdef SDG_WALK_TRACE  // dev aid (scripts/mb_real2.cu): per-level clocks of lane 0 of every warp
+__device__ long long g_walk_trace[1024 * 16 * 4];
+#define WALK_CLK(L, k)                                          \
+    if ((threadIdx.x & 31) == 0 && (L) < 1024)                  \
+    g_walk_trace[((L) * 16 + (threadIdx.x >> 5)) * 4 + (k)] = clock64()
+#else
+#define WALK_CLK(L, k)
+#endif
+
 constexpr int kBars = 32;      // chunk mbarriers (chunks in flight at most)
 constexpr int kK2Bytes = 48;
 constexpr int kK8Bytes = 112;
@@ -61,26 +70,52 @@ struct WalkArgs {
     double* z_new;
 };
 
+__device__ __forceinline__ int ld_volatile(const int* p) {
+    int v;
+    asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_volatile(int* p, int v) {
+    asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+    unsigned done;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+
 // The level loop of one consumer warp.  Every warp owns one class for the
 // whole sweep (thread t of the class: t-th row of that class at every level),
 // so the loop has no class branches.  Per level: the gathers, coefficient and
 // next-level meta loads are issued together, the row is finished and stored,
 // and the next level's record is requested before the barrier (it lands while
-// the barrier completes).
+// the barrier completes).  The level barrier is a named barrier of the
+// consumer warps only; a level that starts a chunk first checks the
+// producer's `landed` counter.
 template <bool K2>
 __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* meta, const unsigned char* stage,
-                                              const unsigned char* nullrec, double* zr, int t) {
+                                              const unsigned char* nullrec, double* zr, int* flags, int t) {
     const int mask = a.ring - 1, dummy = a.ring + 1;
+    const unsigned ncons = blockDim.x - 32;
     constexpr int K = K2 ? 2 : kMaxK;
     constexpr int RB = K2 ? kK2Bytes : kK8Bytes;
     double b;
     int s[K], rowid, pin, wpos;
     const unsigned char* vrec;
+    // meta = {K2 stage offset, K8 stage offset | chunk-start << 18, K2 pos | n2 << 20, K8 pos | n8 << 20}
+    const unsigned char* nrec = nullrec + (K2 ? 0 : 128);
+    const int toff = t * RB;
     auto fetch = [&](const int4 m) {
-        const int n = K2 ? m.y : m.z;
-        const bool ok = t < n;
-        const unsigned char* q =
-            ok ? stage + m.x + (K2 ? 0 : m.y * kK2Bytes) + t * RB : nullrec + (K2 ? 0 : 128);
+        const int off = K2 ? m.x : (m.y & 0x3ffff);
+        const int pn = K2 ? m.z : m.w;
+        const bool ok = t < (pn >> 20);
+        const unsigned char* q = ok ? stage + off + toff : nrec;
         const int4 h = *reinterpret_cast<const int4*>(q);
         if (K2) {
             const int2 ss = *reinterpret_cast<const int2*>(q + 32);
@@ -96,11 +131,19 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
         rowid = h.z;
         pin = h.w;
         vrec = q + 16;
-        wpos = ok ? ((m.w + (K2 ? 0 : m.y) + t) & mask) : dummy;
+        wpos = ok ? (((pn & 0xfffff) + t) & mask) : dummy;
     };
-    __syncthreads();  // the producer has waited for the first two levels
-    fetch(meta[0]);
+    int* progress = flags;
+    const int* landed = flags + 1;
+    {
+        const int4 m0 = meta[0];
+        const int need = static_cast<unsigned>(m0.y) >> 18;
+        while (ld_volatile(landed) < need) {
+        }
+        fetch(m0);
+    }
     for (int L = 0; L < a.n_levels; ++L) {
+        WALK_CLK(L, 0);
         double z[K], v[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) z[k] = zr[s[k]];
@@ -111,6 +154,10 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
             v[2 * k + 1] = c.y;
         }
         const int4 mn = meta[L + 1];
+        const int need = static_cast<unsigned>(mn.y) >> 18;  // chunk id + 1 when level L+1 starts a chunk
+        if (need)
+            while (ld_volatile(landed) < need) {
+            }
         double acc;
         if (K2) {
             acc = fma(v[1], z[1], fma(v[0], z[0], b));
@@ -124,15 +171,19 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
         zr[wpos] = acc;
         zr[pin] = acc;
         if (rowid >= 0) a.z_new[rowid] = acc;
+        WALK_CLK(L, 1);
         fetch(mn);
-        __syncthreads();
+        WALK_CLK(L, 2);
+        asm volatile("bar.sync 1, %0;" ::"r"(ncons) : "memory");
+        if (threadIdx.x == 32) st_volatile(progress, L + 1);
     }
 }
 
 __global__ void __launch_bounds__(384, 1) k_gs_walk(WalkArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
-    unsigned char* nullrec = sm + kBars * 8;
+    int* flags = reinterpret_cast<int*>(sm + kBars * 8);  // {levels done, chunks landed}
+    unsigned char* nullrec = sm + kBars * 8 + 16;
     int4* meta = reinterpret_cast<int4*>(nullrec + kNullBytes);
     int4* ctab = reinterpret_cast<int4*>(reinterpret_cast<unsigned char*>(meta) + a.meta_bytes);
     int* cfirst = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(ctab) + a.chunk_bytes);
@@ -145,10 +196,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_walk(WalkArgs a) {
     const int zero_slot = a.ring, dummy = a.ring + 1;
 
     for (int l = tid; l <= nl; l += blockDim.x) meta[l] = a.meta_g[l];
-    for (int c = tid; c < nc; c += blockDim.x) {
-        ctab[c] = a.chunk_g[c];
-        cfirst[c] = a.cfirst_g[c];
-    }
+    for (int c = tid; c < nc; c += blockDim.x) ctab[c] = a.chunk_g[c];
     if (tid < kBars) mbar_init(&bars[tid], 1);
     if (tid < 2) {  // null records
         int* nr = reinterpret_cast<int*>(nullrec + 128 * tid);
@@ -157,52 +205,41 @@ __global__ void __launch_bounds__(384, 1) k_gs_walk(WalkArgs a) {
         nr[3] = dummy;  // pin
         for (int k = 0; k < kMaxK; ++k) nr[(tid ? 20 : 8) + k] = zero_slot;
     }
-    if (tid == 0) zr[zero_slot] = 0.0;
+    if (tid == 0) {
+        zr[zero_slot] = 0.0;
+        flags[0] = 0;
+        flags[1] = 0;
+    }
     fence_mbar_init();
     __syncthreads();
 
     if (wc >= 0) {
         if (wc < a.w2)
-            walk_consumer<true>(a, meta, stage, nullrec, zr, wc * 32 + lane);
+            walk_consumer<true>(a, meta, stage, nullrec, zr, flags, wc * 32 + lane);
         else
-            walk_consumer<false>(a, meta, stage, nullrec, zr, (wc - a.w2) * 32 + lane);
+            walk_consumer<false>(a, meta, stage, nullrec, zr, flags, (wc - a.w2) * 32 + lane);
         return;
     }
-    // producer warp: thread 0 issues chunk copies and waits for the chunk of
-    // the level two ahead before each level barrier
-    int ci = 0, cw = 0, ci_after = INT_MAX, cw_first = INT_MAX;
-    int4 cd = make_int4(0, 0, 0, 0);
-    auto issue_upto = [&](int done) {
-        while (ci_after <= done) {
+    if (tid != 0) return;
+    // producer: issue chunk copies once the consumers' progress frees their
+    // ring space, publish each chunk once it has landed
+    int ci = 0, cw = 0;
+    while (cw < nc) {
+        const int done = ld_volatile(&flags[0]) - 1;  // last completed level
+        while (ci < nc && ci < cw + kBars && ctab[ci].w <= done) {
+            const int4 cd = ctab[ci];
             uint64_t* bar = &bars[ci % kBars];
             mbar_expect_tx(bar, static_cast<unsigned>(cd.y));
             tma_load_1d(stage + cd.z, a.packed + static_cast<size_t>(cd.x) * 16, static_cast<unsigned>(cd.y), bar);
             ++ci;
-            cd = ci < nc ? ctab[ci] : make_int4(0, 0, 0, INT_MAX);
-            ci_after = cd.w;
         }
-    };
-    auto wait_upto = [&](int level) {
-        while (cw_first <= level) {
-            mbar_wait(&bars[cw % kBars], static_cast<unsigned>(cw / kBars) & 1u);
+        if (cw < ci && mbar_test(&bars[cw % kBars], static_cast<unsigned>(cw / kBars) & 1u)) {
+            __threadfence_block();
             ++cw;
-            cw_first = cw < nc ? cfirst[cw] : INT_MAX;
+            st_volatile(&flags[1], cw);
+        } else {
+            __nanosleep(20);
         }
-    };
-    if (tid == 0 && nc > 0) {
-        cd = ctab[0];
-        ci_after = cd.w;
-        cw_first = cfirst[0];
-        issue_upto(-1);
-        wait_upto(1);
-    }
-    __syncthreads();  // levels 0 and 1 landed; consumers fetch their level-0 rows
-    for (int L = 0; L < nl; ++L) {
-        if (tid == 0) {
-            issue_upto(L - 1);
-            wait_upto(L + 2);
-        }
-        __syncthreads();
     }
 }
 
@@ -252,6 +289,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     if (off / 16 >= (static_cast<int64_t>(1) << 31)) return false;
     const int max_warps = std::max(1, max_w2 + max_w8);
     if (max_warps > kMaxWarps) return false;  // one row per consumer thread and level
+    if (n >= (1 << 20) || nl >= (1 << 13)) return false;  // meta packing
 
     // chunks of consecutive levels
     std::vector<int> cfirst, cbytes;
@@ -302,7 +340,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
                 }
             }
         zbytes = pad16(static_cast<int64_t>(ring + 2 + npin) * 8);
-        fixed = kBars * 8 + kNullBytes + meta_bytes + chunk_bytes + cfirst_bytes + zbytes;
+        fixed = kBars * 8 + 16 + kNullBytes + meta_bytes + chunk_bytes + cfirst_bytes + zbytes;
         R = (budget - fixed) / 16 * 16;
         if (R >= min_stage) break;
         if (ring <= 64 || ring / 2 < 2 * max_rows) return false;
@@ -371,7 +409,9 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
                 src[m] = zero_slot;
             }
         }
-        meta_h[q] = make_int4(roff[chunk_of[q]] + in_chunk[q], n2[q], n8[q], lptr[q]);
+        const int starts = cfirst[chunk_of[q]] == q ? chunk_of[q] + 1 : 0;  // chunk id + 1 if q starts a chunk
+        const int o2 = roff[chunk_of[q]] + in_chunk[q], o8 = o2 + n2[q] * kK2Bytes;
+        meta_h[q] = make_int4(o2, o8 | (starts << 18), lptr[q] | (n2[q] << 20), (lptr[q] + n2[q]) | (n8[q] << 20));
     }
     meta_h[nl] = make_int4(0, 0, 0, 0);  // sentinel: the prefetch past the last level reads null rows
     for (int c = 0; c < nc; ++c)

@@ -57,6 +57,40 @@ int main(int argc, char** argv) {
         zc[i] = acc;
         maxd = std::max(maxd, std::abs(acc - hz[i]) / std::abs(acc));
     }
+#ifdef SDG_WALK_TRACE
+    {
+        std::vector<long long> tr(1024 * 16 * 4);
+        cudaMemcpyFromSymbol(tr.data(), g_walk_trace, tr.size() * 8);
+        const int nw = g.nthreads / 32;
+        std::vector<double> arr(nw, 0), solve(nw, 0), fetch(nw, 0), topoff(nw, 0), arroff(nw, 0);
+        double rel = 0, spread = 0;
+        int m = 0;
+        for (int L = 5; L + 1 < g.n_levels && L < 1000; ++L, ++m) {
+            long long amax = 0, amin = 1LL << 62, rmin = 1LL << 62;
+            for (int w = 0; w < nw; ++w) {
+                const long long* t = &tr[(L * 16 + w) * 4];
+                const long long* tn = &tr[((L + 1) * 16 + w) * 4];
+                amax = std::max(amax, t[2]);
+                amin = std::min(amin, t[2]);
+                rmin = std::min(rmin, tn[0]);
+                arr[w] += t[2] - t[0];
+                if (w > 0) { solve[w] += t[1] - t[0]; fetch[w] += t[2] - t[1]; }
+            }
+            long long tmin = 1LL << 62;
+            for (int w = 0; w < nw; ++w) tmin = std::min(tmin, tr[(L * 16 + w) * 4]);
+            for (int w = 0; w < nw; ++w) {
+                topoff[w] += tr[(L * 16 + w) * 4] - tmin;
+                arroff[w] += tr[(L * 16 + w) * 4 + 2] - tmin;
+            }
+            rel += rmin - amax;
+            spread += amax - amin;
+        }
+        printf("per level: last arrival -> first release %.0f, arrival spread %.0f\n", rel / m, spread / m);
+        for (int w = 0; w < nw; ++w)
+            printf("  warp %d: top->arrive %.0f (solve %.0f fetch %.0f) top offset %.0f arrive offset %.0f\n", w,
+                   arr[w] / m, solve[w] / m, fetch[w] / m, topoff[w] / m, arroff[w] / m);
+    }
+#endif
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     printf("nx %d levels %d threads %d: %.2f us/launch, %.0f cycles/level, rel err %.1e (%s)\n",
