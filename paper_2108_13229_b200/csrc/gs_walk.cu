@@ -53,7 +53,7 @@ constexpr int kBars = 32;      // chunk mbarriers (chunks in flight at most)
 constexpr int kK2Bytes = 48;
 constexpr int kK8Bytes = 112;
 constexpr int kMaxK = 8;
-constexpr int kMaxWarps = 11;  // consumer warps (384 threads with the producer warp)
+constexpr int kMaxWarps = 15;  // consumer warps (512 threads with the producer warp)
 constexpr int kChunkBytes = 16 * 1024;
 constexpr int kSmemCap = 227 * 1024;
 constexpr int kNullBytes = 256;  // null K2 record at +0, null K8 record at +128
@@ -179,7 +179,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     }
 }
 
-__global__ void __launch_bounds__(384, 1) k_gs_walk(WalkArgs a) {
+__global__ void __launch_bounds__(512, 1) k_gs_walk(WalkArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
     int* flags = reinterpret_cast<int*>(sm + kBars * 8);  // {levels done, chunks landed}
@@ -250,7 +250,11 @@ __global__ void __launch_bounds__(384, 1) k_gs_walk(WalkArgs a) {
 // staging ring); the caller then builds the banded plan.
 bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, const std::vector<int>& nlow,
                         int max_k, cudaStream_t s) {
-    if (max_k > kMaxK) return false;
+    auto reject = [&](const char* why) {
+        if (std::getenv("SDG_DEBUG")) std::fprintf(stderr, "[sdg gs walk] n=%d: not used (%s)\n", a.n_rows, why);
+        return false;
+    };
+    if (max_k > kMaxK) return reject("a row has more than 8 lower entries");
     n = a.n_rows;
     std::vector<int> lev(n, 0);
     int nl = 0;
@@ -261,35 +265,54 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         lev[i] = d;
         nl = std::max(nl, d + 1);
     }
-    std::vector<int> n2(nl, 0), n8(nl, 0);
-    for (int i = 0; i < n; ++i) ++(nlow[i] <= 2 ? n2 : n8)[lev[i]];
-    std::vector<int> lptr(nl + 1, 0), fill2(nl), fill8(nl), order(n), pos(n);
+    // classes: w2 warps take rows with <= 2 lower entries (48-byte records),
+    // the other warps everything else (112-byte records), including the
+    // small rows of a level that has more of them than the w2 warps hold;
+    // w2 minimises the consumer warp count
+    std::vector<int> c2(nl, 0), c8(nl, 0);
+    for (int i = 0; i < n; ++i) ++(nlow[i] <= 2 ? c2 : c8)[lev[i]];
+    int w2 = 0, w8 = 1 << 20;
+    for (int cand = 0; cand <= kMaxWarps; ++cand) {
+        int need8 = 0;
+        for (int q = 0; q < nl; ++q)
+            need8 = std::max(need8, (c8[q] + std::max(0, c2[q] - 32 * cand) + 31) / 32);
+        if (cand + need8 < w2 + w8 || (cand + need8 == w2 + w8 && cand > w2)) {
+            w2 = cand;
+            w8 = need8;
+        }
+    }
+    const int max_warps = std::max(1, w2 + w8);
+    if (max_warps > kMaxWarps) return reject("levels wider than the block");
+    std::vector<int> n2(nl), n8(nl);
+    for (int q = 0; q < nl; ++q) {
+        n2[q] = std::min(c2[q], 32 * w2);
+        n8[q] = c8[q] + c2[q] - n2[q];
+    }
+    std::vector<int> lptr(nl + 1, 0), fill2(nl), fill8(nl), order(n), pos(n), seen2(nl, 0);
     for (int q = 0; q < nl; ++q) lptr[q + 1] = lptr[q] + n2[q] + n8[q];
     for (int q = 0; q < nl; ++q) {
         fill2[q] = lptr[q];
         fill8[q] = lptr[q] + n2[q];
     }
     for (int i = 0; i < n; ++i) {
-        const int p = (nlow[i] <= 2 ? fill2 : fill8)[lev[i]]++;
+        const int q = lev[i];
+        const bool small = nlow[i] <= 2 && seen2[q]++ < n2[q];
+        const int p = (small ? fill2 : fill8)[q]++;
         order[p] = i;
         pos[i] = p;
     }
-    int max_rows = 1, max_w2 = 0, max_w8 = 0;
+    int max_rows = 1;
     std::vector<int> lbytes(nl);
     std::vector<int64_t> goff(nl);
     int64_t off = 0;
     for (int q = 0; q < nl; ++q) {
         max_rows = std::max(max_rows, n2[q] + n8[q]);
-        max_w2 = std::max(max_w2, (n2[q] + 31) / 32);
-        max_w8 = std::max(max_w8, (n8[q] + 31) / 32);
         lbytes[q] = n2[q] * kK2Bytes + n8[q] * kK8Bytes;
         goff[q] = off;
         off += lbytes[q];
     }
-    if (off / 16 >= (static_cast<int64_t>(1) << 31)) return false;
-    const int max_warps = std::max(1, max_w2 + max_w8);
-    if (max_warps > kMaxWarps) return false;  // one row per consumer thread and level
-    if (n >= (1 << 20) || nl >= (1 << 13)) return false;  // meta packing
+    if (off / 16 >= (static_cast<int64_t>(1) << 31)) return reject("packed buffer too large");
+    if (n >= (1 << 20) || nl >= (1 << 13)) return reject("too many rows or levels for the meta packing");
 
     // chunks of consecutive levels
     std::vector<int> cfirst, cbytes;
@@ -343,7 +366,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         fixed = kBars * 8 + 16 + kNullBytes + meta_bytes + chunk_bytes + cfirst_bytes + zbytes;
         R = (budget - fixed) / 16 * 16;
         if (R >= min_stage) break;
-        if (ring <= 64 || ring / 2 < 2 * max_rows) return false;
+        if (ring <= 64 || ring / 2 < 2 * max_rows) return reject("shared memory: ring + pinned values + staging");
         ring >>= 1;
     }
     const int zero_slot = ring, dummy_slot = ring + 1, pin_base = ring + 2;
@@ -366,7 +389,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
                 break;
             }
         }
-        if (aft >= 0 && aft > cfirst[c] - 3) return false;
+        if (aft >= 0 && aft > cfirst[c] - 3) return reject("staging ring too small for the look-ahead");
         after[c] = aft;
         cur += sz;
     }
@@ -428,7 +451,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     walk_cfirst_bytes = cfirst_bytes;
     walk_zbytes = zbytes;
     walk_chunks = nc;
-    walk_w2 = max_w2;
+    walk_w2 = w2;
     max_seg = max_chunk;
     halo = npin;
     smem = static_cast<size_t>(fixed) + R;
