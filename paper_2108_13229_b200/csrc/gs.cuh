@@ -55,10 +55,9 @@ struct GsPlan {
     int64_t global_refs = 0;
     int meta_bytes_ = 0, chunk_tab_bytes_ = 0, pbar_bytes_ = 0;
     bool walk = false;         // single-CTA walk (gs_walk.cu) instead of the banded cluster kernel
-    int walk_meta_bytes = 0, walk_chunk_bytes = 0, walk_cfirst_bytes = 0, walk_zbytes = 0, walk_chunks = 0;
-    int walk_w2 = 0;           // consumer warps owning the <= 2-entry rows
+    int walk_meta_bytes = 0, walk_chunk_bytes = 0, walk_zbytes = 0, walk_chunks = 0;
+    int walk_r2 = 1, walk_r8 = 0;  // rows per consumer thread and level (<= 2-entry / wider rows)
     DevBuf<int4> walk_iss;     // per chunk {global off16, bytes, stage off, issue after level}
-    DevBuf<int> walk_cfirst;   // per chunk: first level
     DevBuf<int4> meta;         // per (band, level) {chunk-local off16, nS | global flag << 31, nL | nE << 16, chunk}
     DevBuf<int4> chunk_tab;    // per (band, chunk) {off16, bytes16, first level, levels}
     DevBuf<int4> band_info;    // per band {meta base, n levels, packet base, n packets}, then {chunk base, n chunks}

@@ -1,9 +1,11 @@
 // Single-CTA lower solve of the fast Gauss-Seidel smoother (one band; see
 // gs.cuh for the prep / lower split and gs.cu for the banded cluster kernel).
 //
-// The rows of each dependency level are split into two classes, each an array
-// of fixed-size records (16-byte vector loads with immediate offsets; 48 and
-// 112 are odd multiples of 16, so a warp's loads are bank-conflict free):
+// Rows are walked level by level (a level = rows whose lower dependencies are
+// all in earlier levels).  The rows of a level are split into two classes,
+// each an array of fixed-size records (16-byte vector loads with immediate
+// offsets; 48 and 112 are odd multiples of 16, so a warp's loads are
+// bank-conflict free):
 //   K2 (<= 2 lower entries, 48 B): { double b; int rowid; int pin; double v[2]; int src[2]; int pad[2] }
 //   K8 (3..8 lower entries, 112 B): { double b; int rowid; int pin; double v[8]; int src[8] }
 // b = (r - U z_old)_i / d_i (written by the prep kernels), v = -a_ij / d_i, so
@@ -13,23 +15,29 @@
 // `pin` is where a row also stores its value (a dummy slot when nobody needs
 // it late).  The ring slot of a row is its level-order position.
 //
-// Warps own one class for a whole level (the first ceil(n2/32) consumer warps
-// take K2 rows, the next ceil(n8/32) K8 rows); lanes past the end of their
-// class point at a null record in shared memory (b = 0, sources = zero slot,
-// stores to a dummy slot, rowid -1), so the per-row path has no branches.
-// Consecutive levels are grouped into chunks that one TMA bulk copy (issued by
-// thread 0) brings into a byte ring of shared memory; the host plan places
-// every chunk and names the level after whose barrier it may overwrite older
-// bytes.  Thread 0 also waits for the chunk of the level two ahead before
-// joining the level barrier, so consumers never touch mbarriers.  Consumers
-// hold the next level's row in registers (ping-pong between two register
-// sets), and the per-level critical path is
-//   barrier -> shared gathers -> two FMAs -> shared store -> barrier.
+// W consumer warps each hold R2 K2 rows and R8 K8 rows per level (row slot
+// r * 32W + 32 * warp + lane); a level wider than that is split into several
+// consecutive pseudo-levels (its rows are independent).  Slots past the end
+// of a class point at a null record (b = 0, sources = zero slot, stores to a
+// dummy slot, rowid -1), so the per-row path has no branches.  With W = 1 the
+// level hand-off is a __syncwarp: no CTA barrier at all.  The host plan picks
+// (W, R2, R8) per system from a cost model.
+//
+// Consecutive levels are grouped into chunks that one TMA bulk copy brings
+// into a byte ring of shared memory.  A producer thread (warp 0, lane 0)
+// issues each copy once the consumers' published progress shows that the
+// bytes it overwrites are dead, and publishes a `landed` count as copies
+// complete; a consumer checks it only at the first level of a chunk.  The
+// producer is not part of the level barrier.  Each level of a consumer warp:
+// gathers + coefficient loads for all its rows, FMAs, ring stores, prefetch
+// of the next level's records, level hand-off.
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "gs.cuh"
 #include "ptx.cuh"
@@ -49,30 +57,33 @@ __device__ long long g_walk_trace[1024 * 16 * 4];
 #define WALK_CLK(L, k)
 #endif
 
-constexpr int kBars = 32;      // chunk mbarriers (chunks in flight at most)
+constexpr int kBars = 32;  // chunk mbarriers (chunks in flight at most)
 constexpr int kK2Bytes = 48;
 constexpr int kK8Bytes = 112;
 constexpr int kMaxK = 8;
-constexpr int kMaxWarps = 15;  // consumer warps (512 threads with the producer warp)
+constexpr int kMaxR2 = 6, kMaxR8 = 3;
 constexpr int kChunkBytes = 16 * 1024;
 constexpr int kSmemCap = 227 * 1024;
 constexpr int kNullBytes = 256;  // null K2 record at +0, null K8 record at +128
 
 inline int pad16(int64_t b) { return static_cast<int>((b + 15) / 16 * 16); }
 
-struct WalkArgs {
-    const int4* meta_g;    // per level (+1 sentinel) {stage off, n2, n8, pos base}
-    const int4* chunk_g;   // per chunk {global off / 16, bytes, stage off, may issue after the barrier of this level}
-    const int* cfirst_g;   // per chunk: its first level
-    const unsigned char* packed;
-    int n_levels, n_chunks, ring, meta_bytes, chunk_bytes, cfirst_bytes, zbytes;
-    int w2;                // consumer warps that own K2 rows (the rest own K8 rows)
-    double* z_new;
-};
+// threads per CTA an instantiation may use (register budget)
+constexpr int max_threads(int r2, int r8) {
+    return r2 + 2 * r8 <= 3 ? 512 : r2 + 2 * r8 <= 5 ? 384 : r2 + 2 * r8 <= 7 ? 256 : 128;
+}
 
 __device__ __forceinline__ int ld_volatile(const int* p) {
     int v;
     asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+
+// acquire: the staged records read after observing `landed` must not be
+// hoisted above it (plain shared loads may be reordered before a volatile one)
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
     return v;
 }
 
@@ -90,112 +101,164 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
     return done != 0;
 }
 
-// The level loop of one consumer warp.  Every warp owns one class for the
-// whole sweep (thread t of the class: t-th row of that class at every level),
-// so the loop has no class branches.  Per level: the gathers, coefficient and
-// next-level meta loads are issued together, the row is finished and stored,
-// and the next level's record is requested before the barrier (it lands while
-// the barrier completes).  The level barrier is a named barrier of the
-// consumer warps only; a level that starts a chunk first checks the
-// producer's `landed` counter.
-template <bool K2>
+struct WalkArgs {
+    const int4* meta_g;   // per level (+2 sentinels) {K2 stage off, K8 stage off | chunk-start << 18,
+                          //   K2 pos | n2 << 20, K8 pos | n8 << 20}
+    const int4* chunk_g;  // per chunk {global off / 16, bytes, stage off, may issue once this level is done}
+    const unsigned char* packed;
+    int n_levels, n_chunks, ring, meta_bytes, chunk_bytes, zbytes;
+    double* z_new;
+};
+
+// Rows a consumer thread holds for one level: R2 small + R8 wide rows (the
+// sources, scalars and the shared address of each record's coefficients).
+template <int R2, int R8>
+struct WalkRows {
+    double b2[R2 > 0 ? R2 : 1], b8[R8 > 0 ? R8 : 1];
+    int s2[R2 > 0 ? R2 : 1][2], s8[R8 > 0 ? R8 : 1][kMaxK];
+    int rid2[R2 > 0 ? R2 : 1], pin2[R2 > 0 ? R2 : 1], wp2[R2 > 0 ? R2 : 1];
+    int rid8[R8 > 0 ? R8 : 1], pin8[R8 > 0 ? R8 : 1], wp8[R8 > 0 ? R8 : 1];
+    const unsigned char* vp2[R2 > 0 ? R2 : 1];
+    const unsigned char* vp8[R8 > 0 ? R8 : 1];
+};
+
+// The level loop of one consumer warp (see the file comment).  Records are
+// fetched two levels ahead (two register sets, alternating), so neither the
+// record loads nor their addresses are on the per-level critical path
+//   gathers (shared) -> FMAs -> ring store -> level hand-off.
+template <int R2, int R8>
 __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* meta, const unsigned char* stage,
-                                              const unsigned char* nullrec, double* zr, int* flags, int t) {
+                                              const unsigned char* nullrec, double* zr, int* flags) {
     const int mask = a.ring - 1, dummy = a.ring + 1;
-    const unsigned ncons = blockDim.x - 32;
-    constexpr int K = K2 ? 2 : kMaxK;
-    constexpr int RB = K2 ? kK2Bytes : kK8Bytes;
-    double b;
-    int s[K], rowid, pin, wpos;
-    const unsigned char* vrec;
-    // meta = {K2 stage offset, K8 stage offset | chunk-start << 18, K2 pos | n2 << 20, K8 pos | n8 << 20}
-    const unsigned char* nrec = nullrec + (K2 ? 0 : 128);
-    const int toff = t * RB;
-    auto fetch = [&](const int4 m) {
-        const int off = K2 ? m.x : (m.y & 0x3ffff);
-        const int pn = K2 ? m.z : m.w;
-        const bool ok = t < (pn >> 20);
-        const unsigned char* q = ok ? stage + off + toff : nrec;
-        const int4 h = *reinterpret_cast<const int4*>(q);
-        if (K2) {
-            const int2 ss = *reinterpret_cast<const int2*>(q + 32);
-            s[0] = ss.x;
-            s[1] = ss.y;
-        } else {
-            const int4 s0 = *reinterpret_cast<const int4*>(q + 80);
-            const int4 s1 = *reinterpret_cast<const int4*>(q + 96);
-            s[0] = s0.x; s[1] = s0.y; s[2 % K] = s0.z; s[3 % K] = s0.w;
-            s[4 % K] = s1.x; s[5 % K] = s1.y; s[6 % K] = s1.z; s[7 % K] = s1.w;
-        }
-        b = __hiloint2double(h.y, h.x);
-        rowid = h.z;
-        pin = h.w;
-        vrec = q + 16;
-        wpos = ok ? (((pn & 0xfffff) + t) & mask) : dummy;
-    };
+    const int nw = (blockDim.x >> 5) - 1;
+    const int t0 = threadIdx.x - 32;  // (warp - 1) * 32 + lane
+    const int stride = 32 * nw;
     int* progress = flags;
     const int* landed = flags + 1;
-    {
-        const int4 m0 = meta[0];
-        const int need = static_cast<unsigned>(m0.y) >> 18;
-        while (ld_volatile(landed) < need) {
-        }
-        fetch(m0);
-    }
-    for (int L = 0; L < a.n_levels; ++L) {
-        WALK_CLK(L, 0);
-        double z[K], v[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) z[k] = zr[s[k]];
-#pragma unroll
-        for (int k = 0; k < K / 2; ++k) {
-            const double2 c = reinterpret_cast<const double2*>(vrec)[k];
-            v[2 * k] = c.x;
-            v[2 * k + 1] = c.y;
-        }
-        const int4 mn = meta[L + 1];
-        const int need = static_cast<unsigned>(mn.y) >> 18;  // chunk id + 1 when level L+1 starts a chunk
+    using Rows = WalkRows<R2, R8>;
+    auto wait_landed = [&](const int4 m) {
+        const int need = static_cast<unsigned>(m.y) >> 18;  // chunk id + 1 when the level starts a chunk
         if (need)
-            while (ld_volatile(landed) < need) {
+            while (ld_acquire(landed) < need) {
             }
-        double acc;
-        if (K2) {
-            acc = fma(v[1], z[1], fma(v[0], z[0], b));
-        } else {
-            const double q0 = fma(v[1], z[1], fma(v[0], z[0], b));
-            const double q1 = fma(v[3 % K], z[3 % K], v[2 % K] * z[2 % K]);
-            const double q2 = fma(v[5 % K], z[5 % K], v[4 % K] * z[4 % K]);
-            const double q3 = fma(v[7 % K], z[7 % K], v[6 % K] * z[6 % K]);
-            acc = (q0 + q1) + (q2 + q3);
+    };
+    auto fetch = [&](Rows& x, const int4 m) {
+#pragma unroll
+        for (int r = 0; r < R2; ++r) {
+            const int u = r * stride + t0;
+            const bool ok = u < (m.z >> 20);
+            const unsigned char* q = ok ? stage + m.x + u * kK2Bytes : nullrec;
+            const int4 h = *reinterpret_cast<const int4*>(q);
+            const int2 ss = *reinterpret_cast<const int2*>(q + 32);
+            x.b2[r] = __hiloint2double(h.y, h.x);
+            x.rid2[r] = h.z;
+            x.pin2[r] = h.w;
+            x.s2[r][0] = ss.x;
+            x.s2[r][1] = ss.y;
+            x.vp2[r] = q + 16;
+            x.wp2[r] = ok ? (((m.z & 0xfffff) + u) & mask) : dummy;
         }
-        zr[wpos] = acc;
-        zr[pin] = acc;
-        if (rowid >= 0) a.z_new[rowid] = acc;
+#pragma unroll
+        for (int r = 0; r < R8; ++r) {
+            const int u = r * stride + t0;
+            const bool ok = u < (m.w >> 20);
+            const unsigned char* q = ok ? stage + (m.y & 0x3ffff) + u * kK8Bytes : nullrec + 128;
+            const int4 h = *reinterpret_cast<const int4*>(q);
+            const int4 x0 = *reinterpret_cast<const int4*>(q + 80);
+            const int4 x1 = *reinterpret_cast<const int4*>(q + 96);
+            x.b8[r] = __hiloint2double(h.y, h.x);
+            x.rid8[r] = h.z;
+            x.pin8[r] = h.w;
+            x.s8[r][0] = x0.x; x.s8[r][1] = x0.y; x.s8[r][2] = x0.z; x.s8[r][3] = x0.w;
+            x.s8[r][4] = x1.x; x.s8[r][5] = x1.y; x.s8[r][6] = x1.z; x.s8[r][7] = x1.w;
+            x.vp8[r] = q + 16;
+            x.wp8[r] = ok ? (((m.w & 0xfffff) + u) & mask) : dummy;
+        }
+    };
+    // solve the rows of level L held in x, then fetch level L+2 into x
+    auto step = [&](int L, Rows& x) {
+        WALK_CLK(L, 0);
+        double z2[R2 > 0 ? R2 : 1][2], v2[R2 > 0 ? R2 : 1][2];
+        double z8[R8 > 0 ? R8 : 1][kMaxK], v8[R8 > 0 ? R8 : 1][kMaxK];
+#pragma unroll
+        for (int r = 0; r < R2; ++r) {
+            z2[r][0] = zr[x.s2[r][0]];
+            z2[r][1] = zr[x.s2[r][1]];
+            const double2 c = *reinterpret_cast<const double2*>(x.vp2[r]);
+            v2[r][0] = c.x;
+            v2[r][1] = c.y;
+        }
+#pragma unroll
+        for (int r = 0; r < R8; ++r) {
+#pragma unroll
+            for (int k = 0; k < kMaxK; ++k) z8[r][k] = zr[x.s8[r][k]];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double2 c = reinterpret_cast<const double2*>(x.vp8[r])[k];
+                v8[r][2 * k] = c.x;
+                v8[r][2 * k + 1] = c.y;
+            }
+        }
+        const int4 m2 = meta[L + 2];
+#pragma unroll
+        for (int r = 0; r < R2; ++r) {
+            const double acc = fma(v2[r][1], z2[r][1], fma(v2[r][0], z2[r][0], x.b2[r]));
+            zr[x.wp2[r]] = acc;
+            zr[x.pin2[r]] = acc;
+            if (x.rid2[r] >= 0) a.z_new[x.rid2[r]] = acc;
+        }
+#pragma unroll
+        for (int r = 0; r < R8; ++r) {
+            const double* v = v8[r];
+            const double* z = z8[r];
+            const double q0 = fma(v[1], z[1], fma(v[0], z[0], x.b8[r]));
+            const double q1 = fma(v[3], z[3], v[2] * z[2]);
+            const double q2 = fma(v[5], z[5], v[4] * z[4]);
+            const double q3 = fma(v[7], z[7], v[6] * z[6]);
+            const double acc = (q0 + q1) + (q2 + q3);
+            zr[x.wp8[r]] = acc;
+            zr[x.pin8[r]] = acc;
+            if (x.rid8[r] >= 0) a.z_new[x.rid8[r]] = acc;
+        }
         WALK_CLK(L, 1);
-        fetch(mn);
+        wait_landed(m2);
+        fetch(x, m2);
         WALK_CLK(L, 2);
-        asm volatile("bar.sync 1, %0;" ::"r"(ncons) : "memory");
+        if (nw == 1)
+            __syncwarp();
+        else
+            asm volatile("bar.sync 1, %0;" ::"r"(stride) : "memory");
         if (threadIdx.x == 32) st_volatile(progress, L + 1);
+    };
+    Rows x, y;
+    {
+        const int4 m0 = meta[0], m1 = meta[1];
+        wait_landed(m0);
+        fetch(x, m0);
+        wait_landed(m1);
+        fetch(y, m1);
+    }
+    for (int L = 0; L < a.n_levels; L += 2) {
+        step(L, x);
+        if (L + 1 < a.n_levels) step(L + 1, y);
     }
 }
 
-__global__ void __launch_bounds__(512, 1) k_gs_walk(WalkArgs a) {
+template <int R2, int R8>
+__global__ void __launch_bounds__(max_threads(R2, R8), 1) k_gs_walk(WalkArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
     int* flags = reinterpret_cast<int*>(sm + kBars * 8);  // {levels done, chunks landed}
     unsigned char* nullrec = sm + kBars * 8 + 16;
     int4* meta = reinterpret_cast<int4*>(nullrec + kNullBytes);
     int4* ctab = reinterpret_cast<int4*>(reinterpret_cast<unsigned char*>(meta) + a.meta_bytes);
-    int* cfirst = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(ctab) + a.chunk_bytes);
-    double* zr = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(cfirst) + a.cfirst_bytes);
+    double* zr = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ctab) + a.chunk_bytes);
     unsigned char* stage = reinterpret_cast<unsigned char*>(zr) + a.zbytes;
     const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int wc = (tid >> 5) - 1;  // consumer warp index (-1: producer warp)
     const int nl = a.n_levels, nc = a.n_chunks;
     const int zero_slot = a.ring, dummy = a.ring + 1;
 
-    for (int l = tid; l <= nl; l += blockDim.x) meta[l] = a.meta_g[l];
+    for (int l = tid; l <= nl + 1; l += blockDim.x) meta[l] = a.meta_g[l];
     for (int c = tid; c < nc; c += blockDim.x) ctab[c] = a.chunk_g[c];
     if (tid < kBars) mbar_init(&bars[tid], 1);
     if (tid < 2) {  // null records
@@ -213,11 +276,8 @@ __global__ void __launch_bounds__(512, 1) k_gs_walk(WalkArgs a) {
     fence_mbar_init();
     __syncthreads();
 
-    if (wc >= 0) {
-        if (wc < a.w2)
-            walk_consumer<true>(a, meta, stage, nullrec, zr, flags, wc * 32 + lane);
-        else
-            walk_consumer<false>(a, meta, stage, nullrec, zr, flags, (wc - a.w2) * 32 + lane);
+    if (tid >= 32) {
+        walk_consumer<R2, R8>(a, meta, stage, nullrec, zr, flags);
         return;
     }
     if (tid != 0) return;
@@ -234,20 +294,40 @@ __global__ void __launch_bounds__(512, 1) k_gs_walk(WalkArgs a) {
             ++ci;
         }
         if (cw < ci && mbar_test(&bars[cw % kBars], static_cast<unsigned>(cw / kBars) & 1u)) {
-            __threadfence_block();
             ++cw;
-            st_volatile(&flags[1], cw);
+            asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_addr(&flags[1])), "r"(cw) : "memory");
         } else {
             __nanosleep(20);
         }
     }
 }
 
+using WalkKernel = void (*)(WalkArgs);
+
+template <int R2, int R8>
+constexpr WalkKernel kernel_of() {
+    return &k_gs_walk<R2, R8>;
+}
+
+// all instantiations, indexed [R2 - 1][R8]
+template <int... I>
+constexpr auto make_table(std::integer_sequence<int, I...>) {
+    struct T {
+        WalkKernel k[sizeof...(I)];
+    };
+    return T{{kernel_of<I / (kMaxR8 + 1) + 1, I % (kMaxR8 + 1)>()...}};
+}
+
+WalkKernel walk_kernel(int r2, int r8) {
+    static const auto table = make_table(std::make_integer_sequence<int, kMaxR2 * (kMaxR8 + 1)>{});
+    return table.k[(r2 - 1) * (kMaxR8 + 1) + r8];
+}
+
 }  // namespace
 
 // Returns false when the system does not fit the walk (rows with more than 8
-// lower entries, levels wider than the block, a level too large for the
-// staging ring); the caller then builds the banded plan.
+// lower entries, a level too large for the staging ring); the caller then
+// builds the banded plan.
 bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, const std::vector<int>& nlow,
                         int max_k, cudaStream_t s) {
     auto reject = [&](const char* why) {
@@ -256,48 +336,94 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     };
     if (max_k > kMaxK) return reject("a row has more than 8 lower entries");
     n = a.n_rows;
+    if (n >= (1 << 20)) return reject("too many rows for the meta packing");
     std::vector<int> lev(n, 0);
-    int nl = 0;
+    int nlv = 0;
     for (int i = 0; i < n; ++i) {
         int d = 0;
         for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
             if (a.ci[k] < i) d = std::max(d, lev[a.ci[k]] + 1);
         lev[i] = d;
-        nl = std::max(nl, d + 1);
+        nlv = std::max(nlv, d + 1);
     }
-    // classes: w2 warps take rows with <= 2 lower entries (48-byte records),
-    // the other warps everything else (112-byte records), including the
-    // small rows of a level that has more of them than the w2 warps hold;
-    // w2 minimises the consumer warp count
-    std::vector<int> c2(nl, 0), c8(nl, 0);
+    std::vector<int> c2(nlv, 0), c8(nlv, 0);
     for (int i = 0; i < n; ++i) ++(nlow[i] <= 2 ? c2 : c8)[lev[i]];
-    int w2 = 0, w8 = 1 << 20;
-    for (int cand = 0; cand <= kMaxWarps; ++cand) {
-        int need8 = 0;
-        for (int q = 0; q < nl; ++q)
-            need8 = std::max(need8, (c8[q] + std::max(0, c2[q] - 32 * cand) + 31) / 32);
-        if (cand + need8 < w2 + w8 || (cand + need8 == w2 + w8 && cand > w2)) {
-            w2 = cand;
-            w8 = need8;
+
+    // (W, R2, R8) from a cost model in cycles per pseudo-level, fitted to
+    // B200 measurements (scripts/mb_real2.cu): a latency chain that grows
+    // slowly with the warps and rows per thread, or the shared-memory traffic
+    // (records staged and read back, gathers) when that is larger
+    int best_w = 0, best_r2 = 0, best_r8 = 0;
+    double best_cost = 1e300;
+    for (int w : {1, 2, 3, 4, 5, 6, 8, 11, 15})
+        for (int r2 = 1; r2 <= kMaxR2; ++r2)
+            for (int r8 = 0; r8 <= kMaxR8; ++r8) {
+                if (32 + 32 * w > max_threads(r2, r8)) continue;
+                const int cap2 = 32 * w * r2, cap8 = 32 * w * r8;
+                const double chain = 220.0 + 15.0 * w + 35.0 * (r2 - 1) + 60.0 * r8;
+                double cost = 0;
+                bool ok = true;
+                for (int q = 0; q < nlv && ok; ++q) {
+                    if (c8[q] > 0 && r8 == 0) ok = false;
+                    const int p = std::max({1, (c2[q] + cap2 - 1) / cap2, r8 ? (c8[q] + cap8 - 1) / cap8 : 1});
+                    const double bw = (2.0 * (c2[q] * kK2Bytes + c8[q] * kK8Bytes) + 40.0 * c2[q] + 100.0 * c8[q]) /
+                                      (128.0 * p);
+                    cost += p * std::max(chain, bw);
+                }
+                if (ok && cost < best_cost) {
+                    best_cost = cost;
+                    best_w = w;
+                    best_r2 = r2;
+                    best_r8 = r8;
+                }
+            }
+    if (const char* e = std::getenv("SDG_WALK_SHAPE")) {  // dev override "warps,r2,r8"
+        int w = 0, r2 = 0, r8 = 0;
+        if (std::sscanf(e, "%d,%d,%d", &w, &r2, &r8) == 3 && w >= 1 && r2 >= 1 && r2 <= kMaxR2 && r8 >= 0 &&
+            r8 <= kMaxR8 && 32 + 32 * w <= max_threads(r2, r8)) {
+            bool ok = true;
+            for (int q = 0; q < nlv; ++q) ok = ok && (r8 > 0 || c8[q] == 0);
+            if (ok) {
+                best_w = w;
+                best_r2 = r2;
+                best_r8 = r8;
+            }
         }
     }
-    const int max_warps = std::max(1, w2 + w8);
-    if (max_warps > kMaxWarps) return reject("levels wider than the block");
-    std::vector<int> n2(nl), n8(nl);
-    for (int q = 0; q < nl; ++q) {
-        n2[q] = std::min(c2[q], 32 * w2);
-        n8[q] = c8[q] + c2[q] - n2[q];
+    if (best_w == 0) return reject("no (warps, rows per thread) shape fits");
+    const int cap2 = 32 * best_w * best_r2, cap8 = 32 * best_w * best_r8;
+
+    // pseudo-levels: a level wider than one pass of the block is split
+    std::vector<int> plv_of(n);   // pseudo-level of each row
+    std::vector<int> n2, n8;      // per pseudo-level
+    std::vector<int> first_plv(nlv);
+    {
+        for (int q = 0; q < nlv; ++q) {
+            const int p = std::max({1, (c2[q] + cap2 - 1) / cap2, best_r8 ? (c8[q] + cap8 - 1) / cap8 : 1});
+            first_plv[q] = static_cast<int>(n2.size());
+            for (int k = 0; k < p; ++k) {
+                n2.push_back(0);
+                n8.push_back(0);
+            }
+        }
+        std::vector<int> seen2(nlv, 0), seen8(nlv, 0);
+        for (int i = 0; i < n; ++i) {
+            const int q = lev[i];
+            const int pl = nlow[i] <= 2 ? first_plv[q] + seen2[q]++ / cap2 : first_plv[q] + seen8[q]++ / cap8;
+            plv_of[i] = pl;
+            ++(nlow[i] <= 2 ? n2 : n8)[pl];
+        }
     }
-    std::vector<int> lptr(nl + 1, 0), fill2(nl), fill8(nl), order(n), pos(n), seen2(nl, 0);
+    const int nl = static_cast<int>(n2.size());
+    if (nl >= (1 << 13)) return reject("too many levels for the meta packing");
+    std::vector<int> lptr(nl + 1, 0), fill2(nl), fill8(nl), order(n), pos(n);
     for (int q = 0; q < nl; ++q) lptr[q + 1] = lptr[q] + n2[q] + n8[q];
     for (int q = 0; q < nl; ++q) {
         fill2[q] = lptr[q];
         fill8[q] = lptr[q] + n2[q];
     }
     for (int i = 0; i < n; ++i) {
-        const int q = lev[i];
-        const bool small = nlow[i] <= 2 && seen2[q]++ < n2[q];
-        const int p = (small ? fill2 : fill8)[q]++;
+        const int p = (nlow[i] <= 2 ? fill2 : fill8)[plv_of[i]]++;
         order[p] = i;
         pos[i] = p;
     }
@@ -312,7 +438,6 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         off += lbytes[q];
     }
     if (off / 16 >= (static_cast<int64_t>(1) << 31)) return reject("packed buffer too large");
-    if (n >= (1 << 20) || nl >= (1 << 13)) return reject("too many rows or levels for the meta packing");
 
     // chunks of consecutive levels
     std::vector<int> cfirst, cbytes;
@@ -343,10 +468,9 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     SDG_CUDA(cudaGetDevice(&dev));
     SDG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     const int budget = std::min(kSmemCap, optin - 1024);
-    const int meta_bytes = pad16(static_cast<int64_t>(nl + 1) * 16);
+    const int meta_bytes = pad16(static_cast<int64_t>(nl + 2) * 16);
     const int chunk_bytes = pad16(static_cast<int64_t>(nc) * 16);
-    const int cfirst_bytes = pad16(static_cast<int64_t>(nc) * 4);
-    const int min_stage = std::max(3 * max_chunk, kMaxWarps * 32 * kK8Bytes);
+    const int min_stage = 3 * max_chunk;
     ring = 64;
     while (ring < max_dist && ring < 8192) ring <<= 1;
     std::vector<int> pin_of;
@@ -363,7 +487,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
                 }
             }
         zbytes = pad16(static_cast<int64_t>(ring + 2 + npin) * 8);
-        fixed = kBars * 8 + 16 + kNullBytes + meta_bytes + chunk_bytes + cfirst_bytes + zbytes;
+        fixed = kBars * 8 + 16 + kNullBytes + meta_bytes + chunk_bytes + zbytes;
         R = (budget - fixed) / 16 * 16;
         if (R >= min_stage) break;
         if (ring <= 64 || ring / 2 < 2 * max_rows) return reject("shared memory: ring + pinned values + staging");
@@ -379,7 +503,6 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         if (cur + sz > R) cur = 0;
         roff[c] = cur;
         int aft = c > 0 ? after[c - 1] : -1;
-        if (c >= kBars - 2) aft = std::max(aft, cfirst[c - (kBars - 2)]);  // its mbarrier was waited on
         int64_t scanned = 0;
         for (int x = c - 1; x >= 0 && scanned <= 2LL * R; --x) {
             scanned += cbytes[x];
@@ -389,7 +512,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
                 break;
             }
         }
-        if (aft >= 0 && aft > cfirst[c] - 3) return reject("staging ring too small for the look-ahead");
+        if (aft >= 0 && aft > cfirst[c] - 4) return reject("staging ring too small for the look-ahead");
         after[c] = aft;
         cur += sz;
     }
@@ -397,7 +520,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     std::vector<double> pk(static_cast<size_t>(off / 8 + 2), 0.0);
     unsigned char* base = reinterpret_cast<unsigned char*>(pk.data());
     std::vector<int> bidx_h(n);
-    std::vector<int4> meta_h(nl + 1), ctab_h(nc);
+    std::vector<int4> meta_h(nl + 2), ctab_h(nc);
     lower_entries = 0;
     global_refs = 0;
     cross_refs = npin;
@@ -436,7 +559,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         const int o2 = roff[chunk_of[q]] + in_chunk[q], o8 = o2 + n2[q] * kK2Bytes;
         meta_h[q] = make_int4(o2, o8 | (starts << 18), lptr[q] | (n2[q] << 20), (lptr[q] + n2[q]) | (n8[q] << 20));
     }
-    meta_h[nl] = make_int4(0, 0, 0, 0);  // sentinel: the prefetch past the last level reads null rows
+    meta_h[nl] = meta_h[nl + 1] = make_int4(0, 0, 0, 0);  // sentinels: prefetches past the end read null rows
     for (int c = 0; c < nc; ++c)
         ctab_h[c] = make_int4(static_cast<int>(goff[cfirst[c]] / 16), cbytes[c], roff[c], after[c]);
 
@@ -445,36 +568,35 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     bands = 1;
     n_levels = nl;
     max_band_levels = nl;
-    nthreads = 32 + 32 * max_warps;
+    nthreads = 32 + 32 * best_w;
+    walk_r2 = best_r2;
+    walk_r8 = best_r8;
     walk_meta_bytes = meta_bytes;
     walk_chunk_bytes = chunk_bytes;
-    walk_cfirst_bytes = cfirst_bytes;
     walk_zbytes = zbytes;
     walk_chunks = nc;
-    walk_w2 = w2;
     max_seg = max_chunk;
     halo = npin;
     smem = static_cast<size_t>(fixed) + R;
     if (std::getenv("SDG_DEBUG"))
         std::fprintf(stderr,
-                     "[sdg gs walk] n=%d levels=%d chunks=%d threads=%d ring=%d pinned=%d stage=%d max_chunk=%d "
-                     "smem=%zu packed=%.1fKB\n",
-                     n, nl, nc, nthreads, ring, npin, R, max_chunk, smem, off / 1024.0);
+                     "[sdg gs walk] n=%d levels=%d pseudo-levels=%d warps=%d rows/thread=%d+%d chunks=%d ring=%d "
+                     "pinned=%d stage=%d smem=%zu packed=%.1fKB model=%.0f cycles\n",
+                     n, nlv, nl, best_w, best_r2, best_r8, nc, ring, npin, R, smem, off / 1024.0, best_cost);
     meta.upload(meta_h, s);
     walk_iss.upload(ctab_h, s);
-    walk_cfirst.upload(cfirst, s);
     packed.upload(pk, s);
     bidx.upload(bidx_h, s);
-    SDG_CUDA(cudaFuncSetAttribute(k_gs_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+    SDG_CUDA(cudaFuncSetAttribute(walk_kernel(best_r2, best_r8), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  budget));
     SDG_CUDA(cudaStreamSynchronize(s));  // host staging vectors die here
     return true;
 }
 
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new) {
-    WalkArgs a{g.meta.get(), g.walk_iss.get(), g.walk_cfirst.get(),
-               reinterpret_cast<const unsigned char*>(g.packed.get()), g.n_levels, g.walk_chunks, g.ring,
-               g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_cfirst_bytes, g.walk_zbytes, g.walk_w2, z_new};
-    k_gs_walk<<<1, g.nthreads, g.smem, c.stream>>>(a);
+    WalkArgs a{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.packed.get()),
+               g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes, z_new};
+    walk_kernel(g.walk_r2, g.walk_r8)<<<1, g.nthreads, g.smem, c.stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(SDG_ECUDA, std::string("launch_gs_walk: ") + cudaGetErrorString(e));
     c.count();

@@ -34,15 +34,16 @@ int main(int argc, char** argv) {
     cudaMemcpy(g.packed.get(), pk.data(), pk.size() * 8, cudaMemcpyHostToDevice);
     double* z;
     cudaMalloc(&z, n * 8);
-    WalkArgs wa{g.meta.get(), g.walk_iss.get(), g.walk_cfirst.get(),
-                reinterpret_cast<const unsigned char*>(g.packed.get()), g.n_levels, g.walk_chunks, g.ring,
-                g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_cfirst_bytes, g.walk_zbytes, g.walk_w2, z};
-    for (int r = 0; r < 3; ++r) k_gs_walk<<<1, g.nthreads, g.smem, s>>>(wa);
+    WalkArgs wa{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.packed.get()),
+                g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes, z};
+    const auto kern = walk_kernel(g.walk_r2, g.walk_r8);
+    printf("plan: warps %d rows/thread %d+%d levels %d\n", g.nthreads / 32 - 1, g.walk_r2, g.walk_r8, g.n_levels);
+    for (int r = 0; r < 3; ++r) kern<<<1, g.nthreads, g.smem, s>>>(wa);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
-    for (int r = 0; r < 20; ++r) k_gs_walk<<<1, g.nthreads, g.smem, s>>>(wa);
+    for (int r = 0; r < 20; ++r) kern<<<1, g.nthreads, g.smem, s>>>(wa);
     cudaEventRecord(e1, s);
     cudaError_t e = cudaEventSynchronize(e1);
     float ms;
@@ -50,13 +51,20 @@ int main(int argc, char** argv) {
     std::vector<double> hz(n), zc(n);
     cudaMemcpy(hz.data(), z, n * 8, cudaMemcpyDeviceToHost);
     double maxd = 0;
+    int nbad = 0, first_bad = -1;
     for (int i = 0; i < n; ++i) {
         double acc = 0.25 * (1.0 + 1e-3 * (i % 7));
         for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
             if (a.ci[k] < i) acc += 0.25 * zc[a.ci[k]];
         zc[i] = acc;
         maxd = std::max(maxd, std::abs(acc - hz[i]) / std::abs(acc));
+        if (std::abs(acc - hz[i]) > 1e-12 * std::abs(acc)) {
+            if (first_bad < 0) first_bad = i;
+            if (nbad < 24) printf("bad row %d (%d,%d) got %.6f want %.6f\n", i, i % nx, i / nx, hz[i], acc);
+            ++nbad;
+        }
     }
+    if (nbad) printf("mismatches %d first at row %d (got %g want %g)\n", nbad, first_bad, hz[first_bad], zc[first_bad]);
 #ifdef SDG_WALK_TRACE
     {
         std::vector<long long> tr(1024 * 16 * 4);
