@@ -57,6 +57,7 @@ struct GsPlan {
     bool walk = false;         // single-CTA walk (gs_walk.cu) instead of the banded cluster kernel
     int walk_meta_bytes = 0, walk_chunk_bytes = 0, walk_zbytes = 0, walk_chunks = 0;
     int walk_r2 = 1, walk_r8 = 0;  // rows per consumer thread and level (<= 2-entry / wider rows)
+    int walk_kw = 8;               // entries of a wide record (6 or 8)
     DevBuf<int4> walk_iss;     // per chunk {global off16, bytes, stage off, issue after level}
     DevBuf<int4> meta;         // per (band, level) {chunk-local off16, nS | global flag << 31, nL | nE << 16, chunk}
     DevBuf<int4> chunk_tab;    // per (band, chunk) {off16, bytes16, first level, levels}

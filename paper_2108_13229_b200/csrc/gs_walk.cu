@@ -60,6 +60,7 @@ __device__ long long g_walk_trace[1024 * 16 * 4];
 constexpr int kBars = 32;  // chunk mbarriers (chunks in flight at most)
 constexpr int kK2Bytes = 48;
 constexpr int kK8Bytes = 112;
+constexpr int kK6Bytes = 80;  // <= 6 entries, 16-bit sources
 constexpr int kMaxK = 8;
 constexpr int kMaxR2 = 6, kMaxR8 = 3;
 constexpr int kChunkBytes = 16 * 1024;
@@ -112,10 +113,10 @@ struct WalkArgs {
 
 // Rows a consumer thread holds for one level: R2 small + R8 wide rows (the
 // sources, scalars and the shared address of each record's coefficients).
-template <int R2, int R8>
+template <int R2, int R8, int KW>
 struct WalkRows {
     double b2[R2 > 0 ? R2 : 1], b8[R8 > 0 ? R8 : 1];
-    int s2[R2 > 0 ? R2 : 1][2], s8[R8 > 0 ? R8 : 1][kMaxK];
+    int s2[R2 > 0 ? R2 : 1][2], s8[R8 > 0 ? R8 : 1][KW];
     int rid2[R2 > 0 ? R2 : 1], pin2[R2 > 0 ? R2 : 1], wp2[R2 > 0 ? R2 : 1];
     int rid8[R8 > 0 ? R8 : 1], pin8[R8 > 0 ? R8 : 1], wp8[R8 > 0 ? R8 : 1];
     const unsigned char* vp2[R2 > 0 ? R2 : 1];
@@ -126,7 +127,7 @@ struct WalkRows {
 // fetched two levels ahead (two register sets, alternating), so neither the
 // record loads nor their addresses are on the per-level critical path
 //   gathers (shared) -> FMAs -> ring store -> level hand-off.
-template <int R2, int R8>
+template <int R2, int R8, int KW>
 __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* meta, const unsigned char* stage,
                                               const unsigned char* nullrec, double* zr, int* flags) {
     const int mask = a.ring - 1, dummy = a.ring + 1;
@@ -135,7 +136,8 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     const int stride = 32 * nw;
     int* progress = flags;
     const int* landed = flags + 1;
-    using Rows = WalkRows<R2, R8>;
+    using Rows = WalkRows<R2, R8, KW>;
+    constexpr int WB = KW == 8 ? kK8Bytes : kK6Bytes;
     auto wait_landed = [&](const int4 m) {
         const int need = static_cast<unsigned>(m.y) >> 18;  // chunk id + 1 when the level starts a chunk
         if (need)
@@ -162,15 +164,22 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
         for (int r = 0; r < R8; ++r) {
             const int u = r * stride + t0;
             const bool ok = u < (m.w >> 20);
-            const unsigned char* q = ok ? stage + (m.y & 0x3ffff) + u * kK8Bytes : nullrec + 128;
+            const unsigned char* q = ok ? stage + (m.y & 0x3ffff) + u * WB : nullrec + 128;
             const int4 h = *reinterpret_cast<const int4*>(q);
-            const int4 x0 = *reinterpret_cast<const int4*>(q + 80);
-            const int4 x1 = *reinterpret_cast<const int4*>(q + 96);
             x.b8[r] = __hiloint2double(h.y, h.x);
             x.rid8[r] = h.z;
             x.pin8[r] = h.w;
-            x.s8[r][0] = x0.x; x.s8[r][1] = x0.y; x.s8[r][2] = x0.z; x.s8[r][3] = x0.w;
-            x.s8[r][4] = x1.x; x.s8[r][5] = x1.y; x.s8[r][6] = x1.z; x.s8[r][7] = x1.w;
+            if constexpr (KW == 8) {
+                const int4 x0 = *reinterpret_cast<const int4*>(q + 80);
+                const int4 x1 = *reinterpret_cast<const int4*>(q + 96);
+                x.s8[r][0] = x0.x; x.s8[r][1] = x0.y; x.s8[r][2] = x0.z; x.s8[r][3] = x0.w;
+                x.s8[r][4] = x1.x; x.s8[r][5] = x1.y; x.s8[r][6] = x1.z; x.s8[r][7] = x1.w;
+            } else {
+                const int4 x0 = *reinterpret_cast<const int4*>(q + 64);  // six 16-bit sources
+                x.s8[r][0] = x0.x & 0xffff; x.s8[r][1] = static_cast<unsigned>(x0.x) >> 16;
+                x.s8[r][2] = x0.y & 0xffff; x.s8[r][3] = static_cast<unsigned>(x0.y) >> 16;
+                x.s8[r][4] = x0.z & 0xffff; x.s8[r][5] = static_cast<unsigned>(x0.z) >> 16;
+            }
             x.vp8[r] = q + 16;
             x.wp8[r] = ok ? (((m.w & 0xfffff) + u) & mask) : dummy;
         }
@@ -179,7 +188,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     auto step = [&](int L, Rows& x) {
         WALK_CLK(L, 0);
         double z2[R2 > 0 ? R2 : 1][2], v2[R2 > 0 ? R2 : 1][2];
-        double z8[R8 > 0 ? R8 : 1][kMaxK], v8[R8 > 0 ? R8 : 1][kMaxK];
+        double z8[R8 > 0 ? R8 : 1][KW], v8[R8 > 0 ? R8 : 1][KW];
 #pragma unroll
         for (int r = 0; r < R2; ++r) {
             z2[r][0] = zr[x.s2[r][0]];
@@ -191,9 +200,9 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
 #pragma unroll
         for (int r = 0; r < R8; ++r) {
 #pragma unroll
-            for (int k = 0; k < kMaxK; ++k) z8[r][k] = zr[x.s8[r][k]];
+            for (int k = 0; k < KW; ++k) z8[r][k] = zr[x.s8[r][k]];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < KW / 2; ++k) {
                 const double2 c = reinterpret_cast<const double2*>(x.vp8[r])[k];
                 v8[r][2 * k] = c.x;
                 v8[r][2 * k + 1] = c.y;
@@ -214,8 +223,13 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
             const double q0 = fma(v[1], z[1], fma(v[0], z[0], x.b8[r]));
             const double q1 = fma(v[3], z[3], v[2] * z[2]);
             const double q2 = fma(v[5], z[5], v[4] * z[4]);
-            const double q3 = fma(v[7], z[7], v[6] * z[6]);
-            const double acc = (q0 + q1) + (q2 + q3);
+            double acc;
+            if constexpr (KW == 8) {
+                const double q3 = fma(v[7 % KW], z[7 % KW], v[6 % KW] * z[6 % KW]);
+                acc = (q0 + q1) + (q2 + q3);
+            } else {
+                acc = (q0 + q1) + q2;
+            }
             zr[x.wp8[r]] = acc;
             zr[x.pin8[r]] = acc;
             if (x.rid8[r] >= 0) a.z_new[x.rid8[r]] = acc;
@@ -244,7 +258,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     }
 }
 
-template <int R2, int R8>
+template <int R2, int R8, int KW>
 __global__ void __launch_bounds__(max_threads(R2, R8), 1) k_gs_walk(WalkArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
@@ -266,7 +280,10 @@ __global__ void __launch_bounds__(max_threads(R2, R8), 1) k_gs_walk(WalkArgs a) 
         for (int k = 0; k < 32; ++k) nr[k] = 0;
         nr[2] = -1;     // rowid
         nr[3] = dummy;  // pin
-        for (int k = 0; k < kMaxK; ++k) nr[(tid ? 20 : 8) + k] = zero_slot;
+        if (tid == 0 || KW == 8)
+            for (int k = 0; k < kMaxK; ++k) nr[(tid ? 20 : 8) + k] = zero_slot;
+        else
+            for (int k = 0; k < 4; ++k) nr[16 + k] = zero_slot | (zero_slot << 16);
     }
     if (tid == 0) {
         zr[zero_slot] = 0.0;
@@ -277,7 +294,7 @@ __global__ void __launch_bounds__(max_threads(R2, R8), 1) k_gs_walk(WalkArgs a) 
     __syncthreads();
 
     if (tid >= 32) {
-        walk_consumer<R2, R8>(a, meta, stage, nullrec, zr, flags);
+        walk_consumer<R2, R8, KW>(a, meta, stage, nullrec, zr, flags);
         return;
     }
     if (tid != 0) return;
@@ -304,23 +321,23 @@ __global__ void __launch_bounds__(max_threads(R2, R8), 1) k_gs_walk(WalkArgs a) 
 
 using WalkKernel = void (*)(WalkArgs);
 
-template <int R2, int R8>
-constexpr WalkKernel kernel_of() {
-    return &k_gs_walk<R2, R8>;
+template <int I>
+constexpr WalkKernel kernel_at() {
+    return &k_gs_walk<I / (2 * (kMaxR8 + 1)) + 1, (I / 2) % (kMaxR8 + 1), I % 2 ? 8 : 6>;
 }
 
-// all instantiations, indexed [R2 - 1][R8]
+// all instantiations, indexed [R2 - 1][R8][wide width is 8]
 template <int... I>
 constexpr auto make_table(std::integer_sequence<int, I...>) {
     struct T {
         WalkKernel k[sizeof...(I)];
     };
-    return T{{kernel_of<I / (kMaxR8 + 1) + 1, I % (kMaxR8 + 1)>()...}};
+    return T{{kernel_at<I>()...}};
 }
 
-WalkKernel walk_kernel(int r2, int r8) {
-    static const auto table = make_table(std::make_integer_sequence<int, kMaxR2 * (kMaxR8 + 1)>{});
-    return table.k[(r2 - 1) * (kMaxR8 + 1) + r8];
+WalkKernel walk_kernel(int r2, int r8, int kw) {
+    static const auto table = make_table(std::make_integer_sequence<int, kMaxR2 * (kMaxR8 + 1) * 2>{});
+    return table.k[((r2 - 1) * (kMaxR8 + 1) + r8) * 2 + (kw == 8 ? 1 : 0)];
 }
 
 }  // namespace
@@ -348,6 +365,10 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     }
     std::vector<int> c2(nlv, 0), c8(nlv, 0);
     for (int i = 0; i < n; ++i) ++(nlow[i] <= 2 ? c2 : c8)[lev[i]];
+    // wide rows: 6 entries with 16-bit sources (80-byte records) when no row
+    // has more, else 8 entries (112 bytes)
+    int kw = max_k <= 6 ? 6 : 8;
+    int WB = kw == 8 ? kK8Bytes : kK6Bytes;
 
     // (W, R2, R8) from a cost model in cycles per pseudo-level, fitted to
     // B200 measurements (scripts/mb_real2.cu): a latency chain that grows
@@ -366,7 +387,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
                 for (int q = 0; q < nlv && ok; ++q) {
                     if (c8[q] > 0 && r8 == 0) ok = false;
                     const int p = std::max({1, (c2[q] + cap2 - 1) / cap2, r8 ? (c8[q] + cap8 - 1) / cap8 : 1});
-                    const double bw = (2.0 * (c2[q] * kK2Bytes + c8[q] * kK8Bytes) + 40.0 * c2[q] + 100.0 * c8[q]) /
+                    const double bw = (2.0 * (c2[q] * kK2Bytes + c8[q] * WB) + 40.0 * c2[q] + 100.0 * c8[q]) /
                                       (128.0 * p);
                     cost += p * std::max(chain, bw);
                 }
@@ -433,7 +454,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     int64_t off = 0;
     for (int q = 0; q < nl; ++q) {
         max_rows = std::max(max_rows, n2[q] + n8[q]);
-        lbytes[q] = n2[q] * kK2Bytes + n8[q] * kK8Bytes;
+        lbytes[q] = n2[q] * kK2Bytes + n8[q] * WB;
         goff[q] = off;
         off += lbytes[q];
     }
@@ -494,6 +515,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         ring >>= 1;
     }
     const int zero_slot = ring, dummy_slot = ring + 1, pin_base = ring + 2;
+    if (kw == 6 && pin_base + npin >= 65536) return reject("too many shared slots for 16-bit sources");
 
     // staging ring placement and issue points of the chunks
     std::vector<int> roff(nc), after(nc);
@@ -532,27 +554,36 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
             const bool k2 = t < n2[q];
             unsigned char* rec = k2 ? seg + static_cast<size_t>(t) * kK2Bytes
                                     : seg + static_cast<size_t>(n2[q]) * kK2Bytes +
-                                          static_cast<size_t>(t - n2[q]) * kK8Bytes;
+                                          static_cast<size_t>(t - n2[q]) * WB;
             double* recd = reinterpret_cast<double*>(rec);
             int* reci = reinterpret_cast<int*>(rec);
             bidx_h[i] = static_cast<int>((rec - base) / 8);
             reci[2] = i;
             reci[3] = pin_of[i] >= 0 ? pin_base + pin_of[i] : dummy_slot;
-            const int cap = k2 ? 2 : kMaxK;
+            const int cap = k2 ? 2 : kw;
             double* val = recd + 2;
             int* src = reci + (k2 ? 8 : 20);
+            uint16_t* src16 = reinterpret_cast<uint16_t*>(rec + 64);
+            const bool narrow_src = !k2 && kw == 6;
             int m = 0;
             for (int k = a.rp[i]; k < a.rp[i + 1]; ++k) {
                 const int j = a.ci[k];
                 if (j >= i) continue;
                 val[m] = -(a.v[k] * dinv_h[i]);
-                src[m] = lptr[q + 1] - pos[j] <= ring ? (pos[j] & (ring - 1)) : pin_base + pin_of[j];
+                const int slot = lptr[q + 1] - pos[j] <= ring ? (pos[j] & (ring - 1)) : pin_base + pin_of[j];
+                if (narrow_src)
+                    src16[m] = static_cast<uint16_t>(slot);
+                else
+                    src[m] = slot;
                 ++m;
                 ++lower_entries;
             }
             for (; m < cap; ++m) {
                 val[m] = 0.0;
-                src[m] = zero_slot;
+                if (narrow_src)
+                    src16[m] = static_cast<uint16_t>(zero_slot);
+                else
+                    src[m] = zero_slot;
             }
         }
         const int starts = cfirst[chunk_of[q]] == q ? chunk_of[q] + 1 : 0;  // chunk id + 1 if q starts a chunk
@@ -571,6 +602,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     nthreads = 32 + 32 * best_w;
     walk_r2 = best_r2;
     walk_r8 = best_r8;
+    walk_kw = kw;
     walk_meta_bytes = meta_bytes;
     walk_chunk_bytes = chunk_bytes;
     walk_zbytes = zbytes;
@@ -580,14 +612,14 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     smem = static_cast<size_t>(fixed) + R;
     if (std::getenv("SDG_DEBUG"))
         std::fprintf(stderr,
-                     "[sdg gs walk] n=%d levels=%d pseudo-levels=%d warps=%d rows/thread=%d+%d chunks=%d ring=%d "
-                     "pinned=%d stage=%d smem=%zu packed=%.1fKB model=%.0f cycles\n",
-                     n, nlv, nl, best_w, best_r2, best_r8, nc, ring, npin, R, smem, off / 1024.0, best_cost);
+                     "[sdg gs walk] n=%d levels=%d pseudo-levels=%d warps=%d rows/thread=%d+%d wide=%d chunks=%d "
+                     "ring=%d pinned=%d stage=%d smem=%zu packed=%.1fKB model=%.0f cycles\n",
+                     n, nlv, nl, best_w, best_r2, best_r8, kw, nc, ring, npin, R, smem, off / 1024.0, best_cost);
     meta.upload(meta_h, s);
     walk_iss.upload(ctab_h, s);
     packed.upload(pk, s);
     bidx.upload(bidx_h, s);
-    SDG_CUDA(cudaFuncSetAttribute(walk_kernel(best_r2, best_r8), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SDG_CUDA(cudaFuncSetAttribute(walk_kernel(best_r2, best_r8, kw), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   budget));
     SDG_CUDA(cudaStreamSynchronize(s));  // host staging vectors die here
     return true;
@@ -596,7 +628,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new) {
     WalkArgs a{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.packed.get()),
                g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes, z_new};
-    walk_kernel(g.walk_r2, g.walk_r8)<<<1, g.nthreads, g.smem, c.stream>>>(a);
+    walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw)<<<1, g.nthreads, g.smem, c.stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(SDG_ECUDA, std::string("launch_gs_walk: ") + cudaGetErrorString(e));
     c.count();

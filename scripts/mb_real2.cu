@@ -36,7 +36,7 @@ int main(int argc, char** argv) {
     cudaMalloc(&z, n * 8);
     WalkArgs wa{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.packed.get()),
                 g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes, z};
-    const auto kern = walk_kernel(g.walk_r2, g.walk_r8);
+    const auto kern = walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw);
     printf("plan: warps %d rows/thread %d+%d levels %d\n", g.nthreads / 32 - 1, g.walk_r2, g.walk_r8, g.n_levels);
     for (int r = 0; r < 3; ++r) kern<<<1, g.nthreads, g.smem, s>>>(wa);
     cudaEvent_t e0, e1;
