@@ -54,6 +54,21 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
+def job_totals(dist, elapsed, work, device="cpu"):
+    """Whole-job totals over ranks (one replica per rank, weak scaling): the
+    slowest rank's elapsed time and the summed work.  `dist` is
+    torch.distributed (None for a single process); works with NCCL (device
+    tensors) and gloo (CPU tensors, the CPU tests)."""
+    if dist is None:
+        return float(elapsed), float(work)
+    import torch
+    t = torch.tensor([float(elapsed)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    w = torch.tensor([float(work)], dtype=torch.float64, device=device)
+    dist.all_reduce(w, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(w.item())
+
+
 def measured_peak_gbs():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -273,13 +288,7 @@ def run_ours(args):
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
-    work = float(n) * sum(iters)
-    if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        w = torch.tensor([work], dtype=torch.float64, device=dev)
-        dist.all_reduce(w, op=dist.ReduceOp.SUM)
-        total_ms, work = float(t.item()), float(w.item())
+    total_ms, work = job_totals(dist, total_ms, float(n) * sum(iters), dev)
     value = work / (total_ms / 1e3)
 
     # parity self-check of the timed solve (residual of the returned x)
@@ -300,13 +309,7 @@ def run_ours(args):
             res = solve_host(sdc, cfg, s, p, b_np, tol)
             e_its += res.report.iterations
         e_s = time.perf_counter() - t0
-        e_work = float(n) * e_its
-        if dist:
-            t = torch.tensor([e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            w = torch.tensor([e_work], dtype=torch.float64, device=dev)
-            dist.all_reduce(w, op=dist.ReduceOp.SUM)
-            e_s, e_work = float(t.item()), float(w.item())
+        e_s, e_work = job_totals(dist, e_s, float(n) * e_its, dev)
         e2e = {"value": e_work / e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                "ms_per_step": 1e3 * e_s / args.steps, "timing": "host wall clock around the synchronous C-ABI call"}
 
