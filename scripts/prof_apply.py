@@ -1,4 +1,7 @@
-"""Dev helper: c2 system, td_bgs preconditioner, timed applies + per-family profile."""
+"""Dev helper: c2 system, td_bgs preconditioner, timed applies + per-family profile.
+
+With SDG_PROFILER_RANGE=1 the last apply is wrapped in cudaProfilerStart/Stop,
+so `ncu --profile-from-start off` captures exactly one preconditioner apply."""
 import os, sys, time
 import numpy as np
 sys.path.insert(0, os.getcwd())
@@ -18,3 +21,10 @@ ctx.set_profiling(False)
 for k, v in prof.items():
     print(f"{k:10s} launches/apply={v['launches']/5:6.1f} ms/apply={v['ms']/5:8.3f} GB/s={v['bytes']/v['ms']/1e6:8.1f}")
 print("hier", p.hierarchy(0), p.hierarchy(1))
+if os.environ.get("SDG_PROFILER_RANGE"):
+    import torch
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    p.apply(r)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
