@@ -60,6 +60,17 @@ __global__ void k_gs_prep_pre(int n, const double* __restrict__ r, const double*
     if (i < n) packed[bidx[i]] = r[i] * dinv[i];
 }
 
+// b_i += sum_j (-a_ij / d_i) z_j over the earlier label blocks (GsPlan::couple)
+__global__ void k_gs_couple(int rows, int r0, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, const double* __restrict__ z,
+                            const int* __restrict__ bidx, double* __restrict__ packed) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    double acc = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) acc = fma(v[k], z[ci[k]], acc);
+    packed[bidx[r0 + i]] += acc;
+}
+
 __global__ void k_gs_prep_post(int n, const int* __restrict__ urp, const int* __restrict__ uci,
                                const double* __restrict__ uv, const double* __restrict__ r,
                                const double* __restrict__ z, const double* __restrict__ zc,
@@ -362,15 +373,40 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
 
     // ---- bands: one for small systems, more once a single SM's bandwidth
     // becomes the bound (SDG_GS_BANDS overrides) -----------------------------
-    int nb = bands_hint > 0 ? bands_hint : (n >= 200000 ? 8 : n >= 80000 ? 4 : 1);
-    if (const char* e = std::getenv("SDG_GS_BANDS")) nb = std::max(1, std::atoi(e));
-    nb = std::max(1, std::min({nb, 8, std::max(1, n / 256)}));
+    // the single-CTA walk first (gs_walk.cu); the banded cluster kernel when
+    // the walk does not fit or bands are requested (bands_hint, SDG_GS_BANDS)
+    const char* bands_env = std::getenv("SDG_GS_BANDS");
     const char* walk_env = std::getenv("SDG_GS_WALK");
-    if (nb == 1 && !(walk_env && walk_env[0] == '0') && build_walk(a, dinv_h, nlow, max_k, s)) {
+    const bool want_walk = bands_hint <= 0 && !bands_env && !(walk_env && walk_env[0] == '0');
+    int nb = bands_hint > 0 ? bands_hint : (n >= 200000 ? 8 : n >= 80000 ? 4 : 1);
+    if (bands_env) nb = std::max(1, std::atoi(bands_env));
+    nb = std::max(1, std::min({nb, 8, std::max(1, n / 256)}));
+    const char* split_env = std::getenv("SDG_GS_SPLIT");  // test knob: label blocks even when one walk fits
+    const bool force_split = split_env && split_env[0] == '1';
+    if (want_walk && !force_split && build_walk(a, dinv_h, nlow, max_k, s)) {
         dinv.upload(dinv_h, s);
         upper.upload(up, s);
         SDG_CUDA(cudaStreamSynchronize(s));
         return;
+    }
+    // one walk per contiguous label block (e.g. u / v of the velocity block)
+    if (want_walk && comps.size() == static_cast<size_t>(n) && n > 0) {
+        std::vector<int> r0{0};
+        std::vector<int> seen;
+        bool contiguous = true;
+        for (int i = 1; i < n; ++i)
+            if (comps[i] != comps[i - 1]) r0.push_back(i);
+        for (size_t k = 0; k < r0.size(); ++k) {
+            if (std::find(seen.begin(), seen.end(), comps[r0[k]]) != seen.end()) contiguous = false;
+            seen.push_back(comps[r0[k]]);
+        }
+        r0.push_back(n);
+        if (contiguous && r0.size() > 2 && build_parts(a, r0, dinv_h, s)) {
+            dinv.upload(dinv_h, s);
+            upper.upload(up, s);
+            SDG_CUDA(cudaStreamSynchronize(s));
+            return;
+        }
     }
     walk = false;
     const int global_depth = lower_schedule(a).n_levels();
@@ -666,6 +702,80 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     SDG_CUDA(cudaStreamSynchronize(s));  // host staging vectors die here
 }
 
+bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
+                         cudaStream_t s) {
+    const int nparts = static_cast<int>(r0.size()) - 1;
+    std::vector<std::unique_ptr<GsPlan>> ps;
+    for (int k = 0; k < nparts; ++k) {
+        const int lo = r0[k], hi = r0[k + 1], m = hi - lo;
+        HostCsr sub(m, m);
+        std::vector<double> dsub(dinv_h.begin() + lo, dinv_h.begin() + hi);
+        std::vector<int> nlow(m, 0);
+        int max_k = 0;
+        for (int i = lo; i < hi; ++i) {
+            for (int e = a.rp[i]; e < a.rp[i + 1]; ++e) {
+                const int j = a.ci[e];
+                if (j < lo || j >= hi) continue;
+                sub.ci.push_back(j - lo);
+                sub.v.push_back(a.v[e]);
+                if (j < i) ++nlow[i - lo];
+            }
+            sub.rp[i - lo + 1] = static_cast<int>(sub.ci.size());
+            max_k = std::max(max_k, nlow[i - lo]);
+        }
+        auto p = std::make_unique<GsPlan>();
+        if (!p->build_walk(sub, dsub, nlow, max_k, s)) return false;
+        ps.push_back(std::move(p));
+    }
+    // one record buffer; the prep kernels write b through the global bidx
+    size_t total = 0;
+    std::vector<size_t> off(nparts);
+    for (int k = 0; k < nparts; ++k) {
+        off[k] = total;
+        total += ps[k]->packed.size();
+    }
+    packed.resize(total);
+    std::vector<int> bidx_h(n);
+    for (int k = 0; k < nparts; ++k) {
+        GsPlan& p = *ps[k];
+        SDG_CUDA(cudaMemcpyAsync(packed.get() + off[k], p.packed.get(), p.packed.size() * 8,
+                                 cudaMemcpyDeviceToDevice, s));
+        std::vector<int> lb(p.n);
+        SDG_CUDA(cudaMemcpyAsync(lb.data(), p.bidx.get(), p.n * sizeof(int), cudaMemcpyDeviceToHost, s));
+        SDG_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < p.n; ++i) bidx_h[r0[k] + i] = static_cast<int>(off[k]) + lb[i];
+        p.part_doubles = p.packed.size();
+        p.packed.release();
+        p.bidx.release();
+        p.packed_ptr = packed.get() + off[k];
+    }
+    bidx.upload(bidx_h, s);
+    couple.resize(nparts);
+    for (int k = 1; k < nparts; ++k) {
+        HostCsr cp(r0[k + 1] - r0[k], n);
+        for (int i = r0[k]; i < r0[k + 1]; ++i) {
+            for (int e = a.rp[i]; e < a.rp[i + 1]; ++e)
+                if (a.ci[e] < r0[k]) {
+                    cp.ci.push_back(a.ci[e]);
+                    cp.v.push_back(-(a.v[e] * dinv_h[i]));
+                }
+            cp.rp[i - r0[k] + 1] = static_cast<int>(cp.ci.size());
+        }
+        couple[k].upload(cp, s);
+    }
+    parts = std::move(ps);
+    part_r0 = r0;
+    walk = false;
+    usable = true;
+    bands = 1;
+    n_levels = 0;
+    for (auto& p : parts) n_levels += p->n_levels;
+    if (std::getenv("SDG_DEBUG"))
+        std::fprintf(stderr, "[sdg gs plan] n=%d: %d label blocks, one walk each (%d levels in sequence)\n", n, nparts,
+                     n_levels);
+    return true;
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 
@@ -697,6 +807,20 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
 }
 
 void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
+    if (!g.parts.empty()) {
+        for (size_t k = 0; k < g.parts.size(); ++k) {
+            if (k > 0) {
+                const DevCsr& cp = g.couple[k];
+                ProfScope ps_(c, PF_GSPREP, 12.0 * cp.nnz + 4.0 * (cp.n_rows + 1) + 28.0 * cp.n_rows);
+                k_gs_couple<<<(cp.n_rows + 255) / 256, 256, 0, c.stream>>>(
+                    cp.n_rows, g.part_r0[k], cp.rp.get(), cp.ci.get(), cp.v.get(), z_new, g.bidx.get(),
+                    const_cast<double*>(g.packed.get()));
+                SDG_GS_CHECK();
+            }
+            launch_gs_lower(c, *g.parts[k], z_new + g.part_r0[k]);
+        }
+        return;
+    }
     ProfScope ps_(c, PF_GS, g.packed_bytes() + 8.0 * g.n);
     if (g.n == 0) return;
     if (g.walk) {

@@ -30,6 +30,7 @@
 // sdg_sor_sweep and SDG_GS_EXACT=1.
 #pragma once
 
+#include <memory>
 #include <vector>
 
 #include "common.hpp"
@@ -70,13 +71,30 @@ struct GsPlan {
     DevBuf<double> dinv;
     DevCsr upper;              // strict upper triangle (natural order), unscaled
 
+    // Block forward substitution over contiguous label blocks, used when the
+    // whole lower solve does not fit one walk (exact: every row of block k
+    // precedes every row of block k+1).  parts[k] walks rows
+    // [part_r0[k], part_r0[k+1]); before it, couple[k] (rows of block k,
+    // columns of the earlier blocks, values -a_ij / d_i) adds the earlier
+    // blocks' new values to its b.  All records live in this plan's `packed`.
+    std::vector<std::unique_ptr<GsPlan>> parts;
+    std::vector<int> part_r0;
+    std::vector<DevCsr> couple;
+    const double* packed_ptr = nullptr;  // records of a part inside its parent's buffer
+    size_t part_doubles = 0;             // size of a part's records
+
     // components: per-row labels (e.g. u = 0 / v = 1 of the MAC velocity
     // block) so that bands cut every component at the same relative height.
     void build(const HostCsr& a, const std::vector<int>& components, cudaStream_t s,
                int bands_hint = 0);
-    double packed_bytes() const { return static_cast<double>(packed.size()) * 8.0; }
+    double packed_bytes() const {
+        return static_cast<double>(packed_ptr ? part_doubles : packed.size()) * 8.0;
+    }
+    const double* records() const { return packed_ptr ? packed_ptr : packed.get(); }
 
 private:
+    bool build_parts(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
+                     cudaStream_t s);
     bool build_walk(const HostCsr& a, const std::vector<double>& dinv_h, const std::vector<int>& nlow, int max_k,
                     cudaStream_t s);
 };

@@ -59,20 +59,28 @@ __device__ long long g_walk_trace[1024 * 16 * 4];
 
 constexpr int kBars = 32;  // chunk mbarriers (chunks in flight at most)
 constexpr int kK2Bytes = 48;
-constexpr int kK8Bytes = 112;
-constexpr int kK6Bytes = 80;  // <= 6 entries, 16-bit sources
-constexpr int kMaxK = 8;
+constexpr int kMaxK = 16;
+constexpr int kPseudoBytes = 24 * 1024;  // records per pseudo-level (staging granularity)
+
+// wide records: <= 6 entries (80 B, 16-bit sources), <= 8 (112 B, 32-bit
+// sources) or <= 16 (176 B, 16-bit sources); all odd multiples of 16 bytes
+__host__ __device__ constexpr int wide_bytes(int kw) { return kw == 6 ? 80 : kw == 8 ? 112 : 176; }
+__host__ __device__ constexpr int wide_src_off(int kw) { return kw == 6 ? 64 : kw == 8 ? 80 : 144; }
 constexpr int kMaxR2 = 6, kMaxR8 = 3;
 constexpr int kChunkBytes = 16 * 1024;
 constexpr int kSmemCap = 227 * 1024;
-constexpr int kNullBytes = 256;  // null K2 record at +0, null K8 record at +128
+constexpr int kNullBytes = 320;  // null small record at +0, null wide record at +128
 
 inline int pad16(int64_t b) { return static_cast<int>((b + 15) / 16 * 16); }
 
 // threads per CTA an instantiation may use (register budget)
-constexpr int max_threads(int r2, int r8) {
-    return r2 + 2 * r8 <= 3 ? 512 : r2 + 2 * r8 <= 5 ? 384 : r2 + 2 * r8 <= 7 ? 256 : 128;
+constexpr int max_threads(int r2, int r8, int kw) {
+    const int load = r2 + (kw == 16 ? 4 : 2) * r8;
+    return load <= 3 ? 512 : load <= 5 ? 384 : load <= 7 ? 256 : 128;
 }
+
+// shapes whose instantiation fits the register file without spills (ptxas -v)
+constexpr bool shape_ok(int r2, int r8, int kw) { return kw == 16 ? (r8 <= 1 && r2 <= 4) : !(r2 >= 5 && r8 == 3); }
 
 __device__ __forceinline__ int ld_volatile(const int* p) {
     int v;
@@ -137,7 +145,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     int* progress = flags;
     const int* landed = flags + 1;
     using Rows = WalkRows<R2, R8, KW>;
-    constexpr int WB = KW == 8 ? kK8Bytes : kK6Bytes;
+    constexpr int WB = wide_bytes(KW);
     auto wait_landed = [&](const int4 m) {
         const int need = static_cast<unsigned>(m.y) >> 18;  // chunk id + 1 when the level starts a chunk
         if (need)
@@ -172,13 +180,20 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
             if constexpr (KW == 8) {
                 const int4 x0 = *reinterpret_cast<const int4*>(q + 80);
                 const int4 x1 = *reinterpret_cast<const int4*>(q + 96);
-                x.s8[r][0] = x0.x; x.s8[r][1] = x0.y; x.s8[r][2] = x0.z; x.s8[r][3] = x0.w;
-                x.s8[r][4] = x1.x; x.s8[r][5] = x1.y; x.s8[r][6] = x1.z; x.s8[r][7] = x1.w;
-            } else {
-                const int4 x0 = *reinterpret_cast<const int4*>(q + 64);  // six 16-bit sources
-                x.s8[r][0] = x0.x & 0xffff; x.s8[r][1] = static_cast<unsigned>(x0.x) >> 16;
-                x.s8[r][2] = x0.y & 0xffff; x.s8[r][3] = static_cast<unsigned>(x0.y) >> 16;
-                x.s8[r][4] = x0.z & 0xffff; x.s8[r][5] = static_cast<unsigned>(x0.z) >> 16;
+                x.s8[r][0] = x0.x; x.s8[r][1] = x0.y; x.s8[r][2 % KW] = x0.z; x.s8[r][3 % KW] = x0.w;
+                x.s8[r][4 % KW] = x1.x; x.s8[r][5 % KW] = x1.y; x.s8[r][6 % KW] = x1.z; x.s8[r][7 % KW] = x1.w;
+            } else {  // 16-bit sources
+                unsigned w[(KW + 7) / 8 * 4];
+#pragma unroll
+                for (int j = 0; j < (KW + 7) / 8; ++j) {
+                    const int4 x0 = *reinterpret_cast<const int4*>(q + wide_src_off(KW) + 16 * j);
+                    w[4 * j] = x0.x;
+                    w[4 * j + 1] = x0.y;
+                    w[4 * j + 2] = x0.z;
+                    w[4 * j + 3] = x0.w;
+                }
+#pragma unroll
+                for (int k = 0; k < KW; ++k) x.s8[r][k] = (w[k / 2] >> (16 * (k % 2))) & 0xffff;
             }
             x.vp8[r] = q + 16;
             x.wp8[r] = ok ? (((m.w & 0xfffff) + u) & mask) : dummy;
@@ -220,16 +235,16 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
         for (int r = 0; r < R8; ++r) {
             const double* v = v8[r];
             const double* z = z8[r];
-            const double q0 = fma(v[1], z[1], fma(v[0], z[0], x.b8[r]));
-            const double q1 = fma(v[3], z[3], v[2] * z[2]);
-            const double q2 = fma(v[5], z[5], v[4] * z[4]);
-            double acc;
-            if constexpr (KW == 8) {
-                const double q3 = fma(v[7 % KW], z[7 % KW], v[6 % KW] * z[6 % KW]);
-                acc = (q0 + q1) + (q2 + q3);
-            } else {
-                acc = (q0 + q1) + q2;
-            }
+            // pairs, then a balanced tree: (q0 + q1) + q2 for 6, ((q0+q1)+(q2+q3)) for 8, ...
+            double qq[KW / 2];
+            qq[0] = fma(v[1], z[1], fma(v[0], z[0], x.b8[r]));
+#pragma unroll
+            for (int j = 1; j < KW / 2; ++j) qq[j] = fma(v[2 * j + 1], z[2 * j + 1], v[2 * j] * z[2 * j]);
+#pragma unroll
+            for (int w = 1; w < KW / 2; w *= 2)
+#pragma unroll
+                for (int j = 0; j + w < KW / 2; j += 2 * w) qq[j] += qq[j + w];
+            const double acc = qq[0];
             zr[x.wp8[r]] = acc;
             zr[x.pin8[r]] = acc;
             if (x.rid8[r] >= 0) a.z_new[x.rid8[r]] = acc;
@@ -259,7 +274,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
 }
 
 template <int R2, int R8, int KW>
-__global__ void __launch_bounds__(max_threads(R2, R8), 1) k_gs_walk(WalkArgs a) {
+__global__ void __launch_bounds__(max_threads(R2, R8, KW), 1) k_gs_walk(WalkArgs a) {
     extern __shared__ __align__(128) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
     int* flags = reinterpret_cast<int*>(sm + kBars * 8);  // {levels done, chunks landed}
@@ -275,15 +290,18 @@ __global__ void __launch_bounds__(max_threads(R2, R8), 1) k_gs_walk(WalkArgs a) 
     for (int l = tid; l <= nl + 1; l += blockDim.x) meta[l] = a.meta_g[l];
     for (int c = tid; c < nc; c += blockDim.x) ctab[c] = a.chunk_g[c];
     if (tid < kBars) mbar_init(&bars[tid], 1);
-    if (tid < 2) {  // null records
+    if (tid < 2) {  // null records: b = 0, v = 0, sources = zero slot, stores to the dummy slot
         int* nr = reinterpret_cast<int*>(nullrec + 128 * tid);
-        for (int k = 0; k < 32; ++k) nr[k] = 0;
+        for (int k = 0; k < (tid ? wide_bytes(KW) : 48) / 4; ++k) nr[k] = 0;
         nr[2] = -1;     // rowid
         nr[3] = dummy;  // pin
-        if (tid == 0 || KW == 8)
-            for (int k = 0; k < kMaxK; ++k) nr[(tid ? 20 : 8) + k] = zero_slot;
-        else
-            for (int k = 0; k < 4; ++k) nr[16 + k] = zero_slot | (zero_slot << 16);
+        if (tid == 0) {
+            nr[8] = nr[9] = zero_slot;
+        } else if (KW == 8) {
+            for (int k = 0; k < 8; ++k) nr[20 + k] = zero_slot;
+        } else {
+            for (int k = 0; k < KW / 2; ++k) nr[wide_src_off(KW) / 4 + k] = zero_slot | (zero_slot << 16);
+        }
     }
     if (tid == 0) {
         zr[zero_slot] = 0.0;
@@ -321,12 +339,14 @@ __global__ void __launch_bounds__(max_threads(R2, R8), 1) k_gs_walk(WalkArgs a) 
 
 using WalkKernel = void (*)(WalkArgs);
 
+constexpr int kw_of(int i) { return i == 0 ? 6 : i == 1 ? 8 : 16; }
+
 template <int I>
 constexpr WalkKernel kernel_at() {
-    return &k_gs_walk<I / (2 * (kMaxR8 + 1)) + 1, (I / 2) % (kMaxR8 + 1), I % 2 ? 8 : 6>;
+    return &k_gs_walk<I / (3 * (kMaxR8 + 1)) + 1, (I / 3) % (kMaxR8 + 1), kw_of(I % 3)>;
 }
 
-// all instantiations, indexed [R2 - 1][R8][wide width is 8]
+// all instantiations, indexed [R2 - 1][R8][wide width 6 / 8 / 16]
 template <int... I>
 constexpr auto make_table(std::integer_sequence<int, I...>) {
     struct T {
@@ -336,8 +356,8 @@ constexpr auto make_table(std::integer_sequence<int, I...>) {
 }
 
 WalkKernel walk_kernel(int r2, int r8, int kw) {
-    static const auto table = make_table(std::make_integer_sequence<int, kMaxR2 * (kMaxR8 + 1) * 2>{});
-    return table.k[((r2 - 1) * (kMaxR8 + 1) + r8) * 2 + (kw == 8 ? 1 : 0)];
+    static const auto table = make_table(std::make_integer_sequence<int, kMaxR2 * (kMaxR8 + 1) * 3>{});
+    return table.k[((r2 - 1) * (kMaxR8 + 1) + r8) * 3 + (kw == 6 ? 0 : kw == 8 ? 1 : 2)];
 }
 
 }  // namespace
@@ -351,7 +371,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         if (std::getenv("SDG_DEBUG")) std::fprintf(stderr, "[sdg gs walk] n=%d: not used (%s)\n", a.n_rows, why);
         return false;
     };
-    if (max_k > kMaxK) return reject("a row has more than 8 lower entries");
+    if (max_k > kMaxK) return reject("a row has more than 16 lower entries");
     n = a.n_rows;
     if (n >= (1 << 20)) return reject("too many rows for the meta packing");
     std::vector<int> lev(n, 0);
@@ -365,10 +385,9 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     }
     std::vector<int> c2(nlv, 0), c8(nlv, 0);
     for (int i = 0; i < n; ++i) ++(nlow[i] <= 2 ? c2 : c8)[lev[i]];
-    // wide rows: 6 entries with 16-bit sources (80-byte records) when no row
-    // has more, else 8 entries (112 bytes)
-    int kw = max_k <= 6 ? 6 : 8;
-    int WB = kw == 8 ? kK8Bytes : kK6Bytes;
+    // wide rows: the narrowest record that holds every row (see wide_bytes)
+    const int kw = max_k <= 6 ? 6 : max_k <= 8 ? 8 : 16;
+    const int WB = wide_bytes(kw);
 
     // (W, R2, R8) from a cost model in cycles per pseudo-level, fitted to
     // B200 measurements (scripts/mb_real2.cu): a latency chain that grows
@@ -379,14 +398,15 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     for (int w : {1, 2, 3, 4, 5, 6, 8, 11, 15})
         for (int r2 = 1; r2 <= kMaxR2; ++r2)
             for (int r8 = 0; r8 <= kMaxR8; ++r8) {
-                if (32 + 32 * w > max_threads(r2, r8)) continue;
+                if (32 + 32 * w > max_threads(r2, r8, kw) || !shape_ok(r2, r8, kw)) continue;
                 const int cap2 = 32 * w * r2, cap8 = 32 * w * r8;
                 const double chain = 220.0 + 15.0 * w + 35.0 * (r2 - 1) + 60.0 * r8;
                 double cost = 0;
                 bool ok = true;
                 for (int q = 0; q < nlv && ok; ++q) {
                     if (c8[q] > 0 && r8 == 0) ok = false;
-                    const int p = std::max({1, (c2[q] + cap2 - 1) / cap2, r8 ? (c8[q] + cap8 - 1) / cap8 : 1});
+                    const int p = std::max({1, (c2[q] + cap2 - 1) / cap2, r8 ? (c8[q] + cap8 - 1) / cap8 : 1,
+                                            (c2[q] * kK2Bytes + c8[q] * WB + kPseudoBytes - 1) / kPseudoBytes});
                     const double bw = (2.0 * (c2[q] * kK2Bytes + c8[q] * WB) + 40.0 * c2[q] + 100.0 * c8[q]) /
                                       (128.0 * p);
                     cost += p * std::max(chain, bw);
@@ -401,8 +421,8 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     if (const char* e = std::getenv("SDG_WALK_SHAPE")) {  // dev override "warps,r2,r8"
         int w = 0, r2 = 0, r8 = 0;
         if (std::sscanf(e, "%d,%d,%d", &w, &r2, &r8) == 3 && w >= 1 && r2 >= 1 && r2 <= kMaxR2 && r8 >= 0 &&
-            r8 <= kMaxR8 && 32 + 32 * w <= max_threads(r2, r8)) {
-            bool ok = true;
+            r8 <= kMaxR8) {
+            bool ok = 32 + 32 * w <= max_threads(r2, r8, kw) && shape_ok(r2, r8, kw);
             for (int q = 0; q < nlv; ++q) ok = ok && (r8 > 0 || c8[q] == 0);
             if (ok) {
                 best_w = w;
@@ -414,14 +434,17 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     if (best_w == 0) return reject("no (warps, rows per thread) shape fits");
     const int cap2 = 32 * best_w * best_r2, cap8 = 32 * best_w * best_r8;
 
-    // pseudo-levels: a level wider than one pass of the block is split
+    // pseudo-levels: a level wider than one pass of the block, or with more
+    // record bytes than kPseudoBytes, is split evenly (its rows are independent)
     std::vector<int> plv_of(n);   // pseudo-level of each row
     std::vector<int> n2, n8;      // per pseudo-level
-    std::vector<int> first_plv(nlv);
     {
+        std::vector<int> first_plv(nlv), parts(nlv);
         for (int q = 0; q < nlv; ++q) {
-            const int p = std::max({1, (c2[q] + cap2 - 1) / cap2, best_r8 ? (c8[q] + cap8 - 1) / cap8 : 1});
+            const int p = std::max({1, (c2[q] + cap2 - 1) / cap2, best_r8 ? (c8[q] + cap8 - 1) / cap8 : 1,
+                                    (c2[q] * kK2Bytes + c8[q] * WB + kPseudoBytes - 1) / kPseudoBytes});
             first_plv[q] = static_cast<int>(n2.size());
+            parts[q] = p;
             for (int k = 0; k < p; ++k) {
                 n2.push_back(0);
                 n8.push_back(0);
@@ -430,7 +453,9 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         std::vector<int> seen2(nlv, 0), seen8(nlv, 0);
         for (int i = 0; i < n; ++i) {
             const int q = lev[i];
-            const int pl = nlow[i] <= 2 ? first_plv[q] + seen2[q]++ / cap2 : first_plv[q] + seen8[q]++ / cap8;
+            const int pl = nlow[i] <= 2
+                               ? first_plv[q] + static_cast<int>(static_cast<int64_t>(seen2[q]++) * parts[q] / c2[q])
+                               : first_plv[q] + static_cast<int>(static_cast<int64_t>(seen8[q]++) * parts[q] / c8[q]);
             plv_of[i] = pl;
             ++(nlow[i] <= 2 ? n2 : n8)[pl];
         }
@@ -515,7 +540,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         ring >>= 1;
     }
     const int zero_slot = ring, dummy_slot = ring + 1, pin_base = ring + 2;
-    if (kw == 6 && pin_base + npin >= 65536) return reject("too many shared slots for 16-bit sources");
+    if (kw != 8 && pin_base + npin >= 65536) return reject("too many shared slots for 16-bit sources");
 
     // staging ring placement and issue points of the chunks
     std::vector<int> roff(nc), after(nc);
@@ -563,8 +588,8 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
             const int cap = k2 ? 2 : kw;
             double* val = recd + 2;
             int* src = reci + (k2 ? 8 : 20);
-            uint16_t* src16 = reinterpret_cast<uint16_t*>(rec + 64);
-            const bool narrow_src = !k2 && kw == 6;
+            uint16_t* src16 = reinterpret_cast<uint16_t*>(rec + wide_src_off(kw));
+            const bool narrow_src = !k2 && kw != 8;
             int m = 0;
             for (int k = a.rp[i]; k < a.rp[i + 1]; ++k) {
                 const int j = a.ci[k];
@@ -626,7 +651,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
 }
 
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new) {
-    WalkArgs a{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.packed.get()),
+    WalkArgs a{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.records()),
                g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes, z_new};
     walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw)<<<1, g.nthreads, g.smem, c.stream>>>(a);
     cudaError_t e = cudaGetLastError();

@@ -111,6 +111,29 @@ def test_amg_on_system_blocks(ref):
     assert rel_l2(amg.apply(r), td.v_hierarchy.vcycle(r)) < 1e-11
 
 
+@pytest.mark.parametrize("mode", [{"SDG_GS_SPLIT": "1"}, {"SDG_GS_WALK": "0"}, {"SDG_GS_BANDS": "4"}],
+                         ids=["label-block-walks", "cluster-kernel", "cluster-4-bands"])
+def test_smoother_paths_match_reference(ref, golden, monkeypatch, mode):
+    """The other lower-solve plans (one walk per u/v block with a coupling
+    step; the banded cluster kernel) against the reference V-cycle and the
+    golden td_bgs apply."""
+    for k, v in mode.items():
+        monkeypatch.setenv(k, v)
+    s = ref.assemble(50)
+    td = ref.td(s)
+    A = to_sdc(s.a)
+    V = sdc.submatrix(A, 0, s.n_vel, 0, s.n_vel)
+    amg = sdc.AmgPreconditioner(V, sdc.AmgOptions(components=[0] * s.n_u + [1] * (s.n_vel - s.n_u)))
+    r = ref.random_vector(s.n_vel, 8)
+    assert rel_l2(amg.apply(r), td.v_hierarchy.vcycle(r)) < 1e-11
+    g = golden("system_c1")
+    n = int(g["n_total"])
+    system = sdc.CoupledSystem(to_sdc(golden_csr(g, "A", n)), g["rhs"], int(g["n"]), int(g["n_u"]),
+                               int(g["n_vel"]), int(g["n_pff"]), int(g["n_ppm"]))
+    p = sdc.TdPreconditioner(system, "td_bgs", omega_override=float(g["omega"]))
+    assert rel_l2(p.apply(g["apply_r"]), g["apply_z"]) < 1e-10
+
+
 def check_linear(p, seed, n, tol=1e-13):
     # test_precond.cpp:33-47
     rng = np.random.default_rng(seed)
