@@ -48,6 +48,10 @@ using namespace ptx;
 
 namespace {
 
+#ifndef SDG_WALK_EXP
+#define SDG_WALK_EXP 0  // dev knock-out experiments (scripts/mb_real2.cu); 0 in the product
+#endif
+
 #ifdef SDG_WALK_TRACE  // dev aid (scripts/mb_real2.cu): per-level clocks of lane 0 of every warp
 __device__ long long g_walk_trace[1024 * 16 * 4];
 #define WALK_CLK(L, k)                                          \
@@ -80,7 +84,9 @@ constexpr int max_threads(int r2, int r8, int kw) {
 }
 
 // shapes whose instantiation fits the register file without spills (ptxas -v)
-constexpr bool shape_ok(int r2, int r8, int kw) { return kw == 16 ? (r8 <= 1 && r2 <= 4) : !(r2 >= 5 && r8 == 3); }
+constexpr bool shape_ok(int r2, int r8, int kw) {
+    return kw == 16 ? (r8 <= 1 && r2 <= 4) : (r2 + 2 * r8 <= 9 && !(r8 == 3 && r2 >= 4));
+}
 
 __device__ __forceinline__ int ld_volatile(const int* p) {
     int v;
@@ -119,22 +125,66 @@ struct WalkArgs {
     double* z_new;
 };
 
-// Rows a consumer thread holds for one level: R2 small + R8 wide rows (the
-// sources, scalars and the shared address of each record's coefficients).
+// 32-bit shared-memory accesses through explicit addresses (kept in
+// registers; the compiler would otherwise re-derive them from the kernel
+// parameters with constant loads on the critical path)
+__device__ __forceinline__ unsigned keep(unsigned x) {
+    unsigned y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+__device__ __forceinline__ int4 lds4(unsigned a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int2 lds2(unsigned a) {
+    int2 v;
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double ldsd(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 ldsd2(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void stsd(unsigned a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
+// A thread's rows for one level in two forms: the raw record words just
+// loaded from the stage (Raw) and the ready-to-use addresses derived from
+// them one level later (Rows: gather sources, ring and pin stores, global z,
+// coefficients).  Splitting the two keeps the record loads' latency off the
+// in-order issue stream.
+template <int R2, int R8, int KW>
+struct WalkRaw {
+    int4 h2[R2 > 0 ? R2 : 1], h8[R8 > 0 ? R8 : 1];       // {b lo, b hi, rowid, pin}
+    int2 s2[R2 > 0 ? R2 : 1];                            // sources of small rows
+    int4 s8[R8 > 0 ? R8 : 1][KW == 8 ? 2 : (KW + 7) / 8];  // sources of wide rows (32- or 16-bit)
+    unsigned q2[R2 > 0 ? R2 : 1], q8[R8 > 0 ? R8 : 1];   // record addresses
+    int4 m;                                              // the level's meta
+};
+
 template <int R2, int R8, int KW>
 struct WalkRows {
     double b2[R2 > 0 ? R2 : 1], b8[R8 > 0 ? R8 : 1];
-    int s2[R2 > 0 ? R2 : 1][2], s8[R8 > 0 ? R8 : 1][KW];
-    int rid2[R2 > 0 ? R2 : 1], pin2[R2 > 0 ? R2 : 1], wp2[R2 > 0 ? R2 : 1];
-    int rid8[R8 > 0 ? R8 : 1], pin8[R8 > 0 ? R8 : 1], wp8[R8 > 0 ? R8 : 1];
-    const unsigned char* vp2[R2 > 0 ? R2 : 1];
-    const unsigned char* vp8[R8 > 0 ? R8 : 1];
+    unsigned s2[R2 > 0 ? R2 : 1][2], s8[R8 > 0 ? R8 : 1][KW];
+    unsigned wa2[R2 > 0 ? R2 : 1], pa2[R2 > 0 ? R2 : 1], va2[R2 > 0 ? R2 : 1];
+    unsigned wa8[R8 > 0 ? R8 : 1], pa8[R8 > 0 ? R8 : 1], va8[R8 > 0 ? R8 : 1];
+    int rid2[R2 > 0 ? R2 : 1], rid8[R8 > 0 ? R8 : 1];
 };
 
-// The level loop of one consumer warp (see the file comment).  Records are
-// fetched two levels ahead (two register sets, alternating), so neither the
-// record loads nor their addresses are on the per-level critical path
-//   gathers (shared) -> FMAs -> ring store -> level hand-off.
+// The level loop of one consumer warp (see the file comment).  Three-stage
+// software pipeline per level L: solve level L (gathers -> FMAs -> ring/pin
+// stores, global z), turn level L+1's raw record words into addresses, load
+// level L+2's raw records; then the level hand-off.  The critical path per
+// level is gathers -> FMAs -> ring store -> hand-off.
 template <int R2, int R8, int KW>
 __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* meta, const unsigned char* stage,
                                               const unsigned char* nullrec, double* zr, int* flags) {
@@ -142,8 +192,12 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     const int nw = (blockDim.x >> 5) - 1;
     const int t0 = threadIdx.x - 32;  // (warp - 1) * 32 + lane
     const int stride = 32 * nw;
+    const int n_levels = a.n_levels;
+    const unsigned stage_s = smem_addr(stage), null_s = smem_addr(nullrec), zr_s = smem_addr(zr);
+    double* const z_new = a.z_new;
     int* progress = flags;
     const int* landed = flags + 1;
+    using Raw = WalkRaw<R2, R8, KW>;
     using Rows = WalkRows<R2, R8, KW>;
     constexpr int WB = wide_bytes(KW);
     auto wait_landed = [&](const int4 m) {
@@ -152,73 +206,89 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
             while (ld_acquire(landed) < need) {
             }
     };
-    auto fetch = [&](Rows& x, const int4 m) {
+    auto load_raw = [&](Raw& w, const int4 m) {
+        w.m = m;
+#pragma unroll
+        for (int r = 0; r < R2; ++r) {
+            const int u = r * stride + t0;
+            const unsigned q = u < (m.z >> 20) ? stage_s + m.x + u * kK2Bytes : null_s;
+            w.q2[r] = q;
+            w.h2[r] = lds4(q);
+            w.s2[r] = lds2(q + 32);
+        }
+#pragma unroll
+        for (int r = 0; r < R8; ++r) {
+            const int u = r * stride + t0;
+            const unsigned q = u < (m.w >> 20) ? stage_s + (m.y & 0x3ffff) + u * WB : null_s + 128;
+            w.q8[r] = q;
+            w.h8[r] = lds4(q);
+#pragma unroll
+            for (int j = 0; j < (KW == 8 ? 2 : (KW + 7) / 8); ++j)
+                w.s8[r][j] = lds4(q + (KW == 8 ? 80 : wide_src_off(KW)) + 16 * j);
+        }
+    };
+    auto unpack = [&](Rows& x, const Raw& w) {
+        const int4 m = w.m;
 #pragma unroll
         for (int r = 0; r < R2; ++r) {
             const int u = r * stride + t0;
             const bool ok = u < (m.z >> 20);
-            const unsigned char* q = ok ? stage + m.x + u * kK2Bytes : nullrec;
-            const int4 h = *reinterpret_cast<const int4*>(q);
-            const int2 ss = *reinterpret_cast<const int2*>(q + 32);
-            x.b2[r] = __hiloint2double(h.y, h.x);
-            x.rid2[r] = h.z;
-            x.pin2[r] = h.w;
-            x.s2[r][0] = ss.x;
-            x.s2[r][1] = ss.y;
-            x.vp2[r] = q + 16;
-            x.wp2[r] = ok ? (((m.z & 0xfffff) + u) & mask) : dummy;
+            x.b2[r] = __hiloint2double(w.h2[r].y, w.h2[r].x);
+            x.rid2[r] = w.h2[r].z;
+            x.pa2[r] = zr_s + 8u * w.h2[r].w;
+            x.s2[r][0] = zr_s + 8u * w.s2[r].x;
+            x.s2[r][1] = zr_s + 8u * w.s2[r].y;
+            x.va2[r] = w.q2[r] + 16;
+            x.wa2[r] = zr_s + 8u * (ok ? (((m.z & 0xfffff) + u) & mask) : dummy);
         }
 #pragma unroll
         for (int r = 0; r < R8; ++r) {
             const int u = r * stride + t0;
             const bool ok = u < (m.w >> 20);
-            const unsigned char* q = ok ? stage + (m.y & 0x3ffff) + u * WB : nullrec + 128;
-            const int4 h = *reinterpret_cast<const int4*>(q);
-            x.b8[r] = __hiloint2double(h.y, h.x);
-            x.rid8[r] = h.z;
-            x.pin8[r] = h.w;
+            x.b8[r] = __hiloint2double(w.h8[r].y, w.h8[r].x);
+            x.rid8[r] = w.h8[r].z;
+            x.pa8[r] = zr_s + 8u * w.h8[r].w;
             if constexpr (KW == 8) {
-                const int4 x0 = *reinterpret_cast<const int4*>(q + 80);
-                const int4 x1 = *reinterpret_cast<const int4*>(q + 96);
-                x.s8[r][0] = x0.x; x.s8[r][1] = x0.y; x.s8[r][2 % KW] = x0.z; x.s8[r][3 % KW] = x0.w;
-                x.s8[r][4 % KW] = x1.x; x.s8[r][5 % KW] = x1.y; x.s8[r][6 % KW] = x1.z; x.s8[r][7 % KW] = x1.w;
-            } else {  // 16-bit sources
-                unsigned w[(KW + 7) / 8 * 4];
+                const int sv[8] = {w.s8[r][0].x, w.s8[r][0].y, w.s8[r][0].z, w.s8[r][0].w,
+                                   w.s8[r][1 % 2].x, w.s8[r][1 % 2].y, w.s8[r][1 % 2].z, w.s8[r][1 % 2].w};
+#pragma unroll
+                for (int k = 0; k < KW; ++k) x.s8[r][k] = zr_s + 8u * sv[k % 8];
+            } else {
+                unsigned wd[(KW + 7) / 8 * 4];
 #pragma unroll
                 for (int j = 0; j < (KW + 7) / 8; ++j) {
-                    const int4 x0 = *reinterpret_cast<const int4*>(q + wide_src_off(KW) + 16 * j);
-                    w[4 * j] = x0.x;
-                    w[4 * j + 1] = x0.y;
-                    w[4 * j + 2] = x0.z;
-                    w[4 * j + 3] = x0.w;
+                    wd[4 * j] = w.s8[r][j].x;
+                    wd[4 * j + 1] = w.s8[r][j].y;
+                    wd[4 * j + 2] = w.s8[r][j].z;
+                    wd[4 * j + 3] = w.s8[r][j].w;
                 }
 #pragma unroll
-                for (int k = 0; k < KW; ++k) x.s8[r][k] = (w[k / 2] >> (16 * (k % 2))) & 0xffff;
+                for (int k = 0; k < KW; ++k) x.s8[r][k] = zr_s + 8u * ((wd[k / 2] >> (16 * (k % 2))) & 0xffff);
             }
-            x.vp8[r] = q + 16;
-            x.wp8[r] = ok ? (((m.w & 0xfffff) + u) & mask) : dummy;
+            x.va8[r] = w.q8[r] + 16;
+            x.wa8[r] = zr_s + 8u * (ok ? (((m.w & 0xfffff) + u) & mask) : dummy);
         }
     };
-    // solve the rows of level L held in x, then fetch level L+2 into x
-    auto step = [&](int L, Rows& x) {
+    // solve level L (rows in x), unpack level L+1 (raw w) into y, load level L+2 into w
+    auto step = [&](int L, const Rows& x, Rows& y, Raw& w) {
         WALK_CLK(L, 0);
         double z2[R2 > 0 ? R2 : 1][2], v2[R2 > 0 ? R2 : 1][2];
         double z8[R8 > 0 ? R8 : 1][KW], v8[R8 > 0 ? R8 : 1][KW];
 #pragma unroll
         for (int r = 0; r < R2; ++r) {
-            z2[r][0] = zr[x.s2[r][0]];
-            z2[r][1] = zr[x.s2[r][1]];
-            const double2 c = *reinterpret_cast<const double2*>(x.vp2[r]);
+            z2[r][0] = ldsd(x.s2[r][0]);
+            z2[r][1] = ldsd(x.s2[r][1]);
+            const double2 c = ldsd2(x.va2[r]);
             v2[r][0] = c.x;
             v2[r][1] = c.y;
         }
 #pragma unroll
         for (int r = 0; r < R8; ++r) {
 #pragma unroll
-            for (int k = 0; k < KW; ++k) z8[r][k] = zr[x.s8[r][k]];
+            for (int k = 0; k < KW; ++k) z8[r][k] = ldsd(x.s8[r][k]);
 #pragma unroll
             for (int k = 0; k < KW / 2; ++k) {
-                const double2 c = reinterpret_cast<const double2*>(x.vp8[r])[k];
+                const double2 c = ldsd2(x.va8[r] + 16 * k);
                 v8[r][2 * k] = c.x;
                 v8[r][2 * k + 1] = c.y;
             }
@@ -227,9 +297,9 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
 #pragma unroll
         for (int r = 0; r < R2; ++r) {
             const double acc = fma(v2[r][1], z2[r][1], fma(v2[r][0], z2[r][0], x.b2[r]));
-            zr[x.wp2[r]] = acc;
-            zr[x.pin2[r]] = acc;
-            if (x.rid2[r] >= 0) a.z_new[x.rid2[r]] = acc;
+            stsd(x.wa2[r], acc);
+            stsd(x.pa2[r], acc);
+            if (!(SDG_WALK_EXP & 2) && x.rid2[r] >= 0) z_new[x.rid2[r]] = acc;
         }
 #pragma unroll
         for (int r = 0; r < R8; ++r) {
@@ -241,35 +311,40 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
 #pragma unroll
             for (int j = 1; j < KW / 2; ++j) qq[j] = fma(v[2 * j + 1], z[2 * j + 1], v[2 * j] * z[2 * j]);
 #pragma unroll
-            for (int w = 1; w < KW / 2; w *= 2)
+            for (int j2 = 1; j2 < KW / 2; j2 *= 2)
 #pragma unroll
-                for (int j = 0; j + w < KW / 2; j += 2 * w) qq[j] += qq[j + w];
+                for (int j = 0; j + j2 < KW / 2; j += 2 * j2) qq[j] += qq[j + j2];
             const double acc = qq[0];
-            zr[x.wp8[r]] = acc;
-            zr[x.pin8[r]] = acc;
-            if (x.rid8[r] >= 0) a.z_new[x.rid8[r]] = acc;
+            stsd(x.wa8[r], acc);
+            stsd(x.pa8[r], acc);
+            if (!(SDG_WALK_EXP & 2) && x.rid8[r] >= 0) z_new[x.rid8[r]] = acc;
         }
         WALK_CLK(L, 1);
-        wait_landed(m2);
-        fetch(x, m2);
+        unpack(y, w);
+        if (!(SDG_WALK_EXP & 8)) {
+            wait_landed(m2);
+            load_raw(w, m2);
+        }
         WALK_CLK(L, 2);
         if (nw == 1)
             __syncwarp();
         else
             asm volatile("bar.sync 1, %0;" ::"r"(stride) : "memory");
-        if (threadIdx.x == 32) st_volatile(progress, L + 1);
+        if (!(SDG_WALK_EXP & 1) && threadIdx.x == 32) st_volatile(progress, L + 1);
     };
     Rows x, y;
+    Raw w;
     {
         const int4 m0 = meta[0], m1 = meta[1];
         wait_landed(m0);
-        fetch(x, m0);
+        load_raw(w, m0);
+        unpack(x, w);
         wait_landed(m1);
-        fetch(y, m1);
+        load_raw(w, m1);
     }
-    for (int L = 0; L < a.n_levels; L += 2) {
-        step(L, x);
-        if (L + 1 < a.n_levels) step(L + 1, y);
+    for (int L = 0; L < n_levels; L += 2) {
+        step(L, x, y, w);
+        if (L + 1 < n_levels) step(L + 1, y, x, w);
     }
 }
 
