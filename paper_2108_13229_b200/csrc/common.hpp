@@ -121,6 +121,7 @@ struct Context {
     std::atomic<int64_t> launches{0};
     std::unique_ptr<PinnedBuf> pinned;   // status words, small host reads
     void* cusolver = nullptr;            // lazily created cusolverDnHandle_t
+    bool pdl = true;                     // programmatic dependent launch (launch.cuh; SDG_PDL=0 off)
 
     // live profiler: CUDA events bracketing every launch of a family
     struct ProfRec {

@@ -24,6 +24,7 @@
 // are odd multiples of 16 bytes, so 16-byte shared loads of consecutive
 // records are bank-conflict free.
 #include "gs.cuh"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 #include <cooperative_groups.h>
@@ -56,6 +57,7 @@ __host__ __device__ inline int pad16(int64_t b) { return static_cast<int>((b + 1
 
 __global__ void k_gs_prep_pre(int n, const double* __restrict__ r, const double* __restrict__ dinv,
                               const int* __restrict__ bidx, double* __restrict__ packed) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) packed[bidx[i]] = r[i] * dinv[i];
 }
@@ -64,6 +66,7 @@ __global__ void k_gs_prep_pre(int n, const double* __restrict__ r, const double*
 __global__ void k_gs_couple(int rows, int r0, const int* __restrict__ rp, const int* __restrict__ ci,
                             const double* __restrict__ v, const double* __restrict__ z,
                             const int* __restrict__ bidx, double* __restrict__ packed) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows) return;
     double acc = 0.0;
@@ -76,6 +79,7 @@ __global__ void k_gs_prep_post(int n, const int* __restrict__ urp, const int* __
                                const double* __restrict__ z, const double* __restrict__ zc,
                                const int* __restrict__ agg, const double* __restrict__ dinv,
                                const int* __restrict__ bidx, double* __restrict__ packed) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double s = r[i];
@@ -174,6 +178,7 @@ k_gs_cluster(const int4* __restrict__ meta_g, const int4* __restrict__ band_info
              const int* __restrict__ packet_bytes, const int4* __restrict__ chunks_g,
              const double* __restrict__ packed, int ring, int halo, int depth, int max_chunk,
              int meta_bytes, int chunk_tab_bytes, int pbar_bytes, double* z_new) {
+    pdl_begin();
     extern __shared__ __align__(128) unsigned char sm[];
     cg::cluster_group cluster = cg::this_cluster();
     const int band = static_cast<int>(cluster.block_rank());
@@ -310,6 +315,7 @@ __global__ void k_restrict_warp(int n_coarse, const int* __restrict__ pt_ptr,
                                 const double* __restrict__ r, const double* __restrict__ z,
                                 double* __restrict__ rc, const double* __restrict__ next_dinv,
                                 const int* __restrict__ next_bidx, double* __restrict__ next_packed) {
+    pdl_begin();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= n_coarse) return;
@@ -789,7 +795,7 @@ bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std
 void launch_gs_prep_pre(Context& c, const GsPlan& g, const double* r) {
     ProfScope ps_(c, PF_GSPREP, 24.0 * g.n + 8.0 * g.n);
     if (g.n == 0) return;
-    k_gs_prep_pre<<<(g.n + 255) / 256, 256, 0, c.stream>>>(g.n, r, g.dinv.get(), g.bidx.get(),
+    launch_k(c, k_gs_prep_pre, (g.n + 255) / 256, 256, 0, g.n, r, g.dinv.get(), g.bidx.get(),
                                                             const_cast<double*>(g.packed.get()));
     SDG_GS_CHECK();
 }
@@ -800,7 +806,7 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
                   12.0 * g.upper.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (z ? 2 : 1) + (zc ? 12.0 * g.n : 0.0) +
                       16.0 * g.n);
     if (g.n == 0) return;
-    k_gs_prep_post<<<(g.n + 255) / 256, 256, 0, c.stream>>>(
+    launch_k(c, k_gs_prep_post, (g.n + 255) / 256, 256, 0, 
         g.n, g.upper.rp.get(), g.upper.ci.get(), g.upper.v.get(), r, z, zc, agg, g.dinv.get(),
         g.bidx.get(), const_cast<double*>(g.packed.get()));
     SDG_GS_CHECK();
@@ -812,7 +818,7 @@ void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
             if (k > 0) {
                 const DevCsr& cp = g.couple[k];
                 ProfScope ps_(c, PF_GSPREP, 12.0 * cp.nnz + 4.0 * (cp.n_rows + 1) + 28.0 * cp.n_rows);
-                k_gs_couple<<<(cp.n_rows + 255) / 256, 256, 0, c.stream>>>(
+                launch_k(c, k_gs_couple, (cp.n_rows + 255) / 256, 256, 0, 
                     cp.n_rows, g.part_r0[k], cp.rp.get(), cp.ci.get(), cp.v.get(), z_new, g.bidx.get(),
                     const_cast<double*>(g.packed.get()));
                 SDG_GS_CHECK();
@@ -857,7 +863,7 @@ void launch_restrict_warp(Context& c, const DevCsr& a, const int* pt_ptr, const 
     if (n_coarse == 0) return;
     const int threads = 256;
     const int blocks = static_cast<int>((static_cast<int64_t>(n_coarse) * 32 + threads - 1) / threads);
-    k_restrict_warp<<<blocks, threads, 0, c.stream>>>(
+    launch_k(c, k_restrict_warp, blocks, threads, 0, 
         n_coarse, pt_ptr, pt_rows, a.rp.get(), a.ci.get(), a.v.get(), r, z, rc,
         next ? next->dinv.get() : nullptr, next ? next->bidx.get() : nullptr,
         next ? const_cast<double*>(next->packed.get()) : nullptr);

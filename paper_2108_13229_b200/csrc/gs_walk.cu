@@ -40,6 +40,7 @@
 #include <utility>
 
 #include "gs.cuh"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace sdg {
@@ -385,12 +386,17 @@ __global__ void __launch_bounds__(max_threads(R2, R8, KW), 1) k_gs_walk(WalkArgs
     }
     fence_mbar_init();
     __syncthreads();
+    pdl_trigger();  // the next kernel may launch (it waits for this grid itself)
 
     if (tid >= 32) {
         walk_consumer<R2, R8, KW>(a, meta, stage, nullrec, zr, flags);
         return;
     }
     if (tid != 0) return;
+    // the records' b values come from the previous kernel (prep / restriction):
+    // the setup above overlapped it, the copies wait for it.  Consumers touch
+    // global memory only after `landed` shows copies issued after this wait.
+    pdl_wait();
     // producer: issue chunk copies once the consumers' progress frees their
     // ring space, publish each chunk once it has landed
     int ci = 0, cw = 0;
@@ -728,7 +734,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new) {
     WalkArgs a{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.records()),
                g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes, z_new};
-    walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw)<<<1, g.nthreads, g.smem, c.stream>>>(a);
+    launch_k(c, walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw), 1, g.nthreads, g.smem, a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(SDG_ECUDA, std::string("launch_gs_walk: ") + cudaGetErrorString(e));
     c.count();

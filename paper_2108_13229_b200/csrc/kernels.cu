@@ -1,5 +1,6 @@
 // Device kernels of the hot path.  See kernels.cuh for the contracts.
 #include "kernels.cuh"
+#include "launch.cuh"
 
 #include <algorithm>
 #include <string>
@@ -80,6 +81,7 @@ __global__ void k_spmv(int n, const int* __restrict__ rp, const int* __restrict_
                        const double* __restrict__ v, const double* __restrict__ x,
                        const double* __restrict__ y_in, double* __restrict__ y, double alpha,
                        int add) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double sum = 0.0;
@@ -96,6 +98,7 @@ __global__ void __launch_bounds__(kGsThreads)
 k_gs_levels(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
             const int* __restrict__ lvl_ptr, const int* __restrict__ lvl_rows, int n_levels,
             const double* __restrict__ r, const double* z_old, double* z_new, double omega) {
+    pdl_begin();
     for (int l = 0; l < n_levels; ++l) {
         const int b = lvl_ptr[l], e = lvl_ptr[l + 1];
         for (int idx = b + threadIdx.x; idx < e; idx += blockDim.x) {
@@ -126,6 +129,7 @@ __global__ void k_resid_restrict(int n_coarse, const int* __restrict__ pt_ptr,
                                  const int* __restrict__ ci, const double* __restrict__ v,
                                  const double* __restrict__ r, const double* __restrict__ z,
                                  double* __restrict__ rc) {
+    pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= n_coarse) return;
     double acc = 0.0;
@@ -143,6 +147,7 @@ __global__ void k_resid_restrict(int n_coarse, const int* __restrict__ pt_ptr,
 // BITWISE: precond.cpp:247
 __global__ void k_prolong(int n, const int* __restrict__ agg, const double* __restrict__ z,
                           const double* __restrict__ zc, double* __restrict__ out) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = __dadd_rn(z[i], zc[agg[i]]);
 }
@@ -150,6 +155,7 @@ __global__ void k_prolong(int n, const int* __restrict__ agg, const double* __re
 // y = Ainv x, one warp per row.
 __global__ void k_dense_gemv(int n, const double* __restrict__ a, const double* __restrict__ x,
                              double* __restrict__ y) {
+    pdl_begin();
     const int warps = blockDim.x >> 5;
     const int row = blockIdx.x * warps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -173,6 +179,7 @@ __global__ void k_dense_gemv(int n, const double* __restrict__ a, const double* 
 __global__ void k_uzawa_p(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                           const double* __restrict__ v, const double* __restrict__ zv,
                           const double* __restrict__ r_p, double omega, double* __restrict__ z_p) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double sum = 0.0;
@@ -182,12 +189,14 @@ __global__ void k_uzawa_p(int n, const int* __restrict__ rp, const int* __restri
 }
 
 __global__ void k_copy(int64_t n, double* __restrict__ d, const double* __restrict__ s) {
+    pdl_begin();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         d[i] = s[i];
 }
 
 __global__ void k_fill(int64_t n, double* __restrict__ d, double val) {
+    pdl_begin();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         d[i] = val;
@@ -195,12 +204,14 @@ __global__ void k_fill(int64_t n, double* __restrict__ d, double val) {
 
 __global__ void k_csr_to_dense(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                                const double* __restrict__ v, double* __restrict__ dense) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     for (int k = rp[i]; k < rp[i + 1]; ++k) dense[static_cast<size_t>(i) * n + ci[k]] = v[k];
 }
 
 __global__ void k_set_identity(int n, double* dense) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dense[static_cast<size_t>(i) * n + i] = 1.0;
 }
@@ -213,6 +224,7 @@ __global__ void k_set_identity(int n, double* dense) {
 __global__ void k_multidot(int64_t n, int k, const double* __restrict__ X, int64_t ldx,
                            const double* __restrict__ y, int64_t chunk, double* partials,
                            unsigned* ticket, double* __restrict__ out) {
+    pdl_begin();
     __shared__ bool am_last;
     __shared__ double red[kThreads / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -255,6 +267,7 @@ template <bool NORM>
 __global__ void k_multi_axpy(int64_t n, int k, const double* __restrict__ X, int64_t ldx,
                              const double* __restrict__ h, double* __restrict__ w,
                              double* partials, unsigned* ticket, double* out) {
+    pdl_begin();
     __shared__ double hs[kMaxDotVecs];
     if (threadIdx.x < k) hs[threadIdx.x] = h[threadIdx.x];
     __syncthreads();
@@ -274,6 +287,7 @@ __global__ void k_multi_axpy(int64_t n, int k, const double* __restrict__ X, int
 // BITWISE: reference `scale(vi, 1.0 / wn)` (krylov.cpp:115-117)
 __global__ void k_scale_by_inv(int64_t n, const double* __restrict__ src,
                                const double* __restrict__ den, double* __restrict__ dst) {
+    pdl_begin();
     const double d = *den;
     if (!(d > 0.0)) return;
     const double inv = 1.0 / d;
@@ -285,6 +299,7 @@ __global__ void k_scale_by_inv(int64_t n, const double* __restrict__ src,
 // BITWISE: krylov.cpp:153-154 (fill + axpy loop, sequential in v)
 __global__ void k_lincomb(int64_t n, int k, const double* __restrict__ X, int64_t ldx,
                           const double* __restrict__ y, double* __restrict__ w) {
+    pdl_begin();
     __shared__ double ys[kMaxDotVecs];
     if (threadIdx.x < k) ys[threadIdx.x] = y[threadIdx.x];
     __syncthreads();
@@ -297,6 +312,7 @@ __global__ void k_lincomb(int64_t n, int k, const double* __restrict__ X, int64_
 }
 
 __global__ void k_add_inplace(int64_t n, double* __restrict__ x, const double* __restrict__ z) {
+    pdl_begin();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         x[i] = __dadd_rn(x[i], z[i]);
@@ -304,6 +320,7 @@ __global__ void k_add_inplace(int64_t n, double* __restrict__ x, const double* _
 
 __global__ void k_axpy_dev(int64_t n, const double* __restrict__ alpha,
                            const double* __restrict__ x, double* __restrict__ y) {
+    pdl_begin();
     const double a = *alpha;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -312,6 +329,7 @@ __global__ void k_axpy_dev(int64_t n, const double* __restrict__ alpha,
 
 __global__ void k_dot(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
                       double* partials, unsigned* ticket, double* out) {
+    pdl_begin();
     double acc[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -322,6 +340,7 @@ __global__ void k_dot(int64_t n, const double* __restrict__ x, const double* __r
 // BITWISE: krylov.cpp:337
 __global__ void k_div_scalar(int64_t n, const double* __restrict__ y, const double* __restrict__ yn,
                              double* __restrict__ x) {
+    pdl_begin();
     const double d = *yn;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -334,6 +353,7 @@ __global__ void k_div_scalar(int64_t n, const double* __restrict__ y, const doub
 
 __global__ void k_bi_p(int64_t n, BiState* st, const double* __restrict__ r,
                        const double* __restrict__ v, double* __restrict__ p) {
+    pdl_begin();
     if (st->flag) return;
     const double rho_new = st->rho_new;
     if (fabs(rho_new) < 1e-300) {
@@ -349,6 +369,7 @@ __global__ void k_bi_p(int64_t n, BiState* st, const double* __restrict__ r,
 
 __global__ void k_bi_rv(int64_t n, BiState* st, const double* __restrict__ rhat,
                         const double* __restrict__ v, double* partials, unsigned* ticket) {
+    pdl_begin();
     double acc[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -366,6 +387,7 @@ __global__ void k_bi_rv(int64_t n, BiState* st, const double* __restrict__ rhat,
 __global__ void k_bi_s(int64_t n, BiState* st, const double* __restrict__ r,
                        const double* __restrict__ v, double* __restrict__ s, double* partials,
                        unsigned* ticket) {
+    pdl_begin();
     const int flag = st->flag;  // uniform for the whole launch
     double acc[1] = {0.0};
     if (!flag) {
@@ -386,6 +408,7 @@ __global__ void k_bi_s(int64_t n, BiState* st, const double* __restrict__ r,
 
 __global__ void k_bi_t(int64_t n, BiState* st, const double* __restrict__ t,
                        const double* __restrict__ s, double* partials, unsigned* ticket) {
+    pdl_begin();
     const int flag = st->flag;
     double acc[2] = {0.0, 0.0};
     if (!flag) {
@@ -417,6 +440,7 @@ __global__ void k_bi_xr(int64_t n, BiState* st, const double* __restrict__ phat,
                         const double* __restrict__ t, const double* __restrict__ rhat,
                         double* __restrict__ x, double* __restrict__ r, double* partials,
                         unsigned* ticket) {
+    pdl_begin();
     const int flag = st->flag;
     double acc[2] = {0.0, 0.0};
     if (!flag) {
@@ -440,6 +464,7 @@ __global__ void k_bi_xr(int64_t n, BiState* st, const double* __restrict__ phat,
 
 __global__ void k_bi_rho(int64_t n, BiState* st, const double* __restrict__ rhat,
                          const double* __restrict__ r, double* partials, unsigned* ticket) {
+    pdl_begin();
     double acc[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -449,6 +474,7 @@ __global__ void k_bi_rho(int64_t n, BiState* st, const double* __restrict__ rhat
 
 __global__ void k_bi_x_alpha(int64_t n, const BiState* st, const double* __restrict__ phat,
                              double* __restrict__ x) {
+    pdl_begin();
     const double a = st->alpha;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -489,7 +515,7 @@ static inline int stride_blocks(Context& c, int64_t n) {
 void launch_spmv(Context& c, const DevCsr& a, const double* x, double* y) {
     ProfScope ps_(c, PF_SPMV, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 8.0 * a.n_rows);
     if (a.n_rows == 0) return;
-    k_spmv<<<blocks_for(a.n_rows), kThreads, 0, c.stream>>>(a.n_rows, a.rp.get(), a.ci.get(),
+    launch_k(c, k_spmv, blocks_for(a.n_rows), kThreads, 0, a.n_rows, a.rp.get(), a.ci.get(),
                                                             a.v.get(), x, nullptr, y, 0.0, 0);
     SDG_LAUNCHED(c);
 }
@@ -498,7 +524,7 @@ void launch_spmv_add(Context& c, const DevCsr& a, const double* x, const double*
                      double* y_out, double alpha) {
     ProfScope ps_(c, PF_SPMV, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 16.0 * a.n_rows);
     if (a.n_rows == 0) return;
-    k_spmv<<<blocks_for(a.n_rows), kThreads, 0, c.stream>>>(a.n_rows, a.rp.get(), a.ci.get(),
+    launch_k(c, k_spmv, blocks_for(a.n_rows), kThreads, 0, a.n_rows, a.rp.get(), a.ci.get(),
                                                             a.v.get(), x, y_in, y_out, alpha, 1);
     SDG_LAUNCHED(c);
 }
@@ -508,7 +534,7 @@ void launch_gs_levels(Context& c, const DevCsr& a, const int* lvl_ptr, const int
                       double omega) {
     ProfScope ps_(c, PF_GS, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + (z_old ? 24.0 : 16.0) * a.n_rows + 4.0 * a.n_rows + 4.0 * (n_levels + 1));
     if (a.n_rows == 0) return;
-    k_gs_levels<<<1, kGsThreads, 0, c.stream>>>(a.rp.get(), a.ci.get(), a.v.get(), lvl_ptr,
+    launch_k(c, k_gs_levels, 1, kGsThreads, 0, a.rp.get(), a.ci.get(), a.v.get(), lvl_ptr,
                                                 lvl_rows, n_levels, r, z_old, z_new, omega);
     SDG_LAUNCHED(c);
 }
@@ -517,7 +543,7 @@ void launch_resid_restrict(Context& c, const DevCsr& a, const int* pt_ptr, const
                            int n_coarse, const double* r, const double* z, double* rc) {
     ProfScope ps_(c, PF_RESTRICT, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 16.0 * a.n_rows + 4.0 * a.n_rows + 4.0 * (n_coarse + 1) + 8.0 * n_coarse);
     if (n_coarse == 0) return;
-    k_resid_restrict<<<blocks_for(n_coarse, 128), 128, 0, c.stream>>>(
+    launch_k(c, k_resid_restrict, blocks_for(n_coarse, 128), 128, 0, 
         n_coarse, pt_ptr, pt_rows, a.rp.get(), a.ci.get(), a.v.get(), r, z, rc);
     SDG_LAUNCHED(c);
 }
@@ -526,7 +552,7 @@ void launch_prolong(Context& c, int n, const int* agg, const double* z, const do
                     double* out) {
     ProfScope ps_(c, PF_PROLONG, 20.0 * n + 8.0 * n);
     if (n == 0) return;
-    k_prolong<<<blocks_for(n), kThreads, 0, c.stream>>>(n, agg, z, zc, out);
+    launch_k(c, k_prolong, blocks_for(n), kThreads, 0, n, agg, z, zc, out);
     SDG_LAUNCHED(c);
 }
 
@@ -534,7 +560,7 @@ void launch_dense_gemv(Context& c, int n, const double* ainv, const double* x, d
     ProfScope ps_(c, PF_COARSE, 8.0 * n * (double)n + 16.0 * n);
     if (n == 0) return;
     const int warps = kThreads / 32;
-    k_dense_gemv<<<(n + warps - 1) / warps, kThreads, 0, c.stream>>>(n, ainv, x, y);
+    launch_k(c, k_dense_gemv, (n + warps - 1) / warps, kThreads, 0, n, ainv, x, y);
     SDG_LAUNCHED(c);
 }
 
@@ -542,7 +568,7 @@ void launch_uzawa_pressure(Context& c, const DevCsr& cm, const double* z_v, cons
                            double omega, double* z_p) {
     ProfScope ps_(c, PF_UZAWA, 12.0 * cm.nnz + 4.0 * (cm.n_rows + 1) + 8.0 * cm.n_cols + 16.0 * cm.n_rows);
     if (cm.n_rows == 0) return;
-    k_uzawa_p<<<blocks_for(cm.n_rows), kThreads, 0, c.stream>>>(cm.n_rows, cm.rp.get(), cm.ci.get(),
+    launch_k(c, k_uzawa_p, blocks_for(cm.n_rows), kThreads, 0, cm.n_rows, cm.rp.get(), cm.ci.get(),
                                                                 cm.v.get(), z_v, r_p, omega, z_p);
     SDG_LAUNCHED(c);
 }
@@ -550,21 +576,21 @@ void launch_uzawa_pressure(Context& c, const DevCsr& cm, const double* z_v, cons
 void launch_copy(Context& c, double* dst, const double* src, int64_t n) {
     ProfScope ps_(c, PF_VEC, 16.0 * n);
     if (n == 0 || dst == src) return;
-    k_copy<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, dst, src);
+    launch_k(c, k_copy, stride_blocks(c, n), kThreads, 0, n, dst, src);
     SDG_LAUNCHED(c);
 }
 
 void launch_fill(Context& c, double* dst, double v, int64_t n) {
     ProfScope ps_(c, PF_VEC, 8.0 * n);
     if (n == 0) return;
-    k_fill<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, dst, v);
+    launch_k(c, k_fill, stride_blocks(c, n), kThreads, 0, n, dst, v);
     SDG_LAUNCHED(c);
 }
 
 void launch_csr_to_dense(Context& c, const DevCsr& a, double* dense) {
     ProfScope ps_(c, PF_SETUP, 12.0 * a.nnz);
     if (a.n_rows == 0) return;
-    k_csr_to_dense<<<blocks_for(a.n_rows), kThreads, 0, c.stream>>>(a.n_rows, a.rp.get(),
+    launch_k(c, k_csr_to_dense, blocks_for(a.n_rows), kThreads, 0, a.n_rows, a.rp.get(),
                                                                     a.ci.get(), a.v.get(), dense);
     SDG_LAUNCHED(c);
 }
@@ -572,7 +598,7 @@ void launch_csr_to_dense(Context& c, const DevCsr& a, double* dense) {
 void launch_set_identity(Context& c, int n, double* dense) {
     ProfScope ps_(c, PF_SETUP, 8.0 * n);
     if (n == 0) return;
-    k_set_identity<<<blocks_for(n), kThreads, 0, c.stream>>>(n, dense);
+    launch_k(c, k_set_identity, blocks_for(n), kThreads, 0, n, dense);
     SDG_LAUNCHED(c);
 }
 
@@ -586,7 +612,7 @@ void launch_multidot(Context& c, ReduceWs& ws, int64_t n, int k, const double* X
     const int64_t chunk = std::max<int64_t>(1, (n + nb - 1) / nb);
     nb = static_cast<int>((n + chunk - 1) / chunk);
     if (nb < 1) nb = 1;
-    k_multidot<<<nb, kThreads, 0, c.stream>>>(n, k, X, ldx, y, chunk, ws.partials.get(),
+    launch_k(c, k_multidot, nb, kThreads, 0, n, k, X, ldx, y, chunk, ws.partials.get(),
                                               ws.ticket.get(), out);
     SDG_LAUNCHED(c);
 }
@@ -595,7 +621,7 @@ void launch_multi_axpy(Context& c, int64_t n, int k, const double* X, int64_t ld
                        const double* h, double* w) {
     ProfScope ps_(c, PF_ORTHO, 8.0 * (k + 2) * (double)n);
     if (k <= 0) return;
-    k_multi_axpy<false><<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, k, X, ldx, h, w,
+    launch_k(c, k_multi_axpy<false>, stride_blocks(c, n), kThreads, 0, n, k, X, ldx, h, w,
                                                                        nullptr, nullptr, nullptr);
     SDG_LAUNCHED(c);
 }
@@ -605,14 +631,14 @@ void launch_multi_axpy_norm2(Context& c, ReduceWs& ws, int64_t n, int k, const d
     ProfScope ps_(c, PF_ORTHO, 8.0 * (k + 2) * (double)n);
     const int nb = std::min(reduce_blocks(static_cast<int>(std::min<int64_t>(n, 1 << 30)), c.num_sms),
                             ws.max_blocks);
-    k_multi_axpy<true><<<nb, kThreads, 0, c.stream>>>(n, k, X, ldx, h, w, ws.partials.get(),
+    launch_k(c, k_multi_axpy<true>, nb, kThreads, 0, n, k, X, ldx, h, w, ws.partials.get(),
                                                       ws.ticket.get(), out);
     SDG_LAUNCHED(c);
 }
 
 void launch_scale_by_inv(Context& c, int64_t n, const double* src, const double* den, double* dst) {
     ProfScope ps_(c, PF_ORTHO, 16.0 * n);
-    k_scale_by_inv<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, src, den, dst);
+    launch_k(c, k_scale_by_inv, stride_blocks(c, n), kThreads, 0, n, src, den, dst);
     SDG_LAUNCHED(c);
 }
 
@@ -620,19 +646,19 @@ void launch_lincomb(Context& c, int64_t n, int k, const double* X, int64_t ldx, 
                     double* w) {
     ProfScope ps_(c, PF_ORTHO, 8.0 * (k + 1) * (double)n);
     if (k > kMaxDotVecs) fail(SDG_EINVAL, "lincomb: too many vectors");
-    k_lincomb<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, k, X, ldx, y, w);
+    launch_k(c, k_lincomb, stride_blocks(c, n), kThreads, 0, n, k, X, ldx, y, w);
     SDG_LAUNCHED(c);
 }
 
 void launch_add_inplace(Context& c, int64_t n, double* x, const double* z) {
     ProfScope ps_(c, PF_VEC, 24.0 * n);
-    k_add_inplace<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, x, z);
+    launch_k(c, k_add_inplace, stride_blocks(c, n), kThreads, 0, n, x, z);
     SDG_LAUNCHED(c);
 }
 
 void launch_axpy_dev(Context& c, int64_t n, const double* alpha, const double* x, double* y) {
     ProfScope ps_(c, PF_VEC, 24.0 * n);
-    k_axpy_dev<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, alpha, x, y);
+    launch_k(c, k_axpy_dev, stride_blocks(c, n), kThreads, 0, n, alpha, x, y);
     SDG_LAUNCHED(c);
 }
 
@@ -643,34 +669,34 @@ static inline int red_blocks(Context& c, ReduceWs& ws, int64_t n) {
 
 void launch_norm2sq(Context& c, ReduceWs& ws, int64_t n, const double* x, double* out) {
     ProfScope ps_(c, PF_VEC, 8.0 * n);
-    k_dot<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, x, x, ws.partials.get(),
+    launch_k(c, k_dot, red_blocks(c, ws, n), kThreads, 0, n, x, x, ws.partials.get(),
                                                            ws.ticket.get(), out);
     SDG_LAUNCHED(c);
 }
 
 void launch_dot(Context& c, ReduceWs& ws, int64_t n, const double* x, const double* y, double* out) {
     ProfScope ps_(c, PF_VEC, 16.0 * n);
-    k_dot<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, x, y, ws.partials.get(),
+    launch_k(c, k_dot, red_blocks(c, ws, n), kThreads, 0, n, x, y, ws.partials.get(),
                                                            ws.ticket.get(), out);
     SDG_LAUNCHED(c);
 }
 
 void launch_div_scalar(Context& c, int64_t n, const double* y, const double* yn, double* x) {
     ProfScope ps_(c, PF_VEC, 16.0 * n);
-    k_div_scalar<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, y, yn, x);
+    launch_k(c, k_div_scalar, stride_blocks(c, n), kThreads, 0, n, y, yn, x);
     SDG_LAUNCHED(c);
 }
 
 void launch_bi_p(Context& c, int64_t n, BiState* st, const double* r, const double* v, double* p) {
     ProfScope ps_(c, PF_BICG, 32.0 * n);
-    k_bi_p<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, st, r, v, p);
+    launch_k(c, k_bi_p, stride_blocks(c, n), kThreads, 0, n, st, r, v, p);
     SDG_LAUNCHED(c);
 }
 
 void launch_bi_rv(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double* rhat,
                   const double* v) {
     ProfScope ps_(c, PF_BICG, 16.0 * n);
-    k_bi_rv<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, rhat, v, ws.partials.get(),
+    launch_k(c, k_bi_rv, red_blocks(c, ws, n), kThreads, 0, n, st, rhat, v, ws.partials.get(),
                                                              ws.ticket.get());
     SDG_LAUNCHED(c);
 }
@@ -678,7 +704,7 @@ void launch_bi_rv(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double
 void launch_bi_s(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double* r,
                  const double* v, double* s) {
     ProfScope ps_(c, PF_BICG, 24.0 * n);
-    k_bi_s<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, r, v, s, ws.partials.get(),
+    launch_k(c, k_bi_s, red_blocks(c, ws, n), kThreads, 0, n, st, r, v, s, ws.partials.get(),
                                                             ws.ticket.get());
     SDG_LAUNCHED(c);
 }
@@ -686,7 +712,7 @@ void launch_bi_s(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double*
 void launch_bi_t(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double* t,
                  const double* s) {
     ProfScope ps_(c, PF_BICG, 16.0 * n);
-    k_bi_t<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, t, s, ws.partials.get(),
+    launch_k(c, k_bi_t, red_blocks(c, ws, n), kThreads, 0, n, st, t, s, ws.partials.get(),
                                                             ws.ticket.get());
     SDG_LAUNCHED(c);
 }
@@ -695,7 +721,7 @@ void launch_bi_xr(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double
                   const double* shat, const double* s, const double* t, const double* rhat,
                   double* x, double* r) {
     ProfScope ps_(c, PF_BICG, 64.0 * n);
-    k_bi_xr<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, phat, shat, s, t, rhat, x, r,
+    launch_k(c, k_bi_xr, red_blocks(c, ws, n), kThreads, 0, n, st, phat, shat, s, t, rhat, x, r,
                                                              ws.partials.get(), ws.ticket.get());
     SDG_LAUNCHED(c);
 }
@@ -703,14 +729,14 @@ void launch_bi_xr(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double
 void launch_bi_rho(Context& c, ReduceWs& ws, int64_t n, BiState* st, const double* rhat,
                    const double* r) {
     ProfScope ps_(c, PF_BICG, 16.0 * n);
-    k_bi_rho<<<red_blocks(c, ws, n), kThreads, 0, c.stream>>>(n, st, rhat, r, ws.partials.get(),
+    launch_k(c, k_bi_rho, red_blocks(c, ws, n), kThreads, 0, n, st, rhat, r, ws.partials.get(),
                                                               ws.ticket.get());
     SDG_LAUNCHED(c);
 }
 
 void launch_bi_x_alpha(Context& c, int64_t n, BiState* st, const double* phat, double* x) {
     ProfScope ps_(c, PF_BICG, 24.0 * n);
-    k_bi_x_alpha<<<stride_blocks(c, n), kThreads, 0, c.stream>>>(n, st, phat, x);
+    launch_k(c, k_bi_x_alpha, stride_blocks(c, n), kThreads, 0, n, st, phat, x);
     SDG_LAUNCHED(c);
 }
 

@@ -24,6 +24,7 @@ Context::Context(int dev) : device(dev) {
     SDG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     SDG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     pinned = std::make_unique<PinnedBuf>(64 * 1024);
+    if (const char* e = std::getenv("SDG_PDL")) pdl = e[0] != '0';
 }
 
 Context::~Context() {
