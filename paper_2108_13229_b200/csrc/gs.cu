@@ -387,19 +387,11 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     int nb = bands_hint > 0 ? bands_hint : (n >= 200000 ? 8 : n >= 80000 ? 4 : 1);
     if (bands_env) nb = std::max(1, std::atoi(bands_env));
     nb = std::max(1, std::min({nb, 8, std::max(1, n / 256)}));
-    const char* split_env = std::getenv("SDG_GS_SPLIT");  // test knob: label blocks even when one walk fits
-    const bool force_split = split_env && split_env[0] == '1';
-    if (want_walk && !force_split && build_walk(a, dinv_h, nlow, max_k, s)) {
-        dinv.upload(dinv_h, s);
-        upper.upload(up, s);
-        SDG_CUDA(cudaStreamSynchronize(s));
-        return;
-    }
-    // one walk per contiguous label block (e.g. u / v of the velocity block)
-    if (want_walk && comps.size() == static_cast<size_t>(n) && n > 0) {
-        std::vector<int> r0{0};
+    // contiguous label blocks (e.g. u / v of the velocity block)
+    std::vector<int> r0{0};
+    bool contiguous = comps.size() == static_cast<size_t>(n) && n > 0;
+    if (contiguous) {
         std::vector<int> seen;
-        bool contiguous = true;
         for (int i = 1; i < n; ++i)
             if (comps[i] != comps[i - 1]) r0.push_back(i);
         for (size_t k = 0; k < r0.size(); ++k) {
@@ -407,13 +399,22 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
             seen.push_back(comps[r0[k]]);
         }
         r0.push_back(n);
-        if (contiguous && r0.size() > 2 && build_parts(a, r0, dinv_h, s)) {
-            dinv.upload(dinv_h, s);
-            upper.upload(up, s);
-            SDG_CUDA(cudaStreamSynchronize(s));
-            return;
-        }
     }
+    auto finish = [&]() {
+        dinv.upload(dinv_h, s);
+        upper.upload(up, s);
+        SDG_CUDA(cudaStreamSynchronize(s));
+    };
+    const char* split_env = std::getenv("SDG_GS_SPLIT");  // test knob: sequential label-block walks
+    const bool force_split = split_env && split_env[0] == '1';
+    const char* pipe_env = std::getenv("SDG_GS_PIPE");
+    const bool try_pipe = !force_split && pipe_env && pipe_env[0] == '1';  // opt-in
+    // 1. two label blocks walked concurrently on a 2-CTA cluster
+    if (want_walk && try_pipe && contiguous && r0.size() == 3 && build_pipe(a, r0, dinv_h, s)) return finish();
+    // 2. one walk over the whole matrix
+    if (want_walk && !force_split && build_walk(a, dinv_h, nlow, max_k, s)) return finish();
+    // 3. one walk per label block, in sequence, with a coupling step
+    if (want_walk && contiguous && r0.size() > 2 && build_parts(a, r0, dinv_h, s)) return finish();
     walk = false;
     const int global_depth = lower_schedule(a).n_levels();
     std::vector<int> rank_in_comp(n), comp_size;
@@ -782,6 +783,189 @@ bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std
     return true;
 }
 
+// Two label blocks walked concurrently: CTA 0 walks block 0 and pushes the
+// values block 1 needs into CTA 1's import slots (a ring of kImportRing slots,
+// in export order); CTA 1 walks block 1, waiting at each level for the block-0
+// levels its imports come from.  Back-pressure: before a block-0 level
+// overwrites import slots, CTA 0 waits for the block-1 levels that last read
+// them.  A host simulation of the two schedules rules out a deadlock.
+bool GsPlan::build_pipe(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
+                        cudaStream_t s) {
+    const int lo1 = r0[1], n0 = r0[1], n1 = n - r0[1];
+    auto debug = std::getenv("SDG_DEBUG");
+    auto reject = [&](const char* why) {
+        if (debug) std::fprintf(stderr, "[sdg gs plan] n=%d: no 2-CTA pipe (%s)\n", n, why);
+        return false;
+    };
+    // block matrices: A00 (local), A11 (local), L10 (block-1 rows x block-0 columns, lower by construction)
+    HostCsr a0(n0, n0), a1(n1, n1), l10(n1, n0);
+    std::vector<int> nlow0(n0, 0), nlow1(n1, 0);
+    int maxk0 = 0, maxk1 = 0;
+    for (int i = 0; i < n; ++i) {
+        for (int e = a.rp[i]; e < a.rp[i + 1]; ++e) {
+            const int j = a.ci[e];
+            if (i < lo1) {
+                if (j < lo1) {
+                    a0.ci.push_back(j);
+                    a0.v.push_back(a.v[e]);
+                    if (j < i) ++nlow0[i];
+                }
+            } else if (j >= lo1) {
+                a1.ci.push_back(j - lo1);
+                a1.v.push_back(a.v[e]);
+                if (j < i) ++nlow1[i - lo1];
+            } else {
+                l10.ci.push_back(j);
+                l10.v.push_back(a.v[e]);
+                ++nlow1[i - lo1];
+            }
+        }
+        if (i < lo1) {
+            a0.rp[i + 1] = static_cast<int>(a0.ci.size());
+            maxk0 = std::max(maxk0, nlow0[i]);
+        } else {
+            a1.rp[i - lo1 + 1] = static_cast<int>(a1.ci.size());
+            l10.rp[i - lo1 + 1] = static_cast<int>(l10.ci.size());
+            maxk1 = std::max(maxk1, nlow1[i - lo1]);
+        }
+    }
+    std::vector<double> d0(dinv_h.begin(), dinv_h.begin() + lo1), d1(dinv_h.begin() + lo1, dinv_h.end());
+
+    // pass 1: each block's own shape -> one common kernel shape and record width
+    Link s0, s1;
+    s0.role = 1;
+    s1.role = 2;
+    s1.ext = &l10;
+    std::vector<int> zero_slot_of(n0, 0), zero_plv(n0, 0);
+    s1.ext_slot = &zero_slot_of;
+    s1.ext_plv = &zero_plv;
+    s1.import_slots = 1;
+    {
+        GsPlan t0, t1;
+        if (!t0.build_walk(a0, d0, nlow0, maxk0, s, &s0)) return reject("block 0 does not fit a walk");
+        if (!t1.build_walk(a1, d1, nlow1, maxk1, s, &s1)) return reject("block 1 does not fit a walk");
+    }
+    Link f0, f1;
+    f0.force_w = f1.force_w = std::max(s0.shape[0], s1.shape[0]);
+    f0.force_r2 = f1.force_r2 = std::max(s0.shape[1], s1.shape[1]);
+    f0.force_r8 = f1.force_r8 = std::max(s0.shape[2], s1.shape[2]);
+    f0.force_kw = f1.force_kw = std::max(s0.shape[3], s1.shape[3]);
+    // pass 2: block 0's levels -> exports in level order -> import slots (a ring)
+    std::vector<int> plv0, plv1;
+    f0.role = 1;
+    f0.plv_out = &plv0;
+    {
+        GsPlan t0;
+        if (!t0.build_walk(a0, d0, nlow0, maxk0, s, &f0)) return reject("block 0 with the common shape");
+    }
+    std::vector<char> needed(n0, 0);
+    for (int j : l10.ci) needed[j] = 1;
+    std::vector<int> exported;
+    for (int j = 0; j < n0; ++j)
+        if (needed[j]) exported.push_back(j);
+    std::stable_sort(exported.begin(), exported.end(), [&](int x, int y) { return plv0[x] < plv0[y]; });
+    const int nexp = static_cast<int>(exported.size());
+    int per_level = 1, nlev0 = 0;
+    for (int j = 0; j < n0; ++j) nlev0 = std::max(nlev0, plv0[j] + 1);
+    {
+        std::vector<int> cnt(nlev0 + 1, 0);
+        for (int j : exported) per_level = std::max(per_level, ++cnt[plv0[j]]);
+    }
+    int ring_slots = 1024;
+    while (ring_slots < 24 * per_level && ring_slots < 8192) ring_slots <<= 1;
+    std::vector<int> slot(n0, -1);
+    for (int k = 0; k < nexp; ++k) slot[exported[k]] = k % ring_slots;
+    // block 1 with its imports
+    f1.role = 2;
+    f1.ext = &l10;
+    f1.ext_slot = &slot;
+    f1.ext_plv = &plv0;
+    f1.import_slots = ring_slots;
+    f1.plv_out = &plv1;
+    std::vector<int> peer_bytes(nlev0, 0);
+    for (int j : exported) peer_bytes[plv0[j]] += 8;
+    f1.peer_bytes = &peer_bytes;
+    auto q1 = std::make_unique<GsPlan>();
+    if (!q1->build_walk(a1, d1, nlow1, maxk1, s, &f1)) return reject("block 1 with its imports");
+    // back-pressure: block-0 level X may overwrite export k - ring_slots once
+    // the block-1 levels reading it are done
+    std::vector<int> last_read(n0, -1);
+    for (int i = 0; i < n1; ++i)
+        for (int e = l10.rp[i]; e < l10.rp[i + 1]; ++e)
+            last_read[l10.ci[e]] = std::max(last_read[l10.ci[e]], plv1[i]);
+    std::vector<int> need(nlev0, 0);
+    for (int k = ring_slots; k < nexp; ++k) {
+        const int x = plv0[exported[k]];
+        need[x] = std::max(need[x], last_read[exported[k - ring_slots]] + 1);
+    }
+    // no deadlock: both schedules advance whenever allowed and finish
+    {
+        std::vector<int> sync1(q1->n_levels, 0);
+        for (int i = 0; i < n1; ++i)
+            for (int e = l10.rp[i]; e < l10.rp[i + 1]; ++e)
+                sync1[plv1[i]] = std::max(sync1[plv1[i]], plv0[l10.ci[e]] + 1);
+        int d0l = 0, d1l = 0;
+        while (d0l < nlev0 || d1l < q1->n_levels) {
+            bool moved = false;
+            while (d0l < nlev0 && need[d0l] <= d1l) ++d0l, moved = true;
+            while (d1l < q1->n_levels && sync1[d1l] <= d0l) ++d1l, moved = true;
+            if (!moved) return reject("the import ring would deadlock");
+        }
+    }
+    // pass 3: block 0 with its exports and back-pressure levels
+    std::vector<int> plv0b;
+    f0.plv_out = &plv0b;
+    f0.export_slot = &slot;
+    f0.export_need = &need;
+    f0.export_base = q1->walk_import_base;
+    auto q0 = std::make_unique<GsPlan>();
+    if (!q0->build_walk(a0, d0, nlow0, maxk0, s, &f0)) return reject("block 0 with its exports");
+    if (plv0b != plv0) return reject("block 0 changed its level split");
+    if (nlev0 > 4096) return reject("too many block-0 levels for the mbarriers");
+    const int w = f0.force_w, r2 = f0.force_r2, r8 = f0.force_r8, kw = f0.force_kw;
+    if (r2 > 2 || r8 > 2) return reject("no pipe instantiation for the shape");
+    // one record buffer (as build_parts), global bidx for the prep kernels
+    std::vector<std::unique_ptr<GsPlan>> ps;
+    ps.push_back(std::move(q0));
+    ps.push_back(std::move(q1));
+    size_t total = 0;
+    std::vector<size_t> off(2);
+    for (int k = 0; k < 2; ++k) {
+        off[k] = total;
+        total += ps[k]->packed.size();
+    }
+    packed.resize(total);
+    std::vector<int> bidx_h(n);
+    for (int k = 0; k < 2; ++k) {
+        GsPlan& p = *ps[k];
+        SDG_CUDA(cudaMemcpyAsync(packed.get() + off[k], p.packed.get(), p.packed.size() * 8,
+                                 cudaMemcpyDeviceToDevice, s));
+        std::vector<int> lb(p.n);
+        SDG_CUDA(cudaMemcpyAsync(lb.data(), p.bidx.get(), p.n * sizeof(int), cudaMemcpyDeviceToHost, s));
+        SDG_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < p.n; ++i) bidx_h[r0[k] + i] = static_cast<int>(off[k]) + lb[i];
+        p.part_doubles = p.packed.size();
+        p.packed.release();
+        p.bidx.release();
+        p.packed_ptr = packed.get() + off[k];
+    }
+    bidx.upload(bidx_h, s);
+    parts = std::move(ps);
+    part_r0 = r0;
+    couple.clear();
+    pipe = true;
+    walk = false;
+    usable = true;
+    bands = 2;
+    n_levels = std::max(parts[0]->n_levels, parts[1]->n_levels);
+    if (debug)
+        std::fprintf(stderr,
+                     "[sdg gs plan] n=%d: 2-CTA pipe, blocks %d + %d rows, %d + %d levels, %d exports, import ring %d, "
+                     "shape warps=%d rows/thread=%d+%d wide=%d\n",
+                     n, n0, n1, parts[0]->n_levels, parts[1]->n_levels, nexp, ring_slots, w, r2, r8, kw);
+    return true;
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 
@@ -813,6 +997,11 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
 }
 
 void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
+    if (g.pipe) {
+        ProfScope ps_(c, PF_GS, g.packed_bytes() + 8.0 * g.n);
+        launch_gs_pipe(c, g, z_new);
+        return;
+    }
     if (!g.parts.empty()) {
         for (size_t k = 0; k < g.parts.size(); ++k) {
             if (k > 0) {

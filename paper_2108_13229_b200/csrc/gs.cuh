@@ -80,6 +80,11 @@ struct GsPlan {
     std::vector<std::unique_ptr<GsPlan>> parts;
     std::vector<int> part_r0;
     std::vector<DevCsr> couple;
+    bool pipe = false;   // two parts walked concurrently on a 2-CTA cluster (no coupling step)
+    int walk_role = 0;   // WalkArgs::role of a pipe part
+    int walk_import_base = 0;  // first import slot of a walk (pipe role 2)
+    int walk_n_peer = 0, walk_pbar_bytes = 0;
+    DevBuf<int> walk_peer_bytes;  // pipe role 2: bytes the peer pushes at each of its levels
     const double* packed_ptr = nullptr;  // records of a part inside its parent's buffer
     size_t part_doubles = 0;             // size of a part's records
 
@@ -92,11 +97,29 @@ struct GsPlan {
     }
     const double* records() const { return packed_ptr ? packed_ptr : packed.get(); }
 
+    // optional inputs / outputs of build_walk for the parts of a pipe
+    struct Link {
+        int force_w = 0, force_r2 = 0, force_r8 = 0, force_kw = 0;  // shape (0: the cost model's)
+        int role = 0;
+        const std::vector<int>* export_slot = nullptr;  // role 1: per row, import slot in the peer (-1 none)
+        const std::vector<int>* export_need = nullptr;  // role 1: per pseudo-level, peer levels done first
+        int export_base = 0;                            // role 1: the peer's first import slot
+        const HostCsr* ext = nullptr;                   // role 2: rows x peer rows, lower entries to the peer
+        const std::vector<int>* ext_slot = nullptr;     // role 2: peer row -> import slot
+        const std::vector<int>* ext_plv = nullptr;      // role 2: peer row -> its pseudo-level
+        const std::vector<int>* peer_bytes = nullptr;   // role 2: bytes pushed at each peer level
+        int import_slots = 0;
+        std::vector<int>* plv_out = nullptr;  // pseudo-level of every row
+        int shape[4] = {0, 0, 0, 0};          // out: chosen W, R2, R8, wide width
+    };
+
 private:
     bool build_parts(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
                      cudaStream_t s);
-    bool build_walk(const HostCsr& a, const std::vector<double>& dinv_h, const std::vector<int>& nlow, int max_k,
+    bool build_pipe(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
                     cudaStream_t s);
+    bool build_walk(const HostCsr& a, const std::vector<double>& dinv_h, const std::vector<int>& nlow, int max_k,
+                    cudaStream_t s, Link* link = nullptr);
 };
 
 // packed[bidx[i]] = r[i] * dinv[i]                      (pre-smoother, z_old = 0)
@@ -108,6 +131,8 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
 void launch_gs_lower(Context& c, const GsPlan& g, double* z_new);
 // single-CTA variant (plans with walk == true; gs_walk.cu)
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new);
+// the two parts of a pipe on a 2-CTA cluster (gs_walk.cu)
+void launch_gs_pipe(Context& c, const GsPlan& g, double* z_new);
 // fused residual + restriction, one warp per aggregate (bit-identical to
 // precond.cpp:241-244); optionally also seeds the next level's packed b
 // (rc * dinv) for its pre-smoother.

@@ -103,6 +103,26 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     return v;
 }
 
+__device__ __forceinline__ int ld_acquire_cluster(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cluster.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_cluster(unsigned cluster_addr, int v) {
+    asm volatile("st.release.cluster.shared::cluster.s32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_cluster(unsigned cluster_addr, int v) {
+    asm volatile("st.relaxed.cluster.shared::cluster.s32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
 __device__ __forceinline__ void st_volatile(int* p, int v) {
     asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
 }
@@ -118,12 +138,28 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
 }
 
 struct WalkArgs {
-    const int4* meta_g;   // per level (+2 sentinels) {K2 stage off, K8 stage off | chunk-start << 18,
-                          //   K2 pos | n2 << 20, K8 pos | n8 << 20}
+    const int4* meta_g;   // per level (+2 sentinels) {K2 stage off | peer level << 18, K8 stage off | chunk-start
+                          //   << 18, K2 pos | n2 << 20, K8 pos | n8 << 20}
     const int4* chunk_g;  // per chunk {global off / 16, bytes, stage off, may issue once this level is done}
     const unsigned char* packed;
     int n_levels, n_chunks, ring, meta_bytes, chunk_bytes, zbytes;
     double* z_new;
+    // 0: one CTA.  In a 2-CTA pipe (two label blocks walked concurrently on a
+    // cluster): 1 = the earlier block, whose small rows push the values the
+    // other block needs into the peer's import slots with st.async, each
+    // completing the transaction count of the peer's mbarrier for that level;
+    // 2 = the later block.  The peer-level field of a level is the peer's
+    // progress it needs first (role 2: the producer levels its imports come
+    // from; role 1: the consumer levels that last read the import slots it is
+    // about to overwrite).
+    int role;
+    int n_peer;               // role 2: levels of the peer (one single-use mbarrier each)
+    int pbar_bytes;           // role 2: shared bytes of those mbarriers
+    const int* peer_bytes_g;  // role 2: bytes the peer pushes at each of its levels
+};
+
+struct WalkPair {
+    WalkArgs a[2];  // indexed by the CTA's rank in the cluster (a[0] only without a cluster)
 };
 
 // 32-bit shared-memory accesses through explicit addresses (kept in
@@ -166,7 +202,7 @@ __device__ __forceinline__ void stsd(unsigned a, double v) {
 template <int R2, int R8, int KW>
 struct WalkRaw {
     int4 h2[R2 > 0 ? R2 : 1], h8[R8 > 0 ? R8 : 1];       // {b lo, b hi, rowid, pin}
-    int2 s2[R2 > 0 ? R2 : 1];                            // sources of small rows
+    int4 s2[R2 > 0 ? R2 : 1];                            // small rows: {source, source, export slot, -}
     int4 s8[R8 > 0 ? R8 : 1][KW == 8 ? 2 : (KW + 7) / 8];  // sources of wide rows (32- or 16-bit)
     unsigned q2[R2 > 0 ? R2 : 1], q8[R8 > 0 ? R8 : 1];   // record addresses
     int4 m;                                              // the level's meta
@@ -179,6 +215,8 @@ struct WalkRows {
     unsigned wa2[R2 > 0 ? R2 : 1], pa2[R2 > 0 ? R2 : 1], va2[R2 > 0 ? R2 : 1];
     unsigned wa8[R8 > 0 ? R8 : 1], pa8[R8 > 0 ? R8 : 1], va8[R8 > 0 ? R8 : 1];
     int rid2[R2 > 0 ? R2 : 1], rid8[R8 > 0 ? R8 : 1];
+    unsigned ex2[R2 > 0 ? R2 : 1];  // shared::cluster address of the export slot in the peer (0: none)
+    int sync;                       // peer progress this level needs (pipe roles)
 };
 
 // The level loop of one consumer warp (see the file comment).  Three-stage
@@ -186,9 +224,11 @@ struct WalkRows {
 // stores, global z), turn level L+1's raw record words into addresses, load
 // level L+2's raw records; then the level hand-off.  The critical path per
 // level is gathers -> FMAs -> ring store -> hand-off.
-template <int R2, int R8, int KW>
+template <int R2, int R8, int KW, bool PIPE>
 __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* meta, const unsigned char* stage,
-                                              const unsigned char* nullrec, double* zr, int* flags) {
+                                              const unsigned char* nullrec, double* zr, int* flags,
+                                              unsigned peer_zr, unsigned peer_flag, unsigned peer_pbar,
+                                              uint64_t* pbars_l) {
     const int mask = a.ring - 1, dummy = a.ring + 1;
     const int nw = (blockDim.x >> 5) - 1;
     const int t0 = threadIdx.x - 32;  // (warp - 1) * 32 + lane
@@ -198,6 +238,22 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     double* const z_new = a.z_new;
     int* progress = flags;
     const int* landed = flags + 1;
+    const int role = PIPE ? a.role : 0;  // compile-time 0 outside pipes (no cost on the plain walk)
+    // peer progress: role 1 reads flags[2] (the peer's level count, stored
+    // remotely), role 2 flags[3] (peer levels whose pushes have all landed,
+    // published by its own producer thread from the mbarriers)
+    int peer_seen = 0;
+    auto wait_peer = [&](int need) {
+        if (need > peer_seen) {
+            if (role == 1) {
+                while ((peer_seen = ld_volatile(flags + 2)) < need) {
+                }
+            } else {
+                for (int l = peer_seen; l < need; ++l) mbar_wait(pbars_l + l, 0);
+                peer_seen = need;
+            }
+        }
+    };
     using Raw = WalkRaw<R2, R8, KW>;
     using Rows = WalkRows<R2, R8, KW>;
     constexpr int WB = wide_bytes(KW);
@@ -212,10 +268,10 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
 #pragma unroll
         for (int r = 0; r < R2; ++r) {
             const int u = r * stride + t0;
-            const unsigned q = u < (m.z >> 20) ? stage_s + m.x + u * kK2Bytes : null_s;
+            const unsigned q = u < (m.z >> 20) ? stage_s + (m.x & 0x3ffff) + u * kK2Bytes : null_s;
             w.q2[r] = q;
             w.h2[r] = lds4(q);
-            w.s2[r] = lds2(q + 32);
+            w.s2[r] = lds4(q + 32);
         }
 #pragma unroll
         for (int r = 0; r < R8; ++r) {
@@ -230,6 +286,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     };
     auto unpack = [&](Rows& x, const Raw& w) {
         const int4 m = w.m;
+        x.sync = static_cast<unsigned>(m.x) >> 18;
 #pragma unroll
         for (int r = 0; r < R2; ++r) {
             const int u = r * stride + t0;
@@ -239,6 +296,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
             x.pa2[r] = zr_s + 8u * w.h2[r].w;
             x.s2[r][0] = zr_s + 8u * w.s2[r].x;
             x.s2[r][1] = zr_s + 8u * w.s2[r].y;
+            x.ex2[r] = PIPE && w.s2[r].z >= 0 ? peer_zr + 8u * w.s2[r].z : 0u;
             x.va2[r] = w.q2[r] + 16;
             x.wa2[r] = zr_s + 8u * (ok ? (((m.z & 0xfffff) + u) & mask) : dummy);
         }
@@ -273,6 +331,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     // solve level L (rows in x), unpack level L+1 (raw w) into y, load level L+2 into w
     auto step = [&](int L, const Rows& x, Rows& y, Raw& w) {
         WALK_CLK(L, 0);
+        if (role == 2) wait_peer(x.sync);  // the imported values of this level have arrived
         double z2[R2 > 0 ? R2 : 1][2], v2[R2 > 0 ? R2 : 1][2];
         double z8[R8 > 0 ? R8 : 1][KW], v8[R8 > 0 ? R8 : 1][KW];
 #pragma unroll
@@ -295,11 +354,13 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
             }
         }
         const int4 m2 = meta[L + 2];
+        if (role == 1) wait_peer(x.sync);  // the import slots about to be overwritten have been read
 #pragma unroll
         for (int r = 0; r < R2; ++r) {
             const double acc = fma(v2[r][1], z2[r][1], fma(v2[r][0], z2[r][0], x.b2[r]));
             stsd(x.wa2[r], acc);
             stsd(x.pa2[r], acc);
+            if (PIPE && x.ex2[r]) st_async_f64(x.ex2[r], acc, peer_pbar + 8u * L);
             if (!(SDG_WALK_EXP & 2) && x.rid2[r] >= 0) z_new[x.rid2[r]] = acc;
         }
 #pragma unroll
@@ -331,7 +392,10 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
             __syncwarp();
         else
             asm volatile("bar.sync 1, %0;" ::"r"(stride) : "memory");
-        if (!(SDG_WALK_EXP & 1) && threadIdx.x == 32) st_volatile(progress, L + 1);
+        if (threadIdx.x == 32) {
+            st_volatile(progress, L + 1);
+            if (role == 2) st_relaxed_cluster(peer_flag, L + 1);  // back-pressure for the peer
+        }
     };
     Rows x, y;
     Raw w;
@@ -349,58 +413,24 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     }
 }
 
-template <int R2, int R8, int KW>
-__global__ void __launch_bounds__(max_threads(R2, R8, KW), 1) k_gs_walk(WalkArgs a) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
-    int* flags = reinterpret_cast<int*>(sm + kBars * 8);  // {levels done, chunks landed}
-    unsigned char* nullrec = sm + kBars * 8 + 16;
-    int4* meta = reinterpret_cast<int4*>(nullrec + kNullBytes);
-    int4* ctab = reinterpret_cast<int4*>(reinterpret_cast<unsigned char*>(meta) + a.meta_bytes);
-    double* zr = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ctab) + a.chunk_bytes);
-    unsigned char* stage = reinterpret_cast<unsigned char*>(zr) + a.zbytes;
-    const int tid = threadIdx.x;
-    const int nl = a.n_levels, nc = a.n_chunks;
-    const int zero_slot = a.ring, dummy = a.ring + 1;
-
-    for (int l = tid; l <= nl + 1; l += blockDim.x) meta[l] = a.meta_g[l];
-    for (int c = tid; c < nc; c += blockDim.x) ctab[c] = a.chunk_g[c];
-    if (tid < kBars) mbar_init(&bars[tid], 1);
-    if (tid < 2) {  // null records: b = 0, v = 0, sources = zero slot, stores to the dummy slot
-        int* nr = reinterpret_cast<int*>(nullrec + 128 * tid);
-        for (int k = 0; k < (tid ? wide_bytes(KW) : 48) / 4; ++k) nr[k] = 0;
-        nr[2] = -1;     // rowid
-        nr[3] = dummy;  // pin
-        if (tid == 0) {
-            nr[8] = nr[9] = zero_slot;
-        } else if (KW == 8) {
-            for (int k = 0; k < 8; ++k) nr[20 + k] = zero_slot;
-        } else {
-            for (int k = 0; k < KW / 2; ++k) nr[wide_src_off(KW) / 4 + k] = zero_slot | (zero_slot << 16);
-        }
-    }
-    if (tid == 0) {
-        zr[zero_slot] = 0.0;
-        flags[0] = 0;
-        flags[1] = 0;
-    }
-    fence_mbar_init();
-    __syncthreads();
-    pdl_trigger();  // the next kernel may launch (it waits for this grid itself)
-
-    if (tid >= 32) {
-        walk_consumer<R2, R8, KW>(a, meta, stage, nullrec, zr, flags);
-        return;
-    }
-    if (tid != 0) return;
+// TMA producer (thread 0): issue chunk copies once the consumers' progress
+// frees their ring space, publish each chunk once it has landed
+__device__ __forceinline__ void walk_producer(const WalkArgs& a, uint64_t* bars, int* flags, const int4* ctab,
+                                              unsigned char* stage, uint64_t* pbars) {
+    const int nc = a.n_chunks, np = 0;  // consumers wait on the peer mbarriers themselves
+    int pl = 0;  // peer levels whose pushes have landed
     // the records' b values come from the previous kernel (prep / restriction):
     // the setup above overlapped it, the copies wait for it.  Consumers touch
     // global memory only after `landed` shows copies issued after this wait.
     pdl_wait();
-    // producer: issue chunk copies once the consumers' progress frees their
-    // ring space, publish each chunk once it has landed
     int ci = 0, cw = 0;
-    while (cw < nc) {
+    while (cw < nc || pl < np) {
+        if (pl < np && mbar_test(&pbars[pl], 0)) {
+            int q = pl + 1;
+            while (q < np && mbar_test(&pbars[q], 0)) ++q;
+            pl = q;
+            asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_addr(&flags[3])), "r"(pl) : "memory");
+        }
         const int done = ld_volatile(&flags[0]) - 1;  // last completed level
         while (ci < nc && ci < cw + kBars && ctab[ci].w <= done) {
             const int4 cd = ctab[ci];
@@ -412,19 +442,97 @@ __global__ void __launch_bounds__(max_threads(R2, R8, KW), 1) k_gs_walk(WalkArgs
         if (cw < ci && mbar_test(&bars[cw % kBars], static_cast<unsigned>(cw / kBars) & 1u)) {
             ++cw;
             asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_addr(&flags[1])), "r"(cw) : "memory");
-        } else {
+        } else if (pl >= np) {
             __nanosleep(20);
         }
     }
 }
 
-using WalkKernel = void (*)(WalkArgs);
+template <int R2, int R8, int KW, bool PIPE>
+__global__ void __launch_bounds__(max_threads(R2, R8, KW), 1) k_gs_walk(WalkPair pair) {
+    const unsigned rank = PIPE ? cluster_ctarank() : 0u;
+    const WalkArgs a = rank ? pair.a[1] : pair.a[0];  // a copy: no dynamically indexed parameter loads
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+    // {levels done, chunks landed, peer levels done (role 1), peer levels landed (role 2)}
+    int* flags = reinterpret_cast<int*>(sm + kBars * 8);
+    unsigned char* nullrec = sm + kBars * 8 + 16;
+    int4* meta = reinterpret_cast<int4*>(nullrec + kNullBytes);
+    int4* ctab = reinterpret_cast<int4*>(reinterpret_cast<unsigned char*>(meta) + a.meta_bytes);
+    uint64_t* pbars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ctab) + a.chunk_bytes);
+    double* zr = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(pbars) + a.pbar_bytes);
+    unsigned char* stage = reinterpret_cast<unsigned char*>(zr) + a.zbytes;
+    const int tid = threadIdx.x;
+    const int nl = a.n_levels, nc = a.n_chunks;
+    const int zero_slot = a.ring, dummy = a.ring + 1;
+
+    for (int l = tid; l <= nl + 1; l += blockDim.x) meta[l] = a.meta_g[l];
+    for (int c = tid; c < nc; c += blockDim.x) ctab[c] = a.chunk_g[c];
+    if (tid < kBars) mbar_init(&bars[tid], 1);
+    if (PIPE && a.role == 2)
+        for (int l = tid; l < a.n_peer; l += blockDim.x) {
+            mbar_init(&pbars[l], 1);
+            mbar_expect_tx(&pbars[l], static_cast<unsigned>(a.peer_bytes_g[l]));
+        }
+    if (tid < 2) {  // null records: b = 0, v = 0, sources = zero slot, stores to the dummy slot
+        int* nr = reinterpret_cast<int*>(nullrec + 128 * tid);
+        for (int k = 0; k < (tid ? wide_bytes(KW) : 48) / 4; ++k) nr[k] = 0;
+        nr[2] = -1;     // rowid
+        nr[3] = dummy;  // pin
+        if (tid == 0) {
+            nr[8] = nr[9] = zero_slot;
+            nr[10] = -1;  // no export
+        } else if (KW == 8) {
+            for (int k = 0; k < 8; ++k) nr[20 + k] = zero_slot;
+        } else {
+            for (int k = 0; k < KW / 2; ++k) nr[wide_src_off(KW) / 4 + k] = zero_slot | (zero_slot << 16);
+        }
+    }
+    if (tid == 0) {
+        zr[zero_slot] = 0.0;
+        flags[0] = 0;
+        flags[1] = 0;
+        flags[2] = 0;
+        flags[3] = 0;
+    }
+    fence_mbar_init();
+    if (PIPE)
+        asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;" ::: "memory");
+    else
+        __syncthreads();
+    pdl_trigger();  // the next kernel may launch (it waits for this grid itself)
+
+    if (tid >= 32) {
+        // the peer CTA's mbarriers, z slots and progress word (in its own layout)
+        unsigned peer_zr = 0, peer_flag = 0, peer_pbar = 0;
+        if (PIPE) {
+            const WalkArgs& pa = rank ? pair.a[0] : pair.a[1];
+            const unsigned char* pb = sm + kBars * 8 + 16 + kNullBytes + pa.meta_bytes + pa.chunk_bytes;
+            peer_pbar = cluster_addr(pb, rank ^ 1u);
+            peer_zr = cluster_addr(pb + pa.pbar_bytes, rank ^ 1u);
+            peer_flag = cluster_addr(flags + 2, rank ^ 1u);
+        }
+        walk_consumer<R2, R8, KW, PIPE>(a, meta, stage, nullrec, zr, flags, peer_zr, peer_flag, peer_pbar, pbars);
+    } else if (tid == 0) {
+        walk_producer(a, bars, flags, ctab, stage, pbars);
+    }
+    // no CTA of a pipe leaves while its peer may still store into it
+    if (PIPE) asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;" ::: "memory");
+}
+
+using WalkKernel = void (*)(WalkPair);
 
 constexpr int kw_of(int i) { return i == 0 ? 6 : i == 1 ? 8 : 16; }
 
 template <int I>
 constexpr WalkKernel kernel_at() {
-    return &k_gs_walk<I / (3 * (kMaxR8 + 1)) + 1, (I / 3) % (kMaxR8 + 1), kw_of(I % 3)>;
+    return &k_gs_walk<I / (3 * (kMaxR8 + 1)) + 1, (I / 3) % (kMaxR8 + 1), kw_of(I % 3), false>;
+}
+
+// 2-CTA pipe instantiations: R2 <= 2, R8 <= 2
+template <int I>
+constexpr WalkKernel pipe_kernel_at() {
+    return &k_gs_walk<I / 9 + 1, (I / 3) % 3, kw_of(I % 3), true>;
 }
 
 // all instantiations, indexed [R2 - 1][R8][wide width 6 / 8 / 16]
@@ -436,9 +544,23 @@ constexpr auto make_table(std::integer_sequence<int, I...>) {
     return T{{kernel_at<I>()...}};
 }
 
-WalkKernel walk_kernel(int r2, int r8, int kw) {
+template <int... I>
+constexpr auto make_pipe_table(std::integer_sequence<int, I...>) {
+    struct T {
+        WalkKernel k[sizeof...(I)];
+    };
+    return T{{pipe_kernel_at<I>()...}};
+}
+
+WalkKernel walk_kernel(int r2, int r8, int kw, bool pipe = false) {
+    const int kwi = kw == 6 ? 0 : kw == 8 ? 1 : 2;
+    if (pipe) {
+        static const auto ptable = make_pipe_table(std::make_integer_sequence<int, 2 * 3 * 3>{});
+        if (r2 < 1 || r2 > 2 || r8 > 2) fail(SDG_EINVAL, "gs pipe: no instantiation for this shape");
+        return ptable.k[((r2 - 1) * 3 + r8) * 3 + kwi];
+    }
     static const auto table = make_table(std::make_integer_sequence<int, kMaxR2 * (kMaxR8 + 1) * 3>{});
-    return table.k[((r2 - 1) * (kMaxR8 + 1) + r8) * 3 + (kw == 6 ? 0 : kw == 8 ? 1 : 2)];
+    return table.k[((r2 - 1) * (kMaxR8 + 1) + r8) * 3 + kwi];
 }
 
 }  // namespace
@@ -447,7 +569,7 @@ WalkKernel walk_kernel(int r2, int r8, int kw) {
 // lower entries, a level too large for the staging ring); the caller then
 // builds the banded plan.
 bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, const std::vector<int>& nlow,
-                        int max_k, cudaStream_t s) {
+                        int max_k, cudaStream_t s, Link* link) {
     auto reject = [&](const char* why) {
         if (std::getenv("SDG_DEBUG")) std::fprintf(stderr, "[sdg gs walk] n=%d: not used (%s)\n", a.n_rows, why);
         return false;
@@ -467,7 +589,8 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     std::vector<int> c2(nlv, 0), c8(nlv, 0);
     for (int i = 0; i < n; ++i) ++(nlow[i] <= 2 ? c2 : c8)[lev[i]];
     // wide rows: the narrowest record that holds every row (see wide_bytes)
-    const int kw = max_k <= 6 ? 6 : max_k <= 8 ? 8 : 16;
+    const int kw = link && link->force_kw ? link->force_kw : max_k <= 6 ? 6 : max_k <= 8 ? 8 : 16;
+    if (max_k > kw) return reject("forced record width too small");
     const int WB = wide_bytes(kw);
 
     // (W, R2, R8) from a cost model in cycles per pseudo-level, fitted to
@@ -511,6 +634,15 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
                 best_r8 = r8;
             }
         }
+    }
+    if (link && link->force_w) {
+        const int w = link->force_w, r2 = link->force_r2, r8 = link->force_r8;
+        bool ok = 32 + 32 * w <= max_threads(r2, r8, kw) && shape_ok(r2, r8, kw);
+        for (int q = 0; q < nlv; ++q) ok = ok && (r8 > 0 || c8[q] == 0);
+        if (!ok) return reject("forced shape does not fit");
+        best_w = w;
+        best_r2 = r2;
+        best_r8 = r8;
     }
     if (best_w == 0) return reject("no (warps, rows per thread) shape fits");
     const int cap2 = 32 * best_w * best_r2, cap8 = 32 * best_w * best_r8;
@@ -597,6 +729,7 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     const int budget = std::min(kSmemCap, optin - 1024);
     const int meta_bytes = pad16(static_cast<int64_t>(nl + 2) * 16);
     const int chunk_bytes = pad16(static_cast<int64_t>(nc) * 16);
+    const int pbar_bytes = link && link->peer_bytes ? pad16(static_cast<int64_t>(link->peer_bytes->size()) * 8) : 0;
     const int min_stage = 3 * max_chunk;
     ring = 64;
     while (ring < max_dist && ring < 8192) ring <<= 1;
@@ -613,15 +746,16 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
                     if (j < i && lptr[q + 1] - pos[j] > ring && pin_of[j] < 0) pin_of[j] = npin++;
                 }
             }
-        zbytes = pad16(static_cast<int64_t>(ring + 2 + npin) * 8);
-        fixed = kBars * 8 + 16 + kNullBytes + meta_bytes + chunk_bytes + zbytes;
+        zbytes = pad16(static_cast<int64_t>(ring + 2 + npin + (link ? link->import_slots : 0)) * 8);
+        fixed = kBars * 8 + 16 + kNullBytes + meta_bytes + chunk_bytes + pbar_bytes + zbytes;
         R = (budget - fixed) / 16 * 16;
         if (R >= min_stage) break;
         if (ring <= 64 || ring / 2 < 2 * max_rows) return reject("shared memory: ring + pinned values + staging");
         ring >>= 1;
     }
-    const int zero_slot = ring, dummy_slot = ring + 1, pin_base = ring + 2;
-    if (kw != 8 && pin_base + npin >= 65536) return reject("too many shared slots for 16-bit sources");
+    const int zero_slot = ring, dummy_slot = ring + 1, pin_base = ring + 2, import_base = pin_base + npin;
+    const int nslots = import_base + (link ? link->import_slots : 0);
+    if (kw != 8 && nslots >= 65536) return reject("too many shared slots for 16-bit sources");
 
     // staging ring placement and issue points of the chunks
     std::vector<int> roff(nc), after(nc);
@@ -648,6 +782,9 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     std::vector<double> pk(static_cast<size_t>(off / 8 + 2), 0.0);
     unsigned char* base = reinterpret_cast<unsigned char*>(pk.data());
     std::vector<int> bidx_h(n);
+    std::vector<int> sync_of(nl, 0);  // peer progress a level needs (pipe roles)
+    if (link && link->export_need)
+        for (int q = 0; q < nl; ++q) sync_of[q] = (*link->export_need)[q];
     std::vector<int4> meta_h(nl + 2), ctab_h(nc);
     lower_entries = 0;
     global_refs = 0;
@@ -666,6 +803,13 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
             bidx_h[i] = static_cast<int>((rec - base) / 8);
             reci[2] = i;
             reci[3] = pin_of[i] >= 0 ? pin_base + pin_of[i] : dummy_slot;
+            const int exp = link && link->export_slot && (*link->export_slot)[i] >= 0
+                                ? link->export_base + (*link->export_slot)[i]
+                                : -1;
+            if (k2)
+                reci[10] = exp;
+            else if (exp >= 0)
+                return reject("a wide row exports to the peer");
             const int cap = k2 ? 2 : kw;
             double* val = recd + 2;
             int* src = reci + (k2 ? 8 : 20);
@@ -684,6 +828,21 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
                 ++m;
                 ++lower_entries;
             }
+            if (link && link->ext) {  // lower entries to the peer block: its values arrive in import slots
+                const HostCsr& x = *link->ext;
+                for (int k = x.rp[i]; k < x.rp[i + 1]; ++k) {
+                    const int j = x.ci[k];
+                    val[m] = -(x.v[k] * dinv_h[i]);
+                    const int slot = import_base + (*link->ext_slot)[j];
+                    if (narrow_src)
+                        src16[m] = static_cast<uint16_t>(slot);
+                    else
+                        src[m] = slot;
+                    ++m;
+                    ++lower_entries;
+                    sync_of[q] = std::max(sync_of[q], (*link->ext_plv)[j] + 1);
+                }
+            }
             for (; m < cap; ++m) {
                 val[m] = 0.0;
                 if (narrow_src)
@@ -694,12 +853,29 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
         }
         const int starts = cfirst[chunk_of[q]] == q ? chunk_of[q] + 1 : 0;  // chunk id + 1 if q starts a chunk
         const int o2 = roff[chunk_of[q]] + in_chunk[q], o8 = o2 + n2[q] * kK2Bytes;
-        meta_h[q] = make_int4(o2, o8 | (starts << 18), lptr[q] | (n2[q] << 20), (lptr[q] + n2[q]) | (n8[q] << 20));
+        if (sync_of[q] >= (1 << 14)) return reject("peer level out of the meta packing");
+        meta_h[q] = make_int4(o2 | (sync_of[q] << 18), o8 | (starts << 18), lptr[q] | (n2[q] << 20),
+                              (lptr[q] + n2[q]) | (n8[q] << 20));
     }
     meta_h[nl] = meta_h[nl + 1] = make_int4(0, 0, 0, 0);  // sentinels: prefetches past the end read null rows
     for (int c = 0; c < nc; ++c)
         ctab_h[c] = make_int4(static_cast<int>(goff[cfirst[c]] / 16), cbytes[c], roff[c], after[c]);
 
+    walk_import_base = import_base;
+    walk_pbar_bytes = pbar_bytes;
+    walk_n_peer = 0;
+    if (link && link->peer_bytes) {
+        walk_n_peer = static_cast<int>(link->peer_bytes->size());
+        walk_peer_bytes.upload(*link->peer_bytes, s);
+    }
+    if (link) {
+        if (link->plv_out) *link->plv_out = plv_of;
+        link->shape[0] = best_w;
+        link->shape[1] = best_r2;
+        link->shape[2] = best_r8;
+        link->shape[3] = kw;
+        walk_role = link->role;
+    }
     walk = true;
     usable = true;
     bands = 1;
@@ -727,16 +903,52 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     bidx.upload(bidx_h, s);
     SDG_CUDA(cudaFuncSetAttribute(walk_kernel(best_r2, best_r8, kw), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   budget));
+    if (link && link->role && best_r2 <= 2 && best_r8 <= 2)
+        SDG_CUDA(cudaFuncSetAttribute(walk_kernel(best_r2, best_r8, kw, true),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
     SDG_CUDA(cudaStreamSynchronize(s));  // host staging vectors die here
     return true;
 }
 
+namespace {
+WalkArgs walk_args(const GsPlan& g, double* z_new) {
+    return WalkArgs{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.records()),
+                    g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes,
+                    z_new, g.walk_role, g.walk_n_peer, g.walk_pbar_bytes, g.walk_peer_bytes.get()};
+}
+}  // namespace
+
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new) {
-    WalkArgs a{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.records()),
-               g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes, z_new};
-    launch_k(c, walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw), 1, g.nthreads, g.smem, a);
+    WalkPair pair{};
+    pair.a[0] = walk_args(g, z_new);
+    launch_k(c, walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw), 1, g.nthreads, g.smem, pair);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(SDG_ECUDA, std::string("launch_gs_walk: ") + cudaGetErrorString(e));
+    c.count();
+}
+
+void launch_gs_pipe(Context& c, const GsPlan& g, double* z_new) {
+    const GsPlan& p0 = *g.parts[0];
+    const GsPlan& p1 = *g.parts[1];
+    WalkPair pair{};
+    pair.a[0] = walk_args(p0, z_new + g.part_r0[0]);
+    pair.a[1] = walk_args(p1, z_new + g.part_r0[1]);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(p0.nthreads);
+    cfg.dynamicSmemBytes = std::max(p0.smem, p1.smem);
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = c.pdl ? 2 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, walk_kernel(p0.walk_r2, p0.walk_r8, p0.walk_kw, true), pair);
+    if (e != cudaSuccess) fail(SDG_ECUDA, std::string("launch_gs_pipe: ") + cudaGetErrorString(e));
     c.count();
 }
 

@@ -34,8 +34,10 @@ int main(int argc, char** argv) {
     cudaMemcpy(g.packed.get(), pk.data(), pk.size() * 8, cudaMemcpyHostToDevice);
     double* z;
     cudaMalloc(&z, n * 8);
-    WalkArgs wa{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.packed.get()),
-                g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes, z};
+    WalkPair wa{};
+    wa.a[0] = WalkArgs{g.meta.get(), g.walk_iss.get(), reinterpret_cast<const unsigned char*>(g.packed.get()),
+                       g.n_levels, g.walk_chunks, g.ring, g.walk_meta_bytes, g.walk_chunk_bytes, g.walk_zbytes, z,
+                       0, 0, 0, nullptr};
     const auto kern = walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw);
     printf("plan: warps %d rows/thread %d+%d levels %d\n", g.nthreads / 32 - 1, g.walk_r2, g.walk_r8, g.n_levels);
     for (int r = 0; r < 3; ++r) kern<<<1, g.nthreads, g.smem, s>>>(wa);

@@ -111,12 +111,14 @@ def test_amg_on_system_blocks(ref):
     assert rel_l2(amg.apply(r), td.v_hierarchy.vcycle(r)) < 1e-11
 
 
-@pytest.mark.parametrize("mode", [{"SDG_GS_SPLIT": "1"}, {"SDG_GS_WALK": "0"}, {"SDG_GS_BANDS": "4"}],
-                         ids=["label-block-walks", "cluster-kernel", "cluster-4-bands"])
+@pytest.mark.parametrize("mode", [{"SDG_GS_SPLIT": "1"}, {"SDG_GS_PIPE": "1"}, {"SDG_GS_WALK": "0"},
+                                  {"SDG_GS_BANDS": "4"}],
+                         ids=["label-block-walks", "2-cta-pipe", "cluster-kernel", "cluster-4-bands"])
 def test_smoother_paths_match_reference(ref, golden, monkeypatch, mode):
     """The other lower-solve plans (one walk per u/v block with a coupling
-    step; the banded cluster kernel) against the reference V-cycle and the
-    golden td_bgs apply."""
+    step; the u/v blocks walked concurrently on a 2-CTA cluster; the banded
+    cluster kernel) against the reference V-cycle and the golden td_bgs
+    apply."""
     for k, v in mode.items():
         monkeypatch.setenv(k, v)
     s = ref.assemble(50)
