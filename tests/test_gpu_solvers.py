@@ -141,3 +141,21 @@ def test_determinism_two_runs(golden):
     assert a.report.iterations == b.report.iterations
     assert np.array_equal(a.report.residual_history, b.report.residual_history)
     assert np.array_equal(a.x, b.x)
+
+
+def test_c2u_gmres50_iterations_match_reference(ref):
+    """c2 shape with uniform K (the parity-pinned sub-case), GMRES(50): the
+    reference needs 172 iterations with and without FMA contraction
+    (profiles/r01/ref_spread_c2.jsonl), so the +-5 % bar applies directly."""
+    cfg = scenarios.CONFIGS["c2u"]
+    s = scenarios.build_system(cfg)
+    from oracle.refpy import Csr, System
+    rs = System(s.n_total(), s.n_u, s.n_vel, s.n_pff, s.n_ppm,
+                Csr(s.n_total(), s.n_total(), s.matrix.row_offsets, s.matrix.col_indices, s.matrix.values), s.rhs)
+    tol = 1e-8 * np.linalg.norm(s.rhs)
+    xr, rr = ref.pd_gmres(rs.a, s.rhs, tol, 400, precond=ref.td(rs), m_init=50, m_min=50, m_max=50)
+    p = sdc.TdPreconditioner(s, "td_bgs")
+    res = sdc.pd_gmres(s.matrix, p, s.rhs, tol, 400, sdc.RestartController.fixed(50))
+    assert rr.converged and res.report.converged
+    assert within(res.report.iterations, rr.iterations)
+    assert rel_l2(res.x, xr) <= X_TOL
