@@ -259,6 +259,72 @@ int sdg_host_hierarchy_level(const sdg_host_hierarchy* h, int lev, int* n, int64
                              double* val, int* agg);
 void sdg_host_hierarchy_destroy(sdg_host_hierarchy* h);
 
+/* ---- strip-sharded multi-GPU solve ----------------------
+ * One process (and one sdg_context) per GPU.  Every rank passes the same
+ * assembled system and the same ownership map (owner rank per global dof;
+ * sdg_strip_partition gives the horizontal strips: rank r owns free-flow
+ * cell rows of strip r from the bottom and porous strip r from the top, so
+ * rank 0 holds the interface).  Vectors at this boundary are the rank's own
+ * rows in ascending global order (sdg_dist_local_rows).  Replaces, per rank,
+ * the same reference entry points as the single-GPU calls (pd_gmres
+ * krylov.hpp:57-59, BlockPreconditioner td_* precond.cpp:304-363,
+ * MonolithicDriver::build_preconditioner bench.cpp:121-182).
+ * The smoother is Gauss-Seidel inside each strip with the previous iterate
+ * across strip boundaries (processor-block GS; identical to the single-GPU
+ * smoother for one rank).  The coarsest AMG level is solved redundantly.
+ *
+ * Transport: NCCL (grouped send/recv for halos, all-gather for the
+ * deterministic reductions), or host callbacks from the caller's runtime
+ * (buffers are host memory staged by the library; return 0 on success):
+ *   exchange: send[soff_p .. + send_counts[p]) to rank p, recv_counts[p]
+ *             doubles from rank p into recv + roff_p (offsets = prefix sums
+ *             in rank order; counts are symmetric by construction);
+ *   allgather: recv[p * count + k] = rank p's send[k]. */
+typedef struct sdg_transport sdg_transport;
+typedef struct sdg_dist_system sdg_dist_system;
+typedef struct sdg_dist_precond sdg_dist_precond;
+typedef int (*sdg_host_exchange_fn)(void* user, const double* send, const int* send_counts, double* recv,
+                                    const int* recv_counts);
+typedef int (*sdg_host_allgather_fn)(void* user, const double* send, int count, double* recv);
+
+int sdg_transport_create_host(int rank, int size, sdg_host_exchange_fn exchange, sdg_host_allgather_fn allgather,
+                              void* user, sdg_transport** out);
+/* NCCL: rank 0 creates the id, the caller distributes it (128 bytes). */
+int sdg_nccl_get_unique_id(unsigned char id[128]);
+int sdg_transport_create_nccl(sdg_context* ctx, const unsigned char id[128], int rank, int size,
+                              sdg_transport** out);
+int sdg_transport_destroy(sdg_transport* t);
+
+/* owner[n_total] for the n x n monolithic layout (sdg_assemble_monolithic). */
+int sdg_strip_partition(int n, int n_ranks, int* owner);
+
+/* Host-only inspection (no GPU): the halo plan of the monolithic operator on
+ * `rank` -- ghost columns sorted by (owner, id) with per-owner counts, and
+ * the rows each peer needs from this rank, grouped by peer.  NULL outputs
+ * are skipped (call once with NULL arrays to size them). */
+int sdg_dist_halo_plan(int n_total, const int* rowptr, const int* col, const int* owner, int rank, int size,
+                       int* n_ghost, int* ghost_gid, int* recv_counts, int* n_send, int* send_gid,
+                       int* send_counts);
+
+int sdg_dist_system_create(sdg_context* ctx, sdg_transport* tr, int n_total, const int* rowptr, const int* col,
+                           const double* val, int n_u, int n_vel, int n_pff, int n_ppm, const int* owner,
+                           sdg_dist_system** out);
+int sdg_dist_system_destroy(sdg_dist_system* s);
+int sdg_dist_local_rows(const sdg_dist_system* s, int* n_local, int* global_ids);
+/* spmv (sparse.cpp:81-90) on the rank's rows; collective. */
+int sdg_dist_spmv(sdg_dist_system* s, const double* x_local, double* y_local);
+/* td_bj / td_bgs as sdg_td_create, over strips; collective.  The system
+ * must outlive the preconditioner. */
+int sdg_dist_td_create(sdg_dist_system* s, int kind, int v_max_levels, int d_max_levels, double omega_override,
+                       sdg_dist_precond** out);
+int sdg_dist_precond_destroy(sdg_dist_precond* p);
+double sdg_dist_precond_omega(const sdg_dist_precond* p);
+double sdg_dist_precond_setup_seconds(const sdg_dist_precond* p);
+int sdg_dist_precond_apply(sdg_dist_system* s, sdg_dist_precond* p, const double* r_local, double* z_local);
+/* pd_gmres over strips; collective; tol_abs is the global absolute tolerance. */
+int sdg_dist_pd_gmres(sdg_dist_system* s, sdg_dist_precond* p, const double* b_local, double* x_local,
+                      double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -124,9 +124,8 @@ AmgPrecond::AmgPrecond(CtxPtr c, const HostCsr& a, const AmgOpts& o) : Precond(s
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
-void AmgPrecond::factor_coarse(const HostCsr& coarse) {
-    Context& cx = *ctx_;
-    n_c_ = coarse.n_rows;
+void dense_inverse(Context& cx, const HostCsr& coarse, DevBuf<double>& coarse_inv_) {
+    const int n_c_ = coarse.n_rows;
     if (n_c_ == 0) return;
     const size_t nn = static_cast<size_t>(n_c_) * n_c_;
     DevCsr dc;
@@ -163,6 +162,11 @@ void AmgPrecond::factor_coarse(const HostCsr& coarse) {
                          n_c_, info.get()) != CUSOLVER_STATUS_SUCCESS)
         fail(SDG_ECUDA, "cusolverDnDgetrs failed");
     cx.sync();
+}
+
+void AmgPrecond::factor_coarse(const HostCsr& coarse) {
+    n_c_ = coarse.n_rows;
+    dense_inverse(*ctx_, coarse, coarse_inv_);
 }
 
 int64_t AmgPrecond::setup_memory_doubles() const {

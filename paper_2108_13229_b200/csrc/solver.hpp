@@ -181,6 +181,10 @@ SolveOut pd_gmres(Matrix& a, Precond* p, const double* b_dev, double* x_dev, dou
 SolveOut bicgstab(Matrix& a, Precond* p, const double* b_dev, double* x_dev, double tol_abs,
                   int max_iters);
 
+// Row-major explicit inverse of a (small, coarsest-level) matrix: dense LU on
+// the device (cuSOLVER getrf) + getrs against I.  Throws SDG_ESINGULAR.
+void dense_inverse(Context& c, const HostCsr& a, DevBuf<double>& inv);
+
 struct PowerOut {
     double value = 0.0;
     bool converged = false;
