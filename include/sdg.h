@@ -325,6 +325,10 @@ int sdg_dist_precond_apply(sdg_dist_system* s, sdg_dist_precond* p, const double
 int sdg_dist_pd_gmres(sdg_dist_system* s, sdg_dist_precond* p, const double* b_local, double* x_local,
                       double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep);
 
+/* bicgstab over strips; collective. */
+int sdg_dist_bicgstab(sdg_dist_system* s, sdg_dist_precond* p, const double* b_local, double* x_local,
+                      double tol_abs, int max_iters, sdg_report* rep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,38 @@ __global__ void k_add_gathered(int n, const int* __restrict__ ptr, const int* __
     acc[t] = a;
 }
 
+// BiCGSTAB vector updates with host scalars, in the reference's operation
+// order (krylov.cpp:246,255,278-279)
+__global__ void k_dbi_p(int n, double beta, double omega, const double* __restrict__ r,
+                        const double* __restrict__ vv, double* __restrict__ p) {
+    pdl_begin();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = __dadd_rn(r[i], __dmul_rn(beta, __dsub_rn(p[i], __dmul_rn(omega, vv[i]))));
+}
+
+__global__ void k_dbi_s(int n, double alpha, const double* __restrict__ r, const double* __restrict__ vv,
+                        double* __restrict__ s) {
+    pdl_begin();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) s[i] = __dsub_rn(r[i], __dmul_rn(alpha, vv[i]));
+}
+
+__global__ void k_dbi_xr(int n, double alpha, double omega, const double* __restrict__ phat,
+                         const double* __restrict__ shat, const double* __restrict__ s,
+                         const double* __restrict__ t, double* __restrict__ x, double* __restrict__ r) {
+    pdl_begin();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    x[i] = __dadd_rn(x[i], __dadd_rn(__dmul_rn(alpha, phat[i]), __dmul_rn(omega, shat[i])));
+    r[i] = __dsub_rn(s[i], __dmul_rn(omega, t[i]));
+}
+
+__global__ void k_daxpy(int n, double alpha, const double* __restrict__ x, double* __restrict__ y) {
+    pdl_begin();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = __dadd_rn(y[i], __dmul_rn(alpha, x[i]));
+}
+
 void launch_gather(Context& c, int n, const int* idx, const double* src, double* dst) {
     ProfScope ps_(c, PF_VEC, 16.0 * n);
     if (n <= 0) return;
@@ -836,6 +868,148 @@ SolveOut dist_pd_gmres(DistSystem& S, DistTd* P, const double* b, double* x, dou
     out.history.push_back(res_norm);
     out.final_residual = res_norm;
     out.converged = res_norm <= tol_abs;
+    finish();
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// BiCGSTAB over strips (krylov.cpp:186-292): host scalars, reductions as
+// deterministic all-gathers of per-rank partials
+
+SolveOut dist_bicgstab(DistSystem& S, DistTd* P, const double* b, double* x, double tol_abs, int max_iters) {
+    Context& c = *S.ctx;
+    Transport& tr = *S.tr;
+    const int n = S.n_local();
+    const int nn = std::max(n, 1);
+    cudaEvent_t ea, eb;
+    SDG_CUDA(cudaEventCreate(&ea));
+    SDG_CUDA(cudaEventCreate(&eb));
+    SDG_CUDA(cudaEventRecord(ea, c.stream));
+    SolveOut out;
+    DevBuf<double> r(nn), rhat(nn), p(nn), vv(nn), s(nn), phat(nn), shat(nn), t(nn), rt(nn), part(4);
+    ReduceWs ws;
+    ws.init(reduce_blocks(nn, c.num_sms), 2, c.stream);
+    double hv[4];
+    auto precond = [&](const double* in, double* o) {
+        if (P)
+            P->apply(in, o);
+        else
+            launch_copy(c, o, in, n);
+    };
+    auto dot1 = [&](const double* a, const double* bb) {
+        launch_dot(c, ws, n, a, bb, part.get());
+        tr.allreduce(c, part.get(), 1, hv);
+        return hv[0];
+    };
+    auto norm = [&](const double* a) {
+        launch_norm2sq(c, ws, n, a, part.get());
+        tr.allreduce(c, part.get(), 1, hv);
+        return std::sqrt(hv[0]);
+    };
+    auto residual = [&](double* dst) { S.A.apply_add(c, tr, x, b, dst, -1.0); };
+    const int g = nblk(n);
+
+    launch_fill(c, x, 0.0, n);
+    launch_copy(c, r.get(), b, n);
+    double res_norm = norm(r.get());
+    out.history.push_back(res_norm);
+    auto finish = [&]() {
+        SDG_CUDA(cudaEventRecord(eb, c.stream));
+        SDG_CUDA(cudaEventSynchronize(eb));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ea, eb);
+        out.device_ms = ms;
+        cudaEventDestroy(ea);
+        cudaEventDestroy(eb);
+    };
+    if (res_norm <= tol_abs) {
+        out.converged = true;
+        out.final_residual = res_norm;
+        finish();
+        return out;
+    }
+    double rho = 1.0, alpha = 1.0, omega = 1.0;
+    auto reset = [&]() {
+        launch_copy(c, rhat.get(), r.get(), n);
+        launch_fill(c, p.get(), 0.0, n);
+        launch_fill(c, vv.get(), 0.0, n);
+        rho = alpha = omega = 1.0;
+    };
+    reset();
+    int restarts = 0, replacements = 0;
+    bool done = false;
+    auto hard_restart = [&]() {
+        if (++restarts > 1) fail(SDG_EBREAKDOWN, "bicgstab: repeated breakdown");
+        residual(r.get());
+        reset();
+    };
+    auto confirmed = [&]() {
+        residual(rt.get());
+        const double tn = norm(rt.get());
+        if (tn <= tol_abs) return true;
+        if (replacements++ < 3) {
+            launch_copy(c, r.get(), rt.get(), n);
+            reset();
+            return false;
+        }
+        done = true;
+        return false;
+    };
+    for (int iter = 0; iter < max_iters && !done; ++iter) {
+        const double rho_new = dot1(rhat.get(), r.get());
+        if (std::abs(rho_new) < 1e-300) {
+            hard_restart();
+            continue;
+        }
+        const double beta = (rho_new / rho) * (alpha / omega);
+        launch_k(c, k_dbi_p, g, kT, 0, n, beta, omega, r.get(), vv.get(), p.get());
+        c.count();
+        precond(p.get(), phat.get());
+        S.A.apply(c, tr, phat.get(), vv.get());
+        const double rv = dot1(rhat.get(), vv.get());
+        if (std::abs(rv) < 1e-300) {
+            hard_restart();
+            continue;
+        }
+        alpha = rho_new / rv;
+        launch_k(c, k_dbi_s, g, kT, 0, n, alpha, r.get(), vv.get(), s.get());
+        c.count();
+        ++out.iterations;
+        const double sn = norm(s.get());
+        if (sn <= tol_abs) {
+            launch_k(c, k_daxpy, g, kT, 0, n, alpha, phat.get(), x);
+            c.count();
+            out.history.push_back(sn);
+            if (confirmed()) break;
+            continue;
+        }
+        precond(s.get(), shat.get());
+        S.A.apply(c, tr, shat.get(), t.get());
+        launch_dot(c, ws, n, t.get(), t.get(), part.get());
+        launch_dot(c, ws, n, t.get(), s.get(), part.get() + 1);
+        tr.allreduce(c, part.get(), 2, hv);
+        const double tt = hv[0];
+        if (tt == 0.0) {
+            hard_restart();
+            continue;
+        }
+        omega = hv[1] / tt;
+        if (std::abs(omega) < 1e-300) {
+            hard_restart();
+            continue;
+        }
+        launch_k(c, k_dbi_xr, g, kT, 0, n, alpha, omega, phat.get(), shat.get(), s.get(), t.get(), x, r.get());
+        c.count();
+        rho = rho_new;
+        res_norm = norm(r.get());
+        out.history.push_back(res_norm);
+        if (res_norm <= tol_abs && confirmed()) break;
+    }
+    residual(rt.get());
+    const double fin = norm(rt.get());
+    out.final_residual = fin;
+    out.history.push_back(fin);
+    out.converged = fin <= tol_abs;
     finish();
     return out;
 }

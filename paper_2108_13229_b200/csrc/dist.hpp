@@ -188,6 +188,9 @@ private:
 SolveOut dist_pd_gmres(DistSystem& s, DistTd* p, const double* b, double* x, double tol_abs, int max_restarts,
                        Restart ctrl);
 
+// bicgstab (krylov.cpp:186-292) over strips.
+SolveOut dist_bicgstab(DistSystem& s, DistTd* p, const double* b, double* x, double tol_abs, int max_iters);
+
 // Horizontal strips of the n x n free-flow box (rank r: cell rows of strip r
 // from the bottom) and of the porous box (rank r: strip r from the top).
 std::vector<int> strip_partition(int n, int size);

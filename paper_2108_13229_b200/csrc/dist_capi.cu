@@ -195,4 +195,22 @@ int sdg_dist_pd_gmres(sdg_dist_system* s, sdg_dist_precond* p, const double* b_l
     });
 }
 
+int sdg_dist_bicgstab(sdg_dist_system* s, sdg_dist_precond* p, const double* b_local, double* x_local,
+                      double tol_abs, int max_iters, sdg_report* rep) {
+    return guard([&] {
+        need(s, "sdg_dist_bicgstab");
+        auto t0 = std::chrono::steady_clock::now();
+        sdg::DistSystem& S = *s->p;
+        sdg::Context& c = *S.ctx;
+        const int n = S.n_local();
+        sdg::DevBuf<double> b(std::max(n, 1)), x(std::max(n, 1));
+        b.upload(b_local, n, c.stream);
+        const int64_t apps0 = p ? p->p->applications() : 0;
+        sdg::SolveOut o = sdg::dist_bicgstab(S, p ? p->p.get() : nullptr, b.get(), x.get(), tol_abs, max_iters);
+        if (n) SDG_CUDA(cudaMemcpyAsync(x_local, x.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        fill_report(o, seconds_since(t0), (p ? p->p->applications() : 0) - apps0, rep);
+    });
+}
+
 }  // extern "C"

@@ -61,6 +61,7 @@ def _lib():
     p("sdg_dist_precond_setup_seconds", _d, [_vp])
     p("sdg_dist_precond_apply", _i, [_vp, _vp, _dp, _dp])
     p("sdg_dist_pd_gmres", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Restart), P(_Report)])
+    p("sdg_dist_bicgstab", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Report)])
     _bound = True
     return L
 
@@ -263,5 +264,20 @@ def dist_pd_gmres(ds: DistSystem, precond: Optional[DistTdPreconditioner], b_loc
     return GmresResult(x, _report(rep, hist))
 
 
-__all__ = ["strip_partition", "halo_plan", "CallbackTransport", "NcclTransport", "DistSystem",
+def dist_bicgstab(ds: DistSystem, precond: Optional[DistTdPreconditioner], b_local, tol_abs: float,
+                  max_iters: int, history_capacity: int = 1 << 16) -> GmresResult:
+    """bicgstab (krylov.cpp:186-292) over strips; collective over the ranks."""
+    b = _f64(b_local)
+    if b.size != ds.n_local():
+        raise ValueError("bicgstab: dimension mismatch")
+    x = np.empty(ds.n_local())
+    hist = np.empty(history_capacity)
+    rep = _Report()
+    rep.residual_history = hist.ctypes.data_as(C.POINTER(_d))
+    rep.history_capacity = history_capacity
+    _check(_lib().sdg_dist_bicgstab(ds.h, precond.h if precond else None, b, x, tol_abs, max_iters, C.byref(rep)))
+    return GmresResult(x, _report(rep, hist))
+
+
+__all__ = ["dist_bicgstab", "strip_partition", "halo_plan", "CallbackTransport", "NcclTransport", "DistSystem",
            "DistTdPreconditioner", "dist_pd_gmres", "SdgCudaError", "SolveReport"]
