@@ -47,6 +47,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-solves", type=int, default=1)
+    ap.add_argument("--sharded", action="store_true",
+                    help="strip-shard one system across the ranks (strong scaling, sdg_dist_*) instead of "
+                         "running one replica per rank")
     return ap.parse_args()
 
 
@@ -369,10 +372,110 @@ def run_ours(args):
     return 0
 
 
+def run_sharded(args):
+    """One system split into horizontal strips over the ranks,
+    NCCL transport; `value` = DoF*iterations of the whole system / max-over-ranks
+    device time (strong scaling: the work is fixed as N grows)."""
+    import torch
+    rank, local_rank, world = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    from paper_2108_13229_b200 import dist as sd
+    from paper_2108_13229_b200 import scenarios, sdc
+
+    cfg = scenarios.CONFIGS[args.config]
+    s = scenarios.build_system(cfg)
+    n = s.n_total()
+    tol = 1e-8 * float(np.linalg.norm(s.rhs))
+    ctx = sdc.Context(local_rank)
+    tr = sd.NcclTransport(ctx)
+    ds = sd.DistSystem(s, tr, ctx=ctx)
+    t0 = time.perf_counter()
+    p = sd.DistTdPreconditioner(ds, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
+    setup_s = time.perf_counter() - t0
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    b_loc = ds.local(s.rhs)
+    b_dev = torch.from_numpy(b_loc).to(dev)
+    x_dev = torch.zeros(ds.n_local(), dtype=torch.float64, device=dev)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    ctrl = sdc.RestartController.fixed(50) if cfg.solver == "gmres50" else sdc.RestartController.defaults()
+    max_it = 20000 if cfg.solver == "bicgstab" else 4000
+
+    def step():
+        return sd.dist_solve_device(ds, p, cfg.solver, b_dev.data_ptr(), x_dev.data_ptr(), tol, max_it, ctrl)
+
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        rep = step()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    evs, iters = [], []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        rep = step()
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        evs.append((e0, e1))
+        iters.append(rep.iterations)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = ctx.launches - launches0
+    clk = clocks.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    # strong scaling: every rank reports the same iterations of the one system
+    total_ms, _ = job_totals(dist, total_ms, 0.0, dev)
+    value = float(n) * sum(iters) / (total_ms / 1e3)
+    e2e = None
+    if not args.no_e2e:
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e_its = 0
+        for _ in range(args.steps):
+            res = (sd.dist_bicgstab(ds, p, b_loc, tol, max_it) if cfg.solver == "bicgstab"
+                   else sd.dist_pd_gmres(ds, p, b_loc, tol, max_it, ctrl))
+            e_its += res.report.iterations
+        e_s = time.perf_counter() - t0
+        e_s, _ = job_totals(dist, e_s, 0.0, dev)
+        e2e = {"value": float(n) * e_its / e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * ds.n_local(),
+               "d2h_bytes_per_step": 8 * ds.n_local(), "ms_per_step": 1e3 * e_s / args.steps,
+               "timing": "host wall clock around the synchronous sdg_dist_* call, max over ranks"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg, s), "dof": n, "nnz": s.matrix.nnz(),
+                   "parallelism": f"horizontal strips x{world} (processor-block GS inside strips, NCCL halos)",
+                   "l2": "flushed between timed solves (256 MiB write, outside the event pair)",
+                   "iterations": iters, "setup_s": setup_s, "omega": p.omega(), "local_rows": ds.n_local()},
+        "gpu_launches": launches, "clocks": clk, "e2e": e2e,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.sharded:
+        return run_sharded(args)
     return run_ours(args)
 
 

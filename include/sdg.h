@@ -329,6 +329,12 @@ int sdg_dist_pd_gmres(sdg_dist_system* s, sdg_dist_precond* p, const double* b_l
 int sdg_dist_bicgstab(sdg_dist_system* s, sdg_dist_precond* p, const double* b_local, double* x_local,
                       double tol_abs, int max_iters, sdg_report* rep);
 
+/* device-pointer variants (b, x on the context's device, stream-ordered). */
+int sdg_dist_pd_gmres_device(sdg_dist_system* s, sdg_dist_precond* p, const double* b_dev, double* x_dev,
+                             double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep);
+int sdg_dist_bicgstab_device(sdg_dist_system* s, sdg_dist_precond* p, const double* b_dev, double* x_dev,
+                             double tol_abs, int max_iters, sdg_report* rep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -213,4 +213,27 @@ int sdg_dist_bicgstab(sdg_dist_system* s, sdg_dist_precond* p, const double* b_l
     });
 }
 
+int sdg_dist_pd_gmres_device(sdg_dist_system* s, sdg_dist_precond* p, const double* b_dev, double* x_dev,
+                             double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep) {
+    return guard([&] {
+        need(s, "sdg_dist_pd_gmres_device");
+        auto t0 = std::chrono::steady_clock::now();
+        const int64_t apps0 = p ? p->p->applications() : 0;
+        sdg::SolveOut o = sdg::dist_pd_gmres(*s->p, p ? p->p.get() : nullptr, b_dev, x_dev, tol_abs, max_restarts,
+                                             restart_from(ctrl));
+        fill_report(o, seconds_since(t0), (p ? p->p->applications() : 0) - apps0, rep);
+    });
+}
+
+int sdg_dist_bicgstab_device(sdg_dist_system* s, sdg_dist_precond* p, const double* b_dev, double* x_dev,
+                             double tol_abs, int max_iters, sdg_report* rep) {
+    return guard([&] {
+        need(s, "sdg_dist_bicgstab_device");
+        auto t0 = std::chrono::steady_clock::now();
+        const int64_t apps0 = p ? p->p->applications() : 0;
+        sdg::SolveOut o = sdg::dist_bicgstab(*s->p, p ? p->p.get() : nullptr, b_dev, x_dev, tol_abs, max_iters);
+        fill_report(o, seconds_since(t0), (p ? p->p->applications() : 0) - apps0, rep);
+    });
+}
+
 }  // extern "C"

@@ -62,6 +62,8 @@ def _lib():
     p("sdg_dist_precond_apply", _i, [_vp, _vp, _dp, _dp])
     p("sdg_dist_pd_gmres", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Restart), P(_Report)])
     p("sdg_dist_bicgstab", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Report)])
+    p("sdg_dist_pd_gmres_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Restart), P(_Report)])
+    p("sdg_dist_bicgstab_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Report)])
     _bound = True
     return L
 
@@ -279,5 +281,23 @@ def dist_bicgstab(ds: DistSystem, precond: Optional[DistTdPreconditioner], b_loc
     return GmresResult(x, _report(rep, hist))
 
 
-__all__ = ["dist_bicgstab", "strip_partition", "halo_plan", "CallbackTransport", "NcclTransport", "DistSystem",
+def dist_solve_device(ds: DistSystem, precond: Optional[DistTdPreconditioner], solver: str, b_ptr: int,
+                      x_ptr: int, tol_abs: float, max_iters: int,
+                      ctrl: Optional[RestartController] = None) -> SolveReport:
+    """Device-pointer solve over strips (b, x: this rank's rows on its GPU)."""
+    rep = _Report()
+    hist = np.empty(1 << 14)
+    rep.residual_history = hist.ctypes.data_as(C.POINTER(_d))
+    rep.history_capacity = hist.size
+    ph = precond.h if precond else None
+    if solver == "bicgstab":
+        _check(_lib().sdg_dist_bicgstab_device(ds.h, ph, b_ptr, x_ptr, tol_abs, max_iters, C.byref(rep)))
+    else:
+        rc = (ctrl or RestartController.defaults())._c()
+        _check(_lib().sdg_dist_pd_gmres_device(ds.h, ph, b_ptr, x_ptr, tol_abs, max_iters, C.byref(rc),
+                                               C.byref(rep)))
+    return _report(rep, hist)
+
+
+__all__ = ["dist_solve_device", "dist_bicgstab", "strip_partition", "halo_plan", "CallbackTransport", "NcclTransport", "DistSystem",
            "DistTdPreconditioner", "dist_pd_gmres", "SdgCudaError", "SolveReport"]
