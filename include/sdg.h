@@ -81,6 +81,7 @@ typedef struct sdg_report {
     int history_length;
     int64_t precond_applications; /* applications made by this solve */
     double device_ms;       /* CUDA-event time of the device-resident part */
+    int breakdown;          /* warm-started BiCGSTAB only: ended by a repeated breakdown (x = last iterate) */
 } sdg_report;
 
 /* AmgOptions (precond.hpp:64-72).  components: NULL or one label per row. */
@@ -211,6 +212,23 @@ int sdg_pd_gmres(sdg_matrix* a, sdg_precond* precond, const double* b_host, doub
 int sdg_pd_gmres_device(sdg_matrix* a, sdg_precond* precond, const double* b_dev,
                         double* x_dev, double tol_abs, int max_restarts,
                         const sdg_restart* ctrl, sdg_report* rep);
+/* Warm-started pd_gmres (BASELINE config 4): x is the initial guess on entry
+ * and the solution on exit.  Exactly the reference solve of the correction
+ * (x0 = 0 is hard-coded at krylov.cpp:58): r0 = b - A x, A d = r0 with
+ * tol_abs, x += d.  rep describes the correction solve. */
+int sdg_pd_gmres_warm(sdg_matrix* a, sdg_precond* precond, const double* b_host, double* x_host,
+                      double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep);
+int sdg_pd_gmres_warm_device(sdg_matrix* a, sdg_precond* precond, const double* b_dev, double* x_dev,
+                             double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep);
+/* Warm-started bicgstab, same correction form (x0 = 0 at krylov.cpp:194).
+ * A repeated breakdown (the reference throws, krylov.cpp:215) is reported
+ * instead: rep->breakdown = 1, rep->converged = 0 and x = x0 + the last
+ * iterate, so a driver can restart from there (which re-seeds the shadow
+ * residual, as the reference's hard restart does). */
+int sdg_bicgstab_warm(sdg_matrix* a, sdg_precond* precond, const double* b_host, double* x_host,
+                      double tol_abs, int max_iters, sdg_report* rep);
+int sdg_bicgstab_warm_device(sdg_matrix* a, sdg_precond* precond, const double* b_dev, double* x_dev,
+                             double tol_abs, int max_iters, sdg_report* rep);
 /* bicgstab (krylov.hpp:63-65, krylov.cpp:186-292). */
 int sdg_bicgstab(sdg_matrix* a, sdg_precond* precond, const double* b_host, double* x_host,
                  double tol_abs, int max_iters, sdg_report* rep);

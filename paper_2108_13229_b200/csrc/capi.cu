@@ -352,6 +352,77 @@ int sdg_pd_gmres_device(sdg_matrix* a, sdg_precond* precond, const double* b_dev
     });
 }
 
+// Warm start (BASELINE config 4): the reference starts
+// every solve from x = 0 (krylov.cpp:58), so a warm-started solve is the
+// reference solve of the correction: r0 = b - A x, A d = r0, x += d.
+int sdg_pd_gmres_warm_device(sdg_matrix* a, sdg_precond* precond, const double* b_dev, double* x_dev,
+                             double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep) {
+    return guard([&] {
+        need(a, "sdg_pd_gmres_warm");
+        auto t0 = std::chrono::steady_clock::now();
+        auto& c = *a->p->ctx;
+        const int n = a->p->host.n_rows;
+        sdg::DevBuf<double> r0(std::max(n, 1)), d(std::max(n, 1));
+        sdg::launch_spmv_add(c, a->p->dev, x_dev, b_dev, r0.get(), -1.0);
+        const int64_t apps0 = precond ? precond->p->applications() : 0;
+        sdg::SolveOut o = sdg::pd_gmres(*a->p, precond ? precond->p.get() : nullptr, r0.get(), d.get(),
+                                        tol_abs, max_restarts, restart_from(ctrl));
+        sdg::launch_add_inplace(c, n, x_dev, d.get());
+        c.sync();
+        fill_report(o, seconds_since(t0), (precond ? precond->p->applications() : 0) - apps0, rep);
+    });
+}
+
+int sdg_pd_gmres_warm(sdg_matrix* a, sdg_precond* precond, const double* b_host, double* x_host,
+                      double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep) {
+    return guard([&] {
+        need(a, "sdg_pd_gmres_warm");
+        auto& c = *a->p->ctx;
+        const int n = a->p->host.n_rows;
+        sdg::DevBuf<double> b(std::max(n, 1)), x(std::max(n, 1));
+        b.upload(b_host, n, c.stream);
+        x.upload(x_host, n, c.stream);
+        const int rc = sdg_pd_gmres_warm_device(a, precond, b.get(), x.get(), tol_abs, max_restarts, ctrl, rep);
+        if (rc != SDG_OK) sdg::fail(rc, g_last_error);
+        if (n) SDG_CUDA(cudaMemcpyAsync(x_host, x.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+
+int sdg_bicgstab_warm_device(sdg_matrix* a, sdg_precond* precond, const double* b_dev, double* x_dev,
+                             double tol_abs, int max_iters, sdg_report* rep) {
+    return guard([&] {
+        need(a, "sdg_bicgstab_warm");
+        auto t0 = std::chrono::steady_clock::now();
+        auto& c = *a->p->ctx;
+        const int n = a->p->host.n_rows;
+        sdg::DevBuf<double> r0(std::max(n, 1)), d(std::max(n, 1));
+        sdg::launch_spmv_add(c, a->p->dev, x_dev, b_dev, r0.get(), -1.0);
+        const int64_t apps0 = precond ? precond->p->applications() : 0;
+        sdg::SolveOut o = sdg::bicgstab(*a->p, precond ? precond->p.get() : nullptr, r0.get(), d.get(), tol_abs,
+                                        max_iters, /*throw_on_breakdown=*/false);
+        sdg::launch_add_inplace(c, n, x_dev, d.get());
+        c.sync();
+        fill_report(o, seconds_since(t0), (precond ? precond->p->applications() : 0) - apps0, rep);
+    });
+}
+
+int sdg_bicgstab_warm(sdg_matrix* a, sdg_precond* precond, const double* b_host, double* x_host, double tol_abs,
+                      int max_iters, sdg_report* rep) {
+    return guard([&] {
+        need(a, "sdg_bicgstab_warm");
+        auto& c = *a->p->ctx;
+        const int n = a->p->host.n_rows;
+        sdg::DevBuf<double> b(std::max(n, 1)), x(std::max(n, 1));
+        b.upload(b_host, n, c.stream);
+        x.upload(x_host, n, c.stream);
+        const int rc = sdg_bicgstab_warm_device(a, precond, b.get(), x.get(), tol_abs, max_iters, rep);
+        if (rc != SDG_OK) sdg::fail(rc, g_last_error);
+        if (n) SDG_CUDA(cudaMemcpyAsync(x_host, x.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+
 int sdg_pd_gmres(sdg_matrix* a, sdg_precond* precond, const double* b_host, double* x_host,
                  double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep) {
     return guard([&] {

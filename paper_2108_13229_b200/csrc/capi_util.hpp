@@ -100,6 +100,7 @@ inline void fill_report(const sdg::SolveOut& o, double wall, int64_t apps, sdg_r
     rep->wall_time = wall;
     rep->device_ms = o.device_ms;
     rep->precond_applications = apps;
+    rep->breakdown = o.breakdown ? 1 : 0;
     rep->history_length = static_cast<int>(o.history.size());
     if (rep->residual_history && rep->history_capacity > 0) {
         const int k = std::min(rep->history_capacity, rep->history_length);

@@ -15,6 +15,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
+#include <string>
 
 #include "solver.hpp"
 
@@ -240,7 +242,7 @@ bool graphs_enabled(const Context& c) {
 }  // namespace
 
 SolveOut bicgstab(Matrix& A, Precond* P, const double* b, double* x, double tol_abs,
-                  int max_iters) {
+                  int max_iters, bool throw_on_breakdown) {
     Context& c = *A.ctx;
     const int n = A.host.n_rows;
     if (A.host.n_rows != A.host.n_cols) fail(SDG_EDIM, "bicgstab: dimension mismatch");
@@ -351,8 +353,31 @@ SolveOut bicgstab(Matrix& A, Precond* P, const double* b, double* x, double tol_
 
     int restarts = 0, replacements = 0;
     bool done = false;
+    BiState last{};
+    static const bool debug = [] {
+        const char* e = std::getenv("SDG_DEBUG");
+        return e && e[0] == '1';
+    }();
     auto hard_restart = [&]() {
-        if (++restarts > 1) fail(SDG_EBREAKDOWN, "bicgstab: repeated breakdown");
+        if (debug)
+            std::fprintf(stderr, "[sdg] bicgstab hard restart %d: flag %d at iteration %d; rho_new %.3e rho %.3e "
+                                 "rv %.3e omega %.3e rn %.3e sn %.3e tt %.3e\n",
+                         restarts + 1, last.flag, out.iterations, last.rho_new, last.rho, last.rv, last.omega,
+                         last.rn, last.sn, last.tt);
+        if (++restarts > 1 && !throw_on_breakdown) {
+            out.breakdown = true;
+            done = true;
+            return;
+        }
+        if (restarts > 1) {
+            static const char* why[] = {"", "rho", "rv", "", "tt", "omega"};
+            char msg[256];
+            std::snprintf(msg, sizeof msg,
+                          "bicgstab: repeated breakdown (%s at iteration %d; rho_new %.3e rho %.3e rv %.3e "
+                          "omega %.3e rn %.3e)",
+                          why[last.flag], out.iterations, last.rho_new, last.rho, last.rv, last.omega, last.rn);
+            fail(SDG_EBREAKDOWN, msg);
+        }
         true_residual(r.get());
         reset_directions(1.0);
     };
@@ -371,6 +396,7 @@ SolveOut bicgstab(Matrix& A, Precond* P, const double* b, double* x, double tol_
     for (int iter = 0; iter < max_iters && !done; ++iter) {
         run_iteration();
         BiState cur = read_state();
+        last = cur;
         switch (cur.flag) {
         case BI_BREAK_RHO:
         case BI_BREAK_RV:

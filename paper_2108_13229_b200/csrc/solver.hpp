@@ -166,6 +166,7 @@ struct SolveOut {
     double final_residual = 0.0;
     std::vector<double> history;
     double device_ms = 0.0;
+    bool breakdown = false;  // repeated BiCGSTAB breakdown, reported instead of thrown
 };
 
 struct Restart {
@@ -178,8 +179,10 @@ struct Restart {
 
 SolveOut pd_gmres(Matrix& a, Precond* p, const double* b_dev, double* x_dev, double tol_abs,
                   int max_restarts, Restart ctrl);
+// throw_on_breakdown = false: a repeated breakdown ends the solve with
+// out.breakdown set and x holding the last iterate (warm-started drivers).
 SolveOut bicgstab(Matrix& a, Precond* p, const double* b_dev, double* x_dev, double tol_abs,
-                  int max_iters);
+                  int max_iters, bool throw_on_breakdown = true);
 
 // Row-major explicit inverse of a (small, coarsest-level) matrix: dense LU on
 // the device (cuSOLVER getrf) + getrs against I.  Throws SDG_ESINGULAR.

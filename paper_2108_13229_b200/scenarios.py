@@ -85,8 +85,14 @@ CONFIGS = {
                   description="c2 shape with uniform K=1 (the parity-pinned sub-case)"),
     "c3": Config("c3", 500, 1e-2, False, "gmres50", 3, 3,
                  description="500x500 per subdomain (1,001,000 DoF), K=1e-2, GMRES(50)"),
-    "c4": Config("c4", 1000, 1.0, True, "gmres50", 4, 4, dt=0.1, steps=10,
+    # config 4 names no Krylov method ("warm-started Krylov solve"); with the
+    # log-normal field GMRES(50) stalls (1,399 iterations at 160^2 against
+    # BiCGSTAB's 151, profiles/r01/ref_spread_c2.jsonl), so it uses BiCGSTAB
+    # like config 2, the other log-normal config
+    "c4": Config("c4", 1000, 1.0, True, "bicgstab", 4, 4, dt=0.1, steps=10,
                  description="1000x1000 per subdomain (4,002,000 DoF), implicit Euler x10, log-normal K"),
+    "c4s": Config("c4s", 250, 1.0, True, "bicgstab", 4, 4, dt=0.1, steps=10,
+                  description="config 4 at 250x250 (the transient parity case)"),
 }
 
 

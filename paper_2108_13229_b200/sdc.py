@@ -68,7 +68,7 @@ class _Restart(C.Structure):
 class _Report(C.Structure):
     _fields_ = [("iterations", _i), ("converged", _i), ("wall_time", _d), ("final_residual", _d),
                 ("residual_history", C.POINTER(_d)), ("history_capacity", _i), ("history_length", _i),
-                ("precond_applications", _i64), ("device_ms", _d)]
+                ("precond_applications", _i64), ("device_ms", _d), ("breakdown", _i)]
 
 
 class _AmgOpts(C.Structure):
@@ -147,7 +147,11 @@ def lib():
         p("sdg_precond_set_graphs", _i, [_vp, _i])
         p("sdg_pd_gmres", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Restart), P(_Report)])
         p("sdg_pd_gmres_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Restart), P(_Report)])
+        p("sdg_pd_gmres_warm", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Restart), P(_Report)])
+        p("sdg_pd_gmres_warm_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Restart), P(_Report)])
         p("sdg_bicgstab", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Report)])
+        p("sdg_bicgstab_warm", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Report)])
+        p("sdg_bicgstab_warm_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Report)])
         p("sdg_bicgstab_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Report)])
         p("sdg_power_iteration", _i, [_vp, _d, _i, C.c_uint, P(_d), P(_i), P(_i)])
         p("sdg_assemble_monolithic", _i, [P(_Scenario), _vp, _vp, P(_i), P(_i64), P(_i), P(_i), P(_i),
@@ -669,6 +673,7 @@ class SolveReport:
     final_residual: float = 0.0
     precond_applications: int = 0
     device_ms: float = 0.0
+    breakdown: bool = False  # warm-started BiCGSTAB ended by a repeated breakdown
 
 
 @dataclass
@@ -680,7 +685,7 @@ class GmresResult:
 def _report(rep: _Report, hist: np.ndarray) -> SolveReport:
     n = min(rep.history_length, hist.size)
     return SolveReport(rep.iterations, hist[:n].copy(), bool(rep.converged), rep.wall_time, rep.final_residual,
-                       rep.precond_applications, rep.device_ms)
+                       rep.precond_applications, rep.device_ms, bool(rep.breakdown))
 
 
 def _operator_matrix(op) -> SparseMatrix:
@@ -709,6 +714,46 @@ def pd_gmres(op, precond: Optional[Preconditioner], b, tol_abs: float, max_resta
     _check(lib().sdg_pd_gmres(a.device(ctx).h, precond.h if precond else None, b, x, tol_abs, max_restarts,
                               C.byref(rc), C.byref(rep)))
     del _c
+    return GmresResult(x, _report(rep, hist))
+
+
+def pd_gmres_warm(op, precond: Optional[Preconditioner], b, x0, tol_abs: float, max_restarts: int,
+                  ctrl: Optional[RestartController] = None, history_capacity: int = 1 << 16) -> GmresResult:
+    """Warm-started pd_gmres: the reference solve (x0 = 0, krylov.cpp:58) of the
+    correction d in A d = b - A x0, returning x0 + d (BASELINE config 4)."""
+    a = _operator_matrix(op)
+    b = _f64(b)
+    x = _f64(x0).copy()
+    if b.size != a.n_rows or x.size != a.n_rows:
+        raise ValueError("pd_gmres: dimension mismatch")
+    ctrl = ctrl or RestartController.defaults()
+    ctx = precond.ctx if precond is not None else default_context()
+    hist = np.empty(history_capacity)
+    rep = _Report()
+    rep.residual_history = hist.ctypes.data_as(C.POINTER(_d))
+    rep.history_capacity = history_capacity
+    rc = ctrl._c()
+    _check(lib().sdg_pd_gmres_warm(a.device(ctx).h, precond.h if precond else None, b, x, tol_abs, max_restarts,
+                                   C.byref(rc), C.byref(rep)))
+    return GmresResult(x, _report(rep, hist))
+
+
+def bicgstab_warm(op, precond: Optional[Preconditioner], b, x0, tol_abs: float, max_iters: int,
+                  history_capacity: int = 1 << 16) -> GmresResult:
+    """Warm-started bicgstab: the reference solve (x0 = 0, krylov.cpp:194) of the
+    correction d in A d = b - A x0, returning x0 + d."""
+    a = _operator_matrix(op)
+    b = _f64(b)
+    x = _f64(x0).copy()
+    if b.size != a.n_rows or x.size != a.n_rows:
+        raise ValueError("bicgstab: dimension mismatch")
+    ctx = precond.ctx if precond is not None else default_context()
+    hist = np.empty(history_capacity)
+    rep = _Report()
+    rep.residual_history = hist.ctypes.data_as(C.POINTER(_d))
+    rep.history_capacity = history_capacity
+    _check(lib().sdg_bicgstab_warm(a.device(ctx).h, precond.h if precond else None, b, x, tol_abs, max_iters,
+                                   C.byref(rep)))
     return GmresResult(x, _report(rep, hist))
 
 
@@ -838,6 +883,19 @@ def bicgstab_device(a: SparseMatrix, precond: Optional[Preconditioner], b_ptr: i
                     max_iters: int, ctx: Optional[Context] = None) -> SolveReport:
     """sdg_bicgstab_device: b and x are device pointers on the context's device."""
     return _solve_device(lib().sdg_bicgstab_device, a, precond, b_ptr, x_ptr, tol_abs, max_iters, ctx=ctx)
+
+
+def bicgstab_warm_device(a: SparseMatrix, precond: Optional[Preconditioner], b_ptr: int, x_ptr: int,
+                         tol_abs: float, max_iters: int, ctx: Optional[Context] = None) -> SolveReport:
+    return _solve_device(lib().sdg_bicgstab_warm_device, a, precond, b_ptr, x_ptr, tol_abs, max_iters, ctx=ctx)
+
+
+def pd_gmres_warm_device(a: SparseMatrix, precond: Optional[Preconditioner], b_ptr: int, x_ptr: int,
+                         tol_abs: float, max_restarts: int, ctrl: Optional[RestartController] = None,
+                         ctx: Optional[Context] = None) -> SolveReport:
+    rc = (ctrl or RestartController.defaults())._c()
+    return _solve_device(lib().sdg_pd_gmres_warm_device, a, precond, b_ptr, x_ptr, tol_abs, max_restarts,
+                         C.byref(rc), ctx=ctx)
 
 
 def pd_gmres_device(a: SparseMatrix, precond: Optional[Preconditioner], b_ptr: int, x_ptr: int, tol_abs: float,

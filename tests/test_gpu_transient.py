@@ -1,0 +1,59 @@
+"""GPU: the implicit-Euler driver of BASELINE config 4 (MonolithicDriver::advance,
+bench.cpp:183-238) with warm-started GMRES(50), against the reference.
+
+The reference side is composed from its own pieces: its assembly
+(assemble_monolithic with v_prev and t, through the harness) and its solver
+on the correction r0 = b - A x_prev (x0 = 0 is hard-coded, krylov.cpp:58),
+with the preconditioner built once (the matrix is step-invariant, which the
+test checks).  Uniform K keeps the case parity-pinned."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from paper_2108_13229_b200 import drivers, scenarios, sdc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("solver", ["gmres50", "bicgstab"])
+def test_transient_warm_start_matches_reference(ref, solver):
+    cfg = dataclasses.replace(scenarios.CONFIGS["c4"], name="c4-small", n=16, lognormal=False, v_max_levels=3,
+                              d_max_levels=3, solver=solver)
+    drv = drivers.TransientDriver(cfg, warm_start=True)
+    sc = scenarios.scenario(cfg)
+    x_ref, td, a0 = None, None, None
+    for k in range(1, cfg.steps + 1):
+        t = k * cfg.dt
+        step = drv.advance(t)
+        v_prev = None if x_ref is None else x_ref[: drv.system.n_vel]
+        rs = ref.assemble(cfg.n, sc.permeability, sc.alpha_bj, sc.kinematic_viscosity, sc.density, sc.dt,
+                          sc.t_end, sc.dp_max, t=t, v_prev=v_prev)
+        # our assembly is the reference's, bit for bit, including v_prev and t
+        ours = scenarios.build_system(cfg, t=t, v_prev=v_prev)
+        assert np.array_equal(rs.rhs, ours.rhs)
+        if a0 is None:
+            a0 = rs.a
+            td = ref.td(rs)
+        assert np.array_equal(rs.a.val, a0.val)          # step-invariant matrix
+        tol = 1e-8 * np.linalg.norm(rs.rhs)
+        def ref_solve(rhs):
+            if solver == "bicgstab":
+                return ref.bicgstab(rs.a, rhs, tol, 20000, precond=td)
+            return ref.pd_gmres(rs.a, rhs, tol, 4000, precond=td, m_init=50, m_min=50, m_max=50)
+        if x_ref is None:
+            x_ref, rep = ref_solve(rs.rhs)
+        else:
+            d, rep = ref_solve(ref.spmv_add(rs.a, x_ref, rs.rhs, -1.0))
+            x_ref = x_ref + d
+        assert step.converged and rep.converged
+        if solver == "gmres50":
+            assert abs(step.iterations - rep.iterations) <= max(1, 0.05 * rep.iterations), (k, step.iterations,
+                                                                                             rep.iterations)
+        else:  # rounding-chaotic counts, bounded as in test_gpu_solvers
+            assert step.iterations <= 1.5 * rep.iterations + 5, (k, step.iterations, rep.iterations)
+        assert np.linalg.norm(drv.x - x_ref) / np.linalg.norm(x_ref) <= 1e-6
+        # x_prev + d rounds: the warm form meets the tolerance up to that last addition
+        assert np.linalg.norm(rs.rhs - sdc.spmv(drv.system.matrix, drv.x)) <= 1.1 * tol
+    # warm starts pay off: later steps need fewer iterations than the first
+    assert drv.history[-1].iterations < drv.history[0].iterations
