@@ -409,6 +409,8 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     const bool force_split = split_env && split_env[0] == '1';
     const char* pipe_env = std::getenv("SDG_GS_PIPE");
     const bool try_pipe = !force_split && pipe_env && pipe_env[0] == '1';  // opt-in
+    // 0. the lane chain, when the matrix is a structured finest level
+    if (want_walk && build_chain(a, comps, dinv_h, s)) return finish();
     // 1. two label blocks walked concurrently on a 2-CTA cluster
     if (want_walk && try_pipe && contiguous && r0.size() == 3 && build_pipe(a, r0, dinv_h, s)) return finish();
     // 2. one walk over the whole matrix
@@ -1018,6 +1020,11 @@ void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
     }
     ProfScope ps_(c, PF_GS, g.packed_bytes() + 8.0 * g.n);
     if (g.n == 0) return;
+    if (g.chain) {
+        launch_gs_chain(c, g, z_new);
+        SDG_GS_CHECK();
+        return;
+    }
     if (g.walk) {
         launch_gs_walk(c, g, z_new);
         return;

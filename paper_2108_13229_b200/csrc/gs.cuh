@@ -85,6 +85,13 @@ struct GsPlan {
     int walk_import_base = 0;  // first import slot of a walk (pipe role 2)
     int walk_n_peer = 0, walk_pbar_bytes = 0;
     DevBuf<int> walk_peer_bytes;  // pipe role 2: bytes the peer pushes at each of its levels
+    // lane-chain lower solve of a structured finest level (gs_chain.cu)
+    bool chain = false;
+    int chain_kind = 0;                  // 1: 5-point grid, 2: MAC velocity (u then v)
+    int chain_nx = 0, chain_ny = 0;      // grid columns (m for MAC) / lanes
+    int chain_steps = 0, chain_bands = 0;
+    size_t chain_smem = 0;
+    DevBuf<double> chain_coef;           // static scaled lower coefficients, [field][band][step][lane]
     const double* packed_ptr = nullptr;  // records of a part inside its parent's buffer
     size_t part_doubles = 0;             // size of a part's records
 
@@ -93,7 +100,7 @@ struct GsPlan {
     void build(const HostCsr& a, const std::vector<int>& components, cudaStream_t s,
                int bands_hint = 0);
     double packed_bytes() const {
-        return static_cast<double>(packed_ptr ? part_doubles : packed.size()) * 8.0;
+        return static_cast<double>(packed_ptr ? part_doubles : packed.size() + chain_coef.size()) * 8.0;
     }
     const double* records() const { return packed_ptr ? packed_ptr : packed.get(); }
 
@@ -114,6 +121,8 @@ struct GsPlan {
     };
 
 private:
+    bool build_chain(const HostCsr& a, const std::vector<int>& comps, const std::vector<double>& dinv_h,
+                     cudaStream_t s);
     bool build_parts(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
                      cudaStream_t s);
     bool build_pipe(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
@@ -129,6 +138,8 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
                          const double* zc, const int* agg);
 // the level walk; writes z_new (natural order)
 void launch_gs_lower(Context& c, const GsPlan& g, double* z_new);
+// lane-chain variant (plans with chain == true; gs_chain.cu)
+void launch_gs_chain(Context& c, const GsPlan& g, double* z_new);
 // single-CTA variant (plans with walk == true; gs_walk.cu)
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new);
 // the two parts of a pipe on a 2-CTA cluster (gs_walk.cu)
