@@ -262,6 +262,21 @@ int sdg_assemble_monolithic(const sdg_scenario* sc, const double* k_cell, const 
                             int* n_total, int64_t* nnz, int* n_u, int* n_vel, int* n_pff,
                             int* n_ppm, int* rowptr, int* col, double* val, double* rhs);
 
+/* ---- partitioned Dirichlet-Neumann subproblems (host, BASELINE config 5) ---
+ * assemble_stokes(ff box, FlowParams, v_prev, {p_in(t), p=0, wall}, &v_gamma)
+ * (assembly.cpp:287-303) and assemble_darcy(pm box, K/mu, {}, &p_gamma)
+ * (assembly.cpp:305-325) on the n x n boxes; uniform permeability, bitwise
+ * the reference.  Two-phase like sdg_assemble_monolithic.  The traces that
+ * close the coupling loop (coupling.cpp:218-242): stokes_pressure_trace
+ * (assembly.cpp:382-391) of the free-flow solution and
+ * darcy_velocity_trace_dirichlet (assembly.cpp:393-402) of the porous one. */
+int sdg_assemble_stokes(const sdg_scenario* sc, const double* v_prev, const double* v_gamma, int* n,
+                        int64_t* nnz, int* rowptr, int* col, double* val, double* rhs);
+int sdg_assemble_darcy(const sdg_scenario* sc, const double* p_gamma, int* n, int64_t* nnz, int* rowptr,
+                       int* col, double* val, double* rhs);
+int sdg_stokes_pressure_trace(const sdg_scenario* sc, const double* x_ff, double* trace);
+int sdg_darcy_velocity_trace(const sdg_scenario* sc, const double* p, const double* p_gamma, double* trace);
+
 /* ---- host-side setup inspection (no GPU needed) ----------------------------
  * The aggregation hierarchy exactly as the device preconditioner builds it
  * (amg_setup, precond.cpp:189-217, minus the coarse factorization), so the

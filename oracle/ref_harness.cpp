@@ -74,6 +74,10 @@ struct HierHandle {
     AMGHierarchy h;
 };
 
+struct PrecondHandle {
+    std::shared_ptr<const Preconditioner> p;
+};
+
 struct TdHandle {
     SparseMatrix a;                         // the monolithic matrix (owned copy)
     std::shared_ptr<UzawaPreconditioner> uz;
@@ -142,6 +146,104 @@ void ref_system_copy(void* hs, int* rp, int* ci, double* v, double* rhs) {
 }
 
 void ref_system_free(void* hs) { delete static_cast<SystemHandle*>(hs); }
+
+// ---------------------------------------------------------------------------
+// partitioned pieces (coupling.cpp:218-242): the standalone Stokes system with
+// Dirichlet interface velocities and the Darcy system with Dirichlet interface
+// pressures, on the n x n boxes, with the traces that close the loop.
+
+static ScenarioConfig scenario_of(int n, double permeability, double alpha_bj, double nu, double rho, double dt,
+                                  double t_end, double dp_max) {
+    ScenarioConfig cfg;
+    cfg.cells_per_unit_square = n;
+    cfg.permeability = permeability;
+    cfg.alpha_bj = alpha_bj;
+    cfg.kinematic_viscosity = nu;
+    cfg.density = rho;
+    cfg.dt = dt;
+    cfg.t_end = t_end;
+    cfg.dp_max = dp_max;
+    return cfg;
+}
+
+// matrix handle + rhs of assemble_stokes(StokesBox{n,n,h}, ..., &v_gamma)
+int ref_stokes_new(int n, double permeability, double alpha_bj, double nu, double rho, double dt, double t_end,
+                   double dp_max, double t, const double* v_prev, const double* v_gamma, void** mat_out,
+                   double* rhs_out) {
+    return guarded([&] {
+        const ScenarioConfig cfg = scenario_of(n, permeability, alpha_bj, nu, rho, dt, t_end, dp_max);
+        const StokesBox box{n, n, 1.0 / n};
+        StokesBcs bcs;
+        bcs.left = StokesSideBc::pressure_bc(cfg.inflow_pressure(t));
+        bcs.right = StokesSideBc::pressure_bc(0.0);
+        bcs.top = StokesSideBc::wall();
+        std::vector<double> vp;
+        if (v_prev) vp.assign(v_prev, v_prev + box.n_vel());
+        std::vector<double> vg(v_gamma, v_gamma + n);
+        auto sys = assemble_stokes(box, FlowParams::from(cfg), vp, bcs, &vg);
+        std::memcpy(rhs_out, sys.rhs.data(), sizeof(double) * sys.rhs.size());
+        *mat_out = new MatrixHandle{std::move(sys.matrix)};
+    });
+}
+
+// matrix handle + rhs of assemble_darcy(DarcyBox{n,n,h}, K/mu, {}, &p_gamma)
+int ref_darcy_new(int n, double k_over_mu, const double* p_gamma, void** mat_out, double* rhs_out) {
+    return guarded([&] {
+        const DarcyBox box{n, n, 1.0 / n};
+        std::vector<double> pg(p_gamma, p_gamma + n);
+        auto sys = assemble_darcy(box, k_over_mu, DarcyBcs{}, &pg);
+        std::memcpy(rhs_out, sys.rhs.data(), sizeof(double) * sys.rhs.size());
+        *mat_out = new MatrixHandle{std::move(sys.matrix)};
+    });
+}
+
+int ref_stokes_pressure_trace(int n, double mu, const double* solution, double* trace) {
+    return guarded([&] {
+        const StokesBox box{n, n, 1.0 / n};
+        auto tr = stokes_pressure_trace(box, mu, std::span<const double>(solution, box.n_total()));
+        std::memcpy(trace, tr.data(), sizeof(double) * tr.size());
+    });
+}
+
+int ref_darcy_velocity_trace(int n, double k_over_mu, const double* p, const double* p_gamma, double* trace) {
+    return guarded([&] {
+        const DarcyBox box{n, n, 1.0 / n};
+        auto tr = darcy_velocity_trace_dirichlet(box, k_over_mu, std::span<const double>(p, box.n_p()),
+                                                 std::span<const double>(p_gamma, n));
+        std::memcpy(trace, tr.data(), sizeof(double) * tr.size());
+    });
+}
+
+// UzawaPreconditioner(v, b, c, cfg) on a Stokes matrix (the CouplingDriver's
+// Stokes-side preconditioner, coupling.cpp:115-138) and AmgPreconditioner on a
+// Darcy matrix (coupling.cpp:140-146), as opaque handles usable with
+// ref_pd_gmres / ref_bicgstab (precond kinds 3 and 4).
+int ref_uzawa_stokes_new(void* mat, int n, int max_levels, void** out) {
+    return guarded([&] {
+        const SparseMatrix& a = static_cast<MatrixHandle*>(mat)->a;
+        const StokesBox box{n, n, 1.0 / n};
+        const int n_vel = box.n_vel(), nt = box.n_total();
+        UzawaConfig ucfg;
+        ucfg.mode = UzawaConfig::Mode::inexact;
+        ucfg.amg.max_levels = max_levels;
+        ucfg.amg.components.assign(n_vel, 0);
+        for (int k = box.n_u(); k < n_vel; ++k) ucfg.amg.components[k] = 1;
+        *out = new PrecondHandle{std::make_shared<UzawaPreconditioner>(
+            submatrix(a, 0, n_vel, 0, n_vel), submatrix(a, 0, n_vel, n_vel, nt), submatrix(a, n_vel, nt, 0, n_vel),
+            ucfg)};
+    });
+}
+
+int ref_amg_precond_new(void* mat, int max_levels, void** out) {
+    return guarded([&] {
+        AmgOptions o;
+        o.max_levels = max_levels;
+        *out = new PrecondHandle{std::make_shared<AmgPreconditioner>(static_cast<MatrixHandle*>(mat)->a, o)};
+    });
+}
+
+void ref_precond_free(void* p) { delete static_cast<PrecondHandle*>(p); }
+
 
 // Interface traces of a monolithic solution (assembly.cpp:382-428).
 int ref_system_traces(void* hs, const double* x, double* p_ff_gamma, double* v_pm_gamma) {
@@ -428,6 +530,7 @@ int ref_pd_gmres(void* mat, int precond_kind, void* precond, const double* b, do
             hp = std::make_unique<HierPrecond>(&static_cast<HierHandle*>(precond)->h);
             p = hp.get();
         }
+        if (precond_kind == 3) p = static_cast<PrecondHandle*>(precond)->p.get();
         auto res = pd_gmres(LinearOperator::from_matrix(a), p,
                             std::span<const double>(b, a.n_rows), tol_abs, max_restarts, c);
         std::memcpy(x, res.x.data(), sizeof(double) * res.x.size());
@@ -447,6 +550,7 @@ int ref_bicgstab(void* mat, int precond_kind, void* precond, const double* b, do
             hp = std::make_unique<HierPrecond>(&static_cast<HierHandle*>(precond)->h);
             p = hp.get();
         }
+        if (precond_kind == 3) p = static_cast<PrecondHandle*>(precond)->p.get();
         auto res = bicgstab(LinearOperator::from_matrix(a), p,
                             std::span<const double>(b, a.n_rows), tol_abs, max_iters);
         std::memcpy(x, res.x.data(), sizeof(double) * res.x.size());

@@ -131,6 +131,13 @@ class RefLib:
         p("ref_matrix_sizes", None, [_vp, C.POINTER(_i), C.POINTER(_i), C.POINTER(C.c_longlong)])
         p("ref_matrix_copy", None, [_vp, _ip, _ip, _dp])
         p("ref_matrix_free", None, [_vp])
+        p("ref_stokes_new", _i, [_i, _d, _d, _d, _d, _d, _d, _d, _d, _vp, _dp, C.POINTER(_vp), _dp])
+        p("ref_darcy_new", _i, [_i, _d, _dp, C.POINTER(_vp), _dp])
+        p("ref_stokes_pressure_trace", _i, [_i, _d, _dp, _dp])
+        p("ref_darcy_velocity_trace", _i, [_i, _d, _dp, _dp, _dp])
+        p("ref_uzawa_stokes_new", _i, [_vp, _i, _i, C.POINTER(_vp)])
+        p("ref_amg_precond_new", _i, [_vp, _i, C.POINTER(_vp)])
+        p("ref_precond_free", None, [_vp])
         p("ref_ground_dof", _i, [_vp, _i, C.POINTER(_vp)])
         p("ref_amg_setup", _i, [_vp, _i, _d, _i, _vp, C.POINTER(_vp)])
         p("ref_hier_num_levels", _i, [_vp])
@@ -228,6 +235,54 @@ class RefLib:
     def matrix(self, a: Csr) -> "RefMatrix":
         return RefMatrix(self, a)
 
+    # -- partitioned pieces (coupling.cpp:218-242) --------------------------
+    def stokes(self, n, permeability=1.0, alpha_bj=1.0, nu=1.0, rho=1.0, dt=float("inf"), t_end=1.0, dp_max=1.0,
+               t=None, v_prev=None, v_gamma=None):
+        """Reference assemble_stokes on the n x n box with Dirichlet interface velocities v_gamma."""
+        t = t_end if t is None else t
+        nt = 2 * n * (n + 1) + n * n
+        rhs = np.empty(nt)
+        h = _vp()
+        vp = None if v_prev is None else _f64(v_prev).ctypes.data_as(_vp)
+        self._check(self.L.ref_stokes_new(n, permeability, alpha_bj, nu, rho, dt, t_end, dp_max, t, vp,
+                                          _f64(v_gamma), C.byref(h), rhs))
+        try:
+            return self._matrix_copy(h), rhs
+        finally:
+            self.L.ref_matrix_free(h)
+
+    def darcy(self, n, k_over_mu, p_gamma):
+        """Reference assemble_darcy on the n x n box with Dirichlet interface pressures p_gamma."""
+        rhs = np.empty(n * n)
+        h = _vp()
+        self._check(self.L.ref_darcy_new(n, k_over_mu, _f64(p_gamma), C.byref(h), rhs))
+        try:
+            return self._matrix_copy(h), rhs
+        finally:
+            self.L.ref_matrix_free(h)
+
+    def stokes_pressure_trace(self, n, mu, x):
+        out = np.empty(n)
+        self._check(self.L.ref_stokes_pressure_trace(n, mu, _f64(x), out))
+        return out
+
+    def darcy_velocity_trace(self, n, k_over_mu, p, p_gamma):
+        out = np.empty(n)
+        self._check(self.L.ref_darcy_velocity_trace(n, k_over_mu, _f64(p), _f64(p_gamma), out))
+        return out
+
+    def uzawa_stokes(self, a: Csr, n, max_levels=3) -> "RefPrecond":
+        with self.matrix(a) as m:
+            h = _vp()
+            self._check(self.L.ref_uzawa_stokes_new(m.h, n, max_levels, C.byref(h)))
+            return RefPrecond(self, h)
+
+    def amg_precond(self, a: Csr, max_levels=3) -> "RefPrecond":
+        with self.matrix(a) as m:
+            h = _vp()
+            self._check(self.L.ref_amg_precond_new(m.h, max_levels, C.byref(h)))
+            return RefPrecond(self, h)
+
     def ground_dof(self, a: Csr, dof=0) -> Csr:
         with self.matrix(a) as m:
             h = _vp()
@@ -263,6 +318,8 @@ class RefLib:
             return 1, precond.h
         if isinstance(precond, RefHierarchy):
             return 2, precond.h
+        if isinstance(precond, RefPrecond):
+            return 3, precond.h
         raise TypeError(precond)
 
     def pd_gmres(self, a: Csr, b, tol_abs, max_restarts, precond=None, m_init=3, m_min=3,
@@ -307,6 +364,17 @@ class RefMatrix:
     def __exit__(self, *exc):
         self.lib.L.ref_matrix_free(self.h)
         self.h = None
+
+
+class RefPrecond:
+    """An owned reference Preconditioner (Uzawa on a Stokes matrix, AMG on a Darcy matrix)."""
+
+    def __init__(self, lib: RefLib, h):
+        self.lib, self.h = lib, h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.L.ref_precond_free(self.h)
 
 
 class RefHierarchy:

@@ -506,6 +506,49 @@ int sdg_assemble_monolithic(const sdg_scenario* sc, const double* k_cell, const 
     });
 }
 
+// ---- partitioned subproblems (host) --------------------------------------------
+namespace {
+int copy_system(const sdg::LinearSystem& s, int* n, int64_t* nnz, int* rowptr, int* col, double* val, double* rhs) {
+    if (n) *n = s.a.n_rows;
+    if (nnz) *nnz = s.a.nnz();
+    if (rowptr) std::memcpy(rowptr, s.a.rp.data(), sizeof(int) * s.a.rp.size());
+    if (col) std::memcpy(col, s.a.ci.data(), sizeof(int) * s.a.ci.size());
+    if (val) std::memcpy(val, s.a.v.data(), sizeof(double) * s.a.v.size());
+    if (rhs) std::memcpy(rhs, s.rhs.data(), sizeof(double) * s.rhs.size());
+    return SDG_OK;
+}
+}  // namespace
+
+int sdg_assemble_stokes(const sdg_scenario* sc, const double* v_prev, const double* v_gamma, int* n,
+                        int64_t* nnz, int* rowptr, int* col, double* val, double* rhs) {
+    return guard([&] {
+        need(sc, "sdg_assemble_stokes");
+        copy_system(sdg::assemble_stokes_dirichlet(*sc, v_prev, v_gamma), n, nnz, rowptr, col, val, rhs);
+    });
+}
+
+int sdg_assemble_darcy(const sdg_scenario* sc, const double* p_gamma, int* n, int64_t* nnz, int* rowptr, int* col,
+                       double* val, double* rhs) {
+    return guard([&] {
+        need(sc, "sdg_assemble_darcy");
+        copy_system(sdg::assemble_darcy_dirichlet(*sc, p_gamma), n, nnz, rowptr, col, val, rhs);
+    });
+}
+
+int sdg_stokes_pressure_trace(const sdg_scenario* sc, const double* x_ff, double* trace) {
+    return guard([&] {
+        need(sc, "sdg_stokes_pressure_trace");
+        sdg::stokes_pressure_trace(*sc, x_ff, trace);
+    });
+}
+
+int sdg_darcy_velocity_trace(const sdg_scenario* sc, const double* p, const double* p_gamma, double* trace) {
+    return guard([&] {
+        need(sc, "sdg_darcy_velocity_trace");
+        sdg::darcy_velocity_trace(*sc, p, p_gamma, trace);
+    });
+}
+
 // ---- host hierarchy inspection ---------------------------------------------------
 int sdg_host_hierarchy_build(int n, const int* rowptr, const int* col, const double* val,
                              const sdg_amg_options* opts, sdg_host_hierarchy** out) {

@@ -445,4 +445,73 @@ Assembled assemble_monolithic(const sdg_scenario& sc, const double* k_cell, cons
     return out;
 }
 
+// ---------------------------------------------------------------------------
+// Partitioned subproblems (see setup.hpp).
+
+LinearSystem assemble_stokes_dirichlet(const sdg_scenario& sc, const double* v_prev, const double* v_gamma) {
+    if (!v_gamma) fail(SDG_EDIM, "assemble_stokes: interface data length mismatch");
+    const Assembled m = assemble_monolithic(sc, nullptr, v_prev);
+    const int n = sc.n, n_ff = m.n_vel + m.n_pff;
+    LinearSystem s;
+    s.a = HostCsr(n_ff, n_ff);
+    s.rhs.assign(m.rhs.begin(), m.rhs.begin() + n_ff);
+    for (int r = 0; r < n_ff; ++r) {
+        const int vi = r - m.n_u;
+        if (vi >= 0 && vi < n) {  // v(i, 0): Dirichlet row (assembly.cpp:137-141)
+            s.a.ci.push_back(r);
+            s.a.v.push_back(1.0);
+            s.rhs[r] = v_gamma[vi];
+        } else {
+            for (int k = m.a.rp[r]; k < m.a.rp[r + 1]; ++k) {
+                if (m.a.ci[k] >= n_ff) fail(SDG_EINVAL, "assemble_stokes: unexpected coupling column");
+                s.a.ci.push_back(m.a.ci[k]);
+                s.a.v.push_back(m.a.v[k]);
+            }
+        }
+        s.a.rp[r + 1] = static_cast<int>(s.a.ci.size());
+    }
+    return s;
+}
+
+LinearSystem assemble_darcy_dirichlet(const sdg_scenario& sc, const double* p_gamma) {
+    if (!p_gamma) fail(SDG_EDIM, "assemble_darcy: interface data length mismatch");
+    const Assembled m = assemble_monolithic(sc, nullptr, nullptr);
+    const int n = sc.n, n_ff = m.n_vel + m.n_pff, np_ = m.n_ppm;
+    const double t2 = 2.0 * (sc.permeability / (sc.nu * sc.rho));
+    LinearSystem s;
+    s.a = HostCsr(np_, np_);
+    s.rhs.assign(np_, 0.0);
+    for (int r = 0; r < np_; ++r) {
+        const int g = n_ff + r;
+        const bool top = r >= (n - 1) * n;
+        for (int k = m.a.rp[g]; k < m.a.rp[g + 1]; ++k) {
+            const int c = m.a.ci[k];
+            if (c < n_ff) continue;  // the coupled top face becomes Dirichlet
+            double v = m.a.v[k];
+            if (top && c == g) v += t2;  // diag accumulated W, E, S, then the top face
+            s.a.ci.push_back(c - n_ff);
+            s.a.v.push_back(v);
+        }
+        if (top) s.rhs[r] += t2 * p_gamma[r - (n - 1) * n];
+        s.a.rp[r + 1] = static_cast<int>(s.a.ci.size());
+    }
+    return s;
+}
+
+void stokes_pressure_trace(const sdg_scenario& sc, const double* x, double* trace) {
+    const int n = sc.n;
+    const double h = 1.0 / n, mu = sc.nu * sc.rho;
+    const int n_u = (n + 1) * n, n_vel = 2 * n * (n + 1);
+    for (int i = 0; i < n; ++i) {
+        const double dvdy = (x[n_u + n + i] - x[n_u + i]) / h;
+        trace[i] = x[n_vel + i] - 2.0 * mu * dvdy;
+    }
+}
+
+void darcy_velocity_trace(const sdg_scenario& sc, const double* p, const double* p_gamma, double* trace) {
+    const int n = sc.n;
+    const double h = 1.0 / n, k_over_mu = sc.permeability / (sc.nu * sc.rho);
+    for (int i = 0; i < n; ++i) trace[i] = 2.0 * k_over_mu * (p[(n - 1) * n + i] - p_gamma[i]) / h;
+}
+
 }  // namespace sdg

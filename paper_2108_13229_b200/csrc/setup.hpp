@@ -68,4 +68,20 @@ struct Assembled {
 };
 Assembled assemble_monolithic(const sdg_scenario& sc, const double* k_cell, const double* v_prev);
 
+// The partitioned subproblems (coupling.cpp:218-242) on the same boxes:
+// assemble_stokes(ff box, ..., &v_gamma) -- Dirichlet normal velocities on the
+// interface, slip for the tangential ones (assembly.cpp:134-141, 115-130) --
+// and assemble_darcy(pm box, K/mu, {}, &p_gamma) -- Dirichlet interface
+// pressures (assembly.cpp:268-270).  Derived from the monolithic rows, which
+// they share everywhere else, so uniform-K results are bitwise the reference's.
+struct LinearSystem {
+    HostCsr a;
+    std::vector<double> rhs;
+};
+LinearSystem assemble_stokes_dirichlet(const sdg_scenario& sc, const double* v_prev, const double* v_gamma);
+LinearSystem assemble_darcy_dirichlet(const sdg_scenario& sc, const double* p_gamma);
+// stokes_pressure_trace (assembly.cpp:382-391) / darcy_velocity_trace_dirichlet (:393-402)
+void stokes_pressure_trace(const sdg_scenario& sc, const double* x_ff, double* trace);
+void darcy_velocity_trace(const sdg_scenario& sc, const double* p, const double* p_gamma, double* trace);
+
 }  // namespace sdg

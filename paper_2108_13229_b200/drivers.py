@@ -96,3 +96,137 @@ class TransientDriver:
         for k in range(1, (steps or self.cfg.steps) + 1):
             self.advance(k * self.cfg.dt)
         return self.history
+
+
+@dataclass
+class CouplingResult:
+    converged: bool
+    coupling_iterations: int
+    inner_iterations: int
+    measure_p: List[float]
+    measure_v: List[float]
+    stokes_iterations: List[int]
+    darcy_iterations: List[int]
+    solution: Optional[np.ndarray]
+    seconds: float
+    solve_seconds: float
+
+
+@dataclass
+class PartitionedDriver:
+    """CouplingDriver::coupled_timestep (coupling.cpp:252-332) for BASELINE
+    config 5: Dirichlet-Neumann alternation of the free-flow problem
+    (assemble_stokes with Dirichlet interface velocities, solved by PD-GMRES +
+    inexact Uzawa(AMG_V), coupling.cpp:115-138,199-203,218-229) and the porous
+    problem (assemble_darcy with Dirichlet interface pressures, BiCGSTAB +
+    AMG, coupling.cpp:140-146,204-206,231-242), with the reference's interface
+    update: relaxation 0.5 on the first iteration, then IQN-ILS
+    (coupling.cpp:45-101, :309-314) -- or, with ``acceleration="relaxation"``,
+    the constant under-relaxation ``v += relaxation * R`` every iteration.
+    Convergence: both relative interface measures below epsilon
+    (coupling.cpp:284-296).  The two matrices do not depend on the interface
+    data (only the right-hand sides do), so both preconditioners are built
+    once, as the reference's caches do.  Inner stop rule ``inner_tol_rel *
+    ||b||`` (the reference's ``10 x direct residual`` needs banded LUs,
+    SURVEY.md §8(d))."""
+
+    cfg: sdc.ScenarioConfig
+    levels: int = 3
+    acceleration: str = "iqn_ils"
+    relaxation: float = 0.5
+    epsilon: float = 1e-8
+    zero_guard: float = 1e-14
+    max_coupling_iterations: int = 100
+    history_capacity: int = 50
+    filter_tolerance: float = 1e-13
+    inner_tol_rel: float = 1e-10
+    ctx: Optional[sdc.Context] = None
+
+    def __post_init__(self):
+        self.ctx = self.ctx or sdc.default_context()
+        n = self.cfg.cells_per_unit_square
+        self.n = n
+        self.mu = self.cfg.kinematic_viscosity * self.cfg.density
+        z = np.zeros(n)
+        self.stokes_matrix, _ = sdc.assemble_stokes(self.cfg, z)
+        self.darcy_matrix, _ = sdc.assemble_darcy(self.cfg, z)
+        n_u = n * (n + 1)
+        n_vel = 2 * n_u
+        nt = self.stokes_matrix.n_rows
+        a = self.stokes_matrix
+        comps = [0] * n_u + [1] * n_u
+        ucfg = sdc.UzawaConfig(amg=sdc.AmgOptions(max_levels=self.levels, components=comps))
+        self.stokes_pre = sdc.UzawaPreconditioner(sdc.submatrix(a, 0, n_vel, 0, n_vel),
+                                                  sdc.submatrix(a, 0, n_vel, n_vel, nt),
+                                                  sdc.submatrix(a, n_vel, nt, 0, n_vel), ucfg, ctx=self.ctx)
+        self.darcy_pre = sdc.AmgPreconditioner(self.darcy_matrix, sdc.AmgOptions(max_levels=self.levels),
+                                               ctx=self.ctx)
+        self.trace_v = np.zeros(n)
+        self.trace_p = np.zeros(n)
+
+    def solve_ff(self, v_gamma):
+        _, b = sdc.assemble_stokes(self.cfg, v_gamma)
+        res = sdc.pd_gmres(self.stokes_matrix, self.stokes_pre, b, self.inner_tol_rel * float(np.linalg.norm(b)),
+                           400, sdc.RestartController.defaults())
+        if not res.report.converged:
+            raise RuntimeError(f"coupling: inner free-flow solve did not converge, final residual "
+                               f"{res.report.final_residual} after {res.report.iterations} iterations")
+        return res, sdc.stokes_pressure_trace(self.cfg, res.x)
+
+    def solve_pm(self, p_gamma):
+        _, b = sdc.assemble_darcy(self.cfg, p_gamma)
+        res = sdc.bicgstab(self.darcy_matrix, self.darcy_pre, b, self.inner_tol_rel * float(np.linalg.norm(b)),
+                           10000)
+        if not res.report.converged:
+            raise RuntimeError(f"coupling: inner porous solve did not converge, final residual "
+                               f"{res.report.final_residual} after {res.report.iterations} iterations")
+        return res, sdc.darcy_velocity_trace(self.cfg, res.x, p_gamma)
+
+    def coupled_step(self) -> CouplingResult:
+        import time
+        from .iqn import IqnIlsHistory, iqn_ils_update
+        t0 = time.perf_counter()
+        solve_s = 0.0
+        v_k, p_k = self.trace_v.copy(), self.trace_p.copy()
+        hist = IqnIlsHistory(self.history_capacity, self.filter_tolerance)
+        out = CouplingResult(False, 0, 0, [], [], [], [], None, 0.0, 0.0)
+
+        def measure(nxt, prev):
+            return float(np.linalg.norm(nxt - prev)), float(np.linalg.norm(nxt))
+
+        for k in range(self.max_coupling_iterations):
+            s0 = time.perf_counter()
+            ff, p_tr = self.solve_ff(v_k)
+            pm, v_tr = self.solve_pm(p_tr)
+            solve_s += time.perf_counter() - s0
+            out.coupling_iterations += 1
+            out.stokes_iterations.append(ff.report.iterations)
+            out.darcy_iterations.append(pm.report.iterations)
+            out.inner_iterations += ff.report.iterations + pm.report.iterations
+            dp, np_ = measure(p_tr, p_k)
+            dv, nv = measure(v_tr, v_k)
+            out.measure_p.append(dp)
+            out.measure_v.append(dv)
+            zg = self.zero_guard
+            ok_p = dp < zg if np_ < zg else dp < self.epsilon * np_
+            ok_v = dv < zg if nv < zg else dv < self.epsilon * nv
+            if ok_p and ok_v or k + 1 == self.max_coupling_iterations:
+                out.converged = bool(ok_p and ok_v)
+                out.solution = np.concatenate([ff.x, pm.x])
+                if out.converged:
+                    self.trace_v, self.trace_p = v_tr, p_tr
+                break
+            residual = v_tr - v_k
+            if self.acceleration == "picard":
+                v_next = v_tr
+            elif self.acceleration == "relaxation":
+                v_next = v_k + self.relaxation * residual
+            elif not hist.has_previous():
+                v_next = v_k + self.relaxation * residual
+                hist.record(residual, v_tr)
+            else:
+                v_next = iqn_ils_update(hist, v_k, residual, v_tr)
+            p_k, v_k = p_tr, v_next
+        out.seconds = time.perf_counter() - t0
+        out.solve_seconds = solve_s
+        return out

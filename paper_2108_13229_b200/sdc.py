@@ -156,6 +156,10 @@ def lib():
         p("sdg_power_iteration", _i, [_vp, _d, _i, C.c_uint, P(_d), P(_i), P(_i)])
         p("sdg_assemble_monolithic", _i, [P(_Scenario), _vp, _vp, P(_i), P(_i64), P(_i), P(_i), P(_i),
                                           P(_i), _vp, _vp, _vp, _vp])
+        p("sdg_assemble_stokes", _i, [P(_Scenario), _vp, _vp, P(_i), P(_i64), _vp, _vp, _vp, _vp])
+        p("sdg_assemble_darcy", _i, [P(_Scenario), _vp, P(_i), P(_i64), _vp, _vp, _vp, _vp])
+        p("sdg_stokes_pressure_trace", _i, [P(_Scenario), _dp, _dp])
+        p("sdg_darcy_velocity_trace", _i, [P(_Scenario), _dp, _dp, _dp])
         p("sdg_host_hierarchy_build", _i, [_i, _ip, _ip, _dp, P(_AmgOpts), P(_vp)])
         p("sdg_host_hierarchy_levels", _i, [_vp])
         p("sdg_host_hierarchy_level", _i, [_vp, _i, P(_i), P(_i64), P(_i), P(_i), _vp, _vp, _vp, _vp])
@@ -862,6 +866,60 @@ def assemble_monolithic(cfg: ScenarioConfig, t: Optional[float] = None, v_prev=N
                                      rhs.ctypes.data_as(_vp)))
     return CoupledSystem(SparseMatrix(N.value, N.value, rp, ci, vv), rhs, n, nu.value, nv.value, npf.value,
                          npm.value)
+
+
+def _scenario_c(cfg: "ScenarioConfig", t: Optional[float]) -> _Scenario:
+    return _Scenario(cfg.cells_per_unit_square, cfg.permeability, cfg.alpha_bj, cfg.kinematic_viscosity,
+                     cfg.density, cfg.dt, cfg.t_end, cfg.dp_max, cfg.t_end if t is None else t)
+
+
+def _two_phase(call):
+    n, nnz = _i(), _i64()
+    _check(call(C.byref(n), C.byref(nnz), None, None, None, None))
+    rp = np.empty(n.value + 1, np.int32)
+    ci = np.empty(nnz.value, np.int32)
+    vv = np.empty(nnz.value, np.float64)
+    rhs = np.empty(n.value, np.float64)
+    _check(call(None, None, rp.ctypes.data_as(_vp), ci.ctypes.data_as(_vp), vv.ctypes.data_as(_vp),
+                rhs.ctypes.data_as(_vp)))
+    return SparseMatrix(n.value, n.value, rp, ci, vv), rhs
+
+
+def assemble_stokes(cfg: "ScenarioConfig", v_gamma, t: Optional[float] = None, v_prev=None):
+    """assemble_stokes (assembly.cpp:287-303) on the n x n free-flow box with
+    Dirichlet interface velocities v_gamma (the partitioned driver's free-flow
+    problem, coupling.cpp:218-229).  Returns (matrix, rhs)."""
+    sc = _scenario_c(cfg, t)
+    vg = _f64(v_gamma)
+    if vg.size != cfg.cells_per_unit_square:
+        raise ValueError("assemble_stokes: interface data length mismatch")
+    vp = None if v_prev is None else _f64(v_prev)
+    vpp = None if vp is None else vp.ctypes.data_as(_vp)
+    return _two_phase(lambda n, nnz, rp, ci, vv, rhs: lib().sdg_assemble_stokes(
+        C.byref(sc), vpp, vg.ctypes.data_as(_vp), n, nnz, rp, ci, vv, rhs))
+
+
+def assemble_darcy(cfg: "ScenarioConfig", p_gamma):
+    """assemble_darcy (assembly.cpp:305-325) on the n x n porous box with
+    Dirichlet interface pressures p_gamma (coupling.cpp:231-242)."""
+    sc = _scenario_c(cfg, None)
+    pg = _f64(p_gamma)
+    if pg.size != cfg.cells_per_unit_square:
+        raise ValueError("assemble_darcy: interface data length mismatch")
+    return _two_phase(lambda n, nnz, rp, ci, vv, rhs: lib().sdg_assemble_darcy(
+        C.byref(sc), pg.ctypes.data_as(_vp), n, nnz, rp, ci, vv, rhs))
+
+
+def stokes_pressure_trace(cfg: "ScenarioConfig", x_ff) -> np.ndarray:
+    out = np.empty(cfg.cells_per_unit_square)
+    _check(lib().sdg_stokes_pressure_trace(C.byref(_scenario_c(cfg, None)), _f64(x_ff), out))
+    return out
+
+
+def darcy_velocity_trace(cfg: "ScenarioConfig", p, p_gamma) -> np.ndarray:
+    out = np.empty(cfg.cells_per_unit_square)
+    _check(lib().sdg_darcy_velocity_trace(C.byref(_scenario_c(cfg, None)), _f64(p), _f64(p_gamma), out))
+    return out
 
 
 # ---------------------------------------------------------------------------

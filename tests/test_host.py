@@ -146,3 +146,27 @@ def test_coo_builder_semantics():
     assert m.col_indices.tolist() == [0, 1, 1]
     assert m.values.tolist() == [5.0, 1.0, 5.0]
     assert m.at(1, 1) == 5.0 and m.at(1, 0) == 0.0
+
+
+@pytest.mark.parametrize("n,k", [(6, 1.0), (16, 1e-2), (50, 1.0)])
+def test_partitioned_subproblems_bitwise(ref, n, k):
+    """assemble_stokes / assemble_darcy with interface data and the two traces
+    (coupling.cpp:218-242, assembly.cpp:287-325,382-402): bitwise the reference."""
+    from paper_2108_13229_b200 import sdc
+    cfg = sdc.ScenarioConfig(cells_per_unit_square=n, permeability=k, alpha_bj=1.0, kinematic_viscosity=1.0,
+                             density=1.0, dt=float("inf"), t_end=1.0, dp_max=1.0)
+    rng = np.random.default_rng(n)
+    vg, pg = rng.standard_normal(n), rng.standard_normal(n)
+    a, b = sdc.assemble_stokes(cfg, vg)
+    ar, br = ref.stokes(n, permeability=k, v_gamma=vg)
+    assert np.array_equal(a.row_offsets, ar.rowptr) and np.array_equal(a.col_indices, ar.col)
+    assert np.array_equal(a.values, ar.val) and np.array_equal(b, br)
+    d, db = sdc.assemble_darcy(cfg, pg)
+    dr, dbr = ref.darcy(n, k, pg)
+    assert np.array_equal(d.row_offsets, dr.rowptr) and np.array_equal(d.col_indices, dr.col)
+    assert np.array_equal(d.values, dr.val) and np.array_equal(db, dbr)
+    x, p = rng.standard_normal(a.n_rows), rng.standard_normal(d.n_rows)
+    assert np.array_equal(sdc.stokes_pressure_trace(cfg, x), ref.stokes_pressure_trace(n, 1.0, x))
+    assert np.array_equal(sdc.darcy_velocity_trace(cfg, p, pg), ref.darcy_velocity_trace(n, k, p, pg))
+    with pytest.raises(ValueError):
+        sdc.assemble_stokes(cfg, vg[:-1])
