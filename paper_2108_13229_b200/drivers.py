@@ -141,6 +141,7 @@ class PartitionedDriver:
     filter_tolerance: float = 1e-13
     inner_tol_rel: float = 1e-10
     ctx: Optional[sdc.Context] = None
+    log: Optional[object] = None  # callable(k, stokes_its, darcy_its, dp_rel, dv_rel, seconds)
 
     def __post_init__(self):
         self.ctx = self.ctx or sdc.default_context()
@@ -148,8 +149,13 @@ class PartitionedDriver:
         self.n = n
         self.mu = self.cfg.kinematic_viscosity * self.cfg.density
         z = np.zeros(n)
-        self.stokes_matrix, _ = sdc.assemble_stokes(self.cfg, z)
+        # the interface data enter only the right-hand sides: assemble once,
+        # then write v_gamma into the Dirichlet rows (assembly.cpp:137-141) and
+        # 2 (K/mu) p_gamma into the top Darcy rows (:268-270) per iteration --
+        # exactly the values a re-assembly produces (tests/test_gpu_partitioned.py)
+        self.stokes_matrix, self.stokes_rhs0 = sdc.assemble_stokes(self.cfg, z)
         self.darcy_matrix, _ = sdc.assemble_darcy(self.cfg, z)
+        self.t2 = 2.0 * (self.cfg.permeability / self.mu)
         n_u = n * (n + 1)
         n_vel = 2 * n_u
         nt = self.stokes_matrix.n_rows
@@ -164,8 +170,19 @@ class PartitionedDriver:
         self.trace_v = np.zeros(n)
         self.trace_p = np.zeros(n)
 
+    def stokes_rhs(self, v_gamma) -> np.ndarray:
+        b = self.stokes_rhs0.copy()
+        n_u = self.n * (self.n + 1)
+        b[n_u:n_u + self.n] = v_gamma
+        return b
+
+    def darcy_rhs(self, p_gamma) -> np.ndarray:
+        b = np.zeros(self.darcy_matrix.n_rows)
+        b[(self.n - 1) * self.n:] = self.t2 * np.asarray(p_gamma, dtype=np.float64)
+        return b
+
     def solve_ff(self, v_gamma):
-        _, b = sdc.assemble_stokes(self.cfg, v_gamma)
+        b = self.stokes_rhs(v_gamma)
         res = sdc.pd_gmres(self.stokes_matrix, self.stokes_pre, b, self.inner_tol_rel * float(np.linalg.norm(b)),
                            400, sdc.RestartController.defaults())
         if not res.report.converged:
@@ -174,7 +191,7 @@ class PartitionedDriver:
         return res, sdc.stokes_pressure_trace(self.cfg, res.x)
 
     def solve_pm(self, p_gamma):
-        _, b = sdc.assemble_darcy(self.cfg, p_gamma)
+        b = self.darcy_rhs(p_gamma)
         res = sdc.bicgstab(self.darcy_matrix, self.darcy_pre, b, self.inner_tol_rel * float(np.linalg.norm(b)),
                            10000)
         if not res.report.converged:
@@ -207,6 +224,9 @@ class PartitionedDriver:
             dv, nv = measure(v_tr, v_k)
             out.measure_p.append(dp)
             out.measure_v.append(dv)
+            if self.log:
+                self.log(k, ff.report.iterations, pm.report.iterations, dp / max(np_, 1e-300), dv / max(nv, 1e-300),
+                         time.perf_counter() - t0)
             zg = self.zero_guard
             ok_p = dp < zg if np_ < zg else dp < self.epsilon * np_
             ok_v = dv < zg if nv < zg else dv < self.epsilon * nv

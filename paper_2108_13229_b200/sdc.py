@@ -365,19 +365,21 @@ def spmv_add(a: SparseMatrix, x, y, alpha: float = 1.0) -> np.ndarray:
 
 
 def submatrix(a: SparseMatrix, row_begin, row_end, col_begin, col_end) -> SparseMatrix:
-    """sparse.cpp:110-127 (host helper)."""
+    """sparse.cpp:110-127 (host helper): rows [row_begin, row_end), columns
+    [col_begin, col_end), entries kept in their row order."""
     if row_begin < 0 or row_end > a.n_rows or col_begin < 0 or col_end > a.n_cols or row_begin > row_end \
             or col_begin > col_end:
         raise ValueError("submatrix: bad range")
-    rp, ci, vv = [0], [], []
-    for i in range(row_begin, row_end):
-        s, e = a.row_offsets[i], a.row_offsets[i + 1]
-        cols = a.col_indices[s:e]
-        m = (cols >= col_begin) & (cols < col_end)
-        ci.extend((cols[m] - col_begin).tolist())
-        vv.extend(a.values[s:e][m].tolist())
-        rp.append(len(ci))
-    return SparseMatrix(row_end - row_begin, col_end - col_begin, rp, ci, vv)
+    nr = row_end - row_begin
+    lo, hi = int(a.row_offsets[row_begin]), int(a.row_offsets[row_end])
+    cols = a.col_indices[lo:hi]
+    vals = a.values[lo:hi]
+    counts = np.diff(a.row_offsets[row_begin:row_end + 1])
+    row_id = np.repeat(np.arange(nr), counts)
+    m = (cols >= col_begin) & (cols < col_end)
+    rp = np.zeros(nr + 1, np.int64)
+    rp[1:] = np.cumsum(np.bincount(row_id[m], minlength=nr))
+    return SparseMatrix(nr, col_end - col_begin, rp, cols[m] - col_begin, vals[m])
 
 
 def ground_dof(a: SparseMatrix, dof: int = 0) -> SparseMatrix:

@@ -59,6 +59,15 @@ def test_partitioned_matches_reference_loop(ref, n, k):
     assert np.linalg.norm(drv.trace_v - v_ref) / np.linalg.norm(v_ref) <= 1e-6
 
 
+def test_rhs_patch_equals_reassembly():
+    cfg = _cfg(16, 1e-2)
+    drv = drivers.PartitionedDriver(cfg)
+    rng = np.random.default_rng(5)
+    vg, pg = rng.standard_normal(16), rng.standard_normal(16)
+    assert np.array_equal(drv.stokes_rhs(vg), sdc.assemble_stokes(cfg, vg)[1])
+    assert np.array_equal(drv.darcy_rhs(pg), sdc.assemble_darcy(cfg, pg)[1])
+
+
 def test_partitioned_agrees_with_monolithic_solution():
     """The converged partitioned solution is the monolithic one (same PDE,
     same discretisation): Stokes block and Darcy pressures within the coupling
