@@ -34,7 +34,7 @@ namespace sdg {
 namespace {
 
 constexpr int kU = 4;           // steps per unrolled block (MAC)
-constexpr int k5U = 8;          // steps per unrolled block (5-point)
+constexpr int k5U = 16;         // steps per unrolled block (5-point)
 constexpr int kMaxBands = 8;    // warps of the one-CTA kernel
 
 __device__ __forceinline__ void bar_arrive(uint64_t* bar) {
