@@ -159,3 +159,27 @@ def test_c2u_gmres50_iterations_match_reference(ref):
     assert rr.converged and res.report.converged
     assert within(res.report.iterations, rr.iterations)
     assert rel_l2(res.x, xr) <= X_TOL
+
+
+def test_c3_full_size_matches_reference_fingerprint():
+    """BASELINE config 3 at full size (1,001,000 DoF, GMRES(50), L3) against the
+    reference's own solve, reduced to fingerprints (tests/golden/c3_reference.json,
+    made by tests/golden/make_c3_golden.py: ~10 min of reference CPU time)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "c3_reference.json")
+    g = json.load(open(path))
+    cfg = scenarios.CONFIGS["c3"]
+    s = scenarios.build_system(cfg)
+    assert s.n_total() == g["n_total"]
+    p = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
+    res = sdc.pd_gmres(s.matrix, p, s.rhs, g["tol"], 4000, sdc.RestartController.fixed(50))
+    assert res.report.converged and g["converged"]
+    assert within(res.report.iterations, g["iterations"]), (res.report.iterations, g["iterations"])
+    x = res.x
+    assert abs(np.linalg.norm(x) - g["x_norm"]) <= 1e-6 * g["x_norm"]
+    sample = np.asarray(g["x_sample"])
+    assert np.linalg.norm(x[::g["stride"]] - sample) <= 1e-6 * np.linalg.norm(sample)
+    for seed, ref_dot in zip(g["probe_seeds"], g["probe_dots"]):
+        pv = np.random.default_rng(seed).standard_normal(x.size)
+        assert abs(np.dot(pv, x) - ref_dot) <= 1e-6 * np.linalg.norm(pv) * g["x_norm"]
