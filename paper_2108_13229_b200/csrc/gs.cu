@@ -95,6 +95,40 @@ __global__ void k_gs_prep_post(int n, const int* __restrict__ urp, const int* __
     packed[bidx[i]] = s * dinv[i];
 }
 
+// merged plans (GsPlan::merged): b'_i = sum_q W_iq r_q [- sum_u WU_iu z_old_u].
+// The rows of W and WU are long (group fill), so kGroup lanes share a row
+// and fold their partial sums with shuffles.
+constexpr int kGroup = 8;
+
+__global__ void k_gs_prep_m(int n, const int* __restrict__ wrp, const int* __restrict__ wci,
+                            const double* __restrict__ wv, const int* __restrict__ urp,
+                            const int* __restrict__ uci, const double* __restrict__ uv,
+                            const double* __restrict__ r, const double* __restrict__ z,
+                            const double* __restrict__ zc, const int* __restrict__ agg,
+                            const int* __restrict__ bidx, double* __restrict__ packed) {
+    pdl_begin();
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = t / kGroup, lane = t % kGroup;
+    double s = 0.0;
+    if (i < n) {
+        for (int k = wrp[i] + lane; k < wrp[i + 1]; k += kGroup) s = fma(wv[k], r[wci[k]], s);
+        if (z) {
+            const int e = urp[i + 1];
+            if (zc) {
+                for (int k = urp[i] + lane; k < e; k += kGroup) {
+                    const int j = uci[k];
+                    s = fma(-uv[k], z[j] + zc[agg[j]], s);
+                }
+            } else {
+                for (int k = urp[i] + lane; k < e; k += kGroup) s = fma(-uv[k], z[uci[k]], s);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = kGroup / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, kGroup);
+    if (i < n && lane == 0) packed[bidx[i]] = s;
+}
+
 // ---- the lower solve -------------------------------------------------------
 
 // Load row t of a level segment into registers.  Small records fill the
@@ -351,12 +385,116 @@ int smem_budget() {
     return std::min(kMaxSmem, optin - static_cast<int>(fa.sharedSizeBytes) - 1024);
 }
 
+// ---- level merging ---------------------------------------------------------
+//
+// The walk's cost is per dependency level (a latency chain), so k consecutive
+// levels are merged into one group: with  z_i = bh_i - sum_{j<i} c_ij z_j
+// (bh = (r - U z_old) / d, c_ij = a_ij / d_i), every lower dependency j in
+// the same group is replaced by its own expression, giving
+//   z_i = sum_q T_iq bh_q - sum_{j in earlier groups} G_ij z_j,
+//   T_i = e_i - sum_{j int} c_ij T_j,   G_i = sum_{j ext} c_ij e_j - sum_{j int} c_ij G_j.
+// The walk runs over G (one level per group); the prep computes
+// b'_i = sum_q T_iq bh_q = (W r - WU z_old)_i with W = T D^{-1}, WU = T D^{-1} U.
+// Exact in exact arithmetic (the same lexicographic Gauss-Seidel sweep,
+// precond.cpp:92-108); rounding differs like the rest of the fast smoother.
+struct MergedLower {
+    HostCsr g, w, wu;
+    std::vector<int> nlow;
+    int max_k = 0;
+    int groups = 0;
+};
+
+bool merge_levels(const HostCsr& a, const std::vector<double>& dinv, const HostCsr& up, int k, int cap,
+                  MergedLower& out) {
+    const int n = a.n_rows;
+    std::vector<int> lev(n, 0);
+    for (int i = 0; i < n; ++i) {
+        int d = 0;
+        for (int e = a.rp[i]; e < a.rp[i + 1]; ++e)
+            if (a.ci[e] < i) d = std::max(d, lev[a.ci[e]] + 1);
+        lev[i] = d;
+    }
+    std::vector<int> grp(n);
+    int ng = 0;
+    for (int i = 0; i < n; ++i) {
+        grp[i] = lev[i] / k;
+        ng = std::max(ng, grp[i] + 1);
+    }
+    // sparse accumulators (dense value + marker + touched list)
+    std::vector<double> accT(n, 0.0), accG(n, 0.0);
+    std::vector<int> mkT(n, -1), mkG(n, -1), lT, lG;
+    HostCsr T(n, n), G(n, n);
+    auto addT = [&](int i, int q, double v) {
+        if (mkT[q] != i) { mkT[q] = i; accT[q] = 0.0; lT.push_back(q); }
+        accT[q] += v;
+    };
+    auto addG = [&](int i, int j, double v) {
+        if (mkG[j] != i) { mkG[j] = i; accG[j] = 0.0; lG.push_back(j); }
+        accG[j] += v;
+    };
+    out.nlow.assign(n, 0);
+    out.max_k = 0;
+    for (int i = 0; i < n; ++i) {
+        lT.clear();
+        lG.clear();
+        addT(i, i, 1.0);
+        for (int e = a.rp[i]; e < a.rp[i + 1]; ++e) {
+            const int j = a.ci[e];
+            if (j >= i) continue;
+            const double c = a.v[e] * dinv[i];
+            if (grp[j] < grp[i]) {
+                addG(i, j, c);
+            } else {
+                for (int f = T.rp[j]; f < T.rp[j + 1]; ++f) addT(i, T.ci[f], -c * T.v[f]);
+                for (int f = G.rp[j]; f < G.rp[j + 1]; ++f) addG(i, G.ci[f], -c * G.v[f]);
+            }
+        }
+        if (static_cast<int>(lG.size()) > cap) return false;
+        std::sort(lT.begin(), lT.end());
+        std::sort(lG.begin(), lG.end());
+        for (int q : lT) { T.ci.push_back(q); T.v.push_back(accT[q]); }
+        for (int j : lG) { G.ci.push_back(j); G.v.push_back(accG[j]); }
+        T.rp[i + 1] = static_cast<int>(T.ci.size());
+        G.rp[i + 1] = static_cast<int>(G.ci.size());
+        out.nlow[i] = static_cast<int>(lG.size());
+        out.max_k = std::max(out.max_k, out.nlow[i]);
+    }
+    // W = T D^{-1}, WU = T D^{-1} U
+    HostCsr W(n, n), WU(n, up.n_cols);
+    std::vector<double> accU(std::max(n, up.n_cols), 0.0);
+    std::vector<int> mkU(accU.size(), -1), lU;
+    for (int i = 0; i < n; ++i) {
+        lU.clear();
+        for (int f = T.rp[i]; f < T.rp[i + 1]; ++f) {
+            const int q = T.ci[f];
+            const double wq = T.v[f] * dinv[q];
+            W.ci.push_back(q);
+            W.v.push_back(wq);
+            for (int e = up.rp[q]; e < up.rp[q + 1]; ++e) {
+                const int u = up.ci[e];
+                if (mkU[u] != i) { mkU[u] = i; accU[u] = 0.0; lU.push_back(u); }
+                accU[u] += wq * up.v[e];
+            }
+        }
+        std::sort(lU.begin(), lU.end());
+        for (int u : lU) { WU.ci.push_back(u); WU.v.push_back(accU[u]); }
+        W.rp[i + 1] = static_cast<int>(W.ci.size());
+        WU.rp[i + 1] = static_cast<int>(WU.ci.size());
+    }
+    out.g = std::move(G);
+    out.w = std::move(W);
+    out.wu = std::move(WU);
+    out.groups = ng;
+    return true;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
 // plan
 
-void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t s, int bands_hint) {
+void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t s, int bands_hint,
+                   bool allow_merge) {
     n = a.n_rows;
     std::vector<double> dinv_h(n);
     std::vector<int> nlow(n, 0);
@@ -411,6 +549,46 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     const bool try_pipe = !force_split && pipe_env && pipe_env[0] == '1';  // opt-in
     // 0. the lane chain, when the matrix is a structured finest level
     if (want_walk && build_chain(a, comps, dinv_h, s)) return finish();
+    // 0b. one walk over merged levels: the largest group size k <= 4 whose
+    //     modelled sweep (walk_model_cost, corrected form) is at least 10 %
+    //     cheaper than the plain walk.  The model ranks merged against plain
+    //     walks but not group sizes among themselves (c2 launch lists: the
+    //     Darcy levels gain most at k = 4, the velocity levels not at all once
+    //     the extra prep of a merged coarse level is counted), hence the rule.
+    //     SDG_GS_MERGE=k forces the group size, 1 disables.
+    if (want_walk && allow_merge && !force_split && !try_pipe) {
+        const char* me = std::getenv("SDG_GS_MERGE");
+        const int kforce = me ? std::atoi(me) : 0;
+        if (kforce != 1) {
+            const double base_cost = walk_model_cost(a, nlow, max_k);
+            int best_k = 1;
+            MergedLower bm;
+            const std::vector<int> ks = kforce > 1 ? std::vector<int>{kforce} : std::vector<int>{4, 3, 2};
+            for (int k : ks) {
+                MergedLower m;
+                if (!merge_levels(a, dinv_h, up, k, 16, m)) continue;
+                const double c = walk_model_cost(m.g, m.nlow, m.max_k);
+                if (std::getenv("SDG_DEBUG"))
+                    std::fprintf(stderr, "[sdg gs merge] n=%d k=%d groups=%d max_k=%d cost=%.0f (unmerged %.0f)\n",
+                                 n, k, m.groups, m.max_k, c, base_cost);
+                if ((kforce > 1 && c < 1e300) || c <= 0.9 * base_cost) {
+                    best_k = k;
+                    bm = std::move(m);
+                    break;
+                }
+            }
+            if (best_k > 1) {
+                const std::vector<double> ones(n, 1.0);
+                if (build_walk(bm.g, ones, bm.nlow, bm.max_k, s)) {
+                    merged = true;
+                    merge_k = best_k;
+                    wmat.upload(bm.w, s);
+                    wumat.upload(bm.wu, s);
+                    return finish();
+                }
+            }
+        }
+    }
     // 1. two label blocks walked concurrently on a 2-CTA cluster
     if (want_walk && try_pipe && contiguous && r0.size() == 3 && build_pipe(a, r0, dinv_h, s)) return finish();
     // 2. one walk over the whole matrix
@@ -979,6 +1157,16 @@ bool GsPlan::build_pipe(const HostCsr& a, const std::vector<int>& r0, const std:
     } while (0)
 
 void launch_gs_prep_pre(Context& c, const GsPlan& g, const double* r) {
+    if (g.merged) {
+        ProfScope ps_(c, PF_GSPREP, 12.0 * g.wmat.nnz + 4.0 * (g.n + 1) + 16.0 * g.n);
+        if (g.n == 0) return;
+        launch_k(c, k_gs_prep_m, (g.n * kGroup + 255) / 256, 256, 0, g.n, g.wmat.rp.get(), g.wmat.ci.get(),
+                 g.wmat.v.get(), g.wumat.rp.get(), g.wumat.ci.get(), g.wumat.v.get(), r,
+                 static_cast<const double*>(nullptr), static_cast<const double*>(nullptr),
+                 static_cast<const int*>(nullptr), g.bidx.get(), const_cast<double*>(g.packed.get()));
+        SDG_GS_CHECK();
+        return;
+    }
     ProfScope ps_(c, PF_GSPREP, 24.0 * g.n + 8.0 * g.n);
     if (g.n == 0) return;
     launch_k(c, k_gs_prep_pre, (g.n + 255) / 256, 256, 0, g.n, r, g.dinv.get(), g.bidx.get(),
@@ -988,6 +1176,17 @@ void launch_gs_prep_pre(Context& c, const GsPlan& g, const double* r) {
 
 void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const double* z,
                          const double* zc, const int* agg) {
+    if (g.merged) {
+        ProfScope ps_(c, PF_GSPREP,
+                      12.0 * (g.wmat.nnz + g.wumat.nnz) + 8.0 * (g.n + 1) + 8.0 * g.n * (z ? 2 : 1) +
+                          (zc ? 12.0 * g.n : 0.0) + 16.0 * g.n);
+        if (g.n == 0) return;
+        launch_k(c, k_gs_prep_m, (g.n * kGroup + 255) / 256, 256, 0, g.n, g.wmat.rp.get(), g.wmat.ci.get(),
+                 g.wmat.v.get(), g.wumat.rp.get(), g.wumat.ci.get(), g.wumat.v.get(), r, z, zc, agg,
+                 g.bidx.get(), const_cast<double*>(g.packed.get()));
+        SDG_GS_CHECK();
+        return;
+    }
     ProfScope ps_(c, PF_GSPREP,
                   12.0 * g.upper.nnz + 4.0 * (g.n + 1) + 8.0 * g.n * (z ? 2 : 1) + (zc ? 12.0 * g.n : 0.0) +
                       16.0 * g.n);

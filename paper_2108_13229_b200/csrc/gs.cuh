@@ -92,13 +92,22 @@ struct GsPlan {
     int chain_steps = 0, chain_bands = 0;
     size_t chain_smem = 0;
     DevBuf<double> chain_coef;           // static scaled lower coefficients, [field][band][step][lane]
+    // level merging (gs.cu, merge_levels): groups of k consecutive dependency
+    // levels are walked as one; rows inside a group are substituted into each
+    // other, so the walk reads only earlier groups and the prep computes the
+    // group-local combination  b' = W r - WU z_old  instead of (r - U z_old)/d
+    bool merged = false;
+    int merge_k = 1;
+    DevCsr wmat, wumat;
     const double* packed_ptr = nullptr;  // records of a part inside its parent's buffer
     size_t part_doubles = 0;             // size of a part's records
 
     // components: per-row labels (e.g. u = 0 / v = 1 of the MAC velocity
     // block) so that bands cut every component at the same relative height.
+    // allow_merge: the caller runs launch_gs_prep_pre for every sweep that
+    // starts from z = 0 (no restriction seeding into a merged plan)
     void build(const HostCsr& a, const std::vector<int>& components, cudaStream_t s,
-               int bands_hint = 0);
+               int bands_hint = 0, bool allow_merge = false);
     double packed_bytes() const {
         return static_cast<double>(packed_ptr ? part_doubles : packed.size() + chain_coef.size()) * 8.0;
     }
@@ -130,6 +139,11 @@ private:
     bool build_walk(const HostCsr& a, const std::vector<double>& dinv_h, const std::vector<int>& nlow, int max_k,
                     cudaStream_t s, Link* link = nullptr);
 };
+
+// modelled cycles of one walk sweep over a (gs_walk.cu); 1e300 if it cannot walk
+double walk_model_cost(const HostCsr& a, const std::vector<int>& nlow, int max_k);
+double walk_shape_cost(const std::vector<int>& c2, const std::vector<int>& c8, int kw, int* w_out, int* r2_out,
+                       int* r8_out, bool corrected);
 
 // packed[bidx[i]] = r[i] * dinv[i]                      (pre-smoother, z_old = 0)
 void launch_gs_prep_pre(Context& c, const GsPlan& g, const double* r);

@@ -568,6 +568,71 @@ WalkKernel walk_kernel(int r2, int r8, int kw, bool pipe = false) {
 // Returns false when the system does not fit the walk (rows with more than 8
 // lower entries, a level too large for the staging ring); the caller then
 // builds the banded plan.
+// (W, R2, R8) from a cost model in cycles per pseudo-level, fitted to B200
+// measurements (scripts/mb_real2.cu): a latency chain that grows slowly with
+// the warps and rows per thread, or the shared-memory traffic (records staged
+// and read back, gathers) when that is larger.  Returns the modelled cycles
+// of one sweep (1e300 when no shape fits).
+//
+// `corrected` is the form used to compare plans (GsPlan::build, level
+// merging): refitted on the c2 launch lists of merged and unmerged walks,
+// where 16-entry records cost ~400 cycles more per level than the chain term
+// and staging-heavy levels ~1.8x the traffic term.
+double walk_shape_cost(const std::vector<int>& c2, const std::vector<int>& c8, int kw, int* w_out, int* r2_out,
+                       int* r8_out, bool corrected) {
+    const int nlv = static_cast<int>(c2.size());
+    const int WB = wide_bytes(kw);
+    int best_w = 0, best_r2 = 0, best_r8 = 0;
+    double best_cost = 1e300;
+    for (int w : {1, 2, 3, 4, 5, 6, 8, 11, 15})
+        for (int r2 = 1; r2 <= kMaxR2; ++r2)
+            for (int r8 = 0; r8 <= kMaxR8; ++r8) {
+                if (32 + 32 * w > max_threads(r2, r8, kw) || !shape_ok(r2, r8, kw)) continue;
+                const int cap2 = 32 * w * r2, cap8 = 32 * w * r8;
+                const double chain = 220.0 + 15.0 * w + 35.0 * (r2 - 1) + 60.0 * r8 +
+                                     (corrected && kw == 16 && r8 ? 400.0 : 0.0);
+                const double bw_scale = corrected ? 1.8 : 1.0;
+                double cost = 0;
+                bool ok = true;
+                for (int q = 0; q < nlv && ok; ++q) {
+                    if (c8[q] > 0 && r8 == 0) ok = false;
+                    const int p = std::max({1, (c2[q] + cap2 - 1) / cap2, r8 ? (c8[q] + cap8 - 1) / cap8 : 1,
+                                            (c2[q] * kK2Bytes + c8[q] * WB + kPseudoBytes - 1) / kPseudoBytes});
+                    const double bw = (2.0 * (c2[q] * kK2Bytes + c8[q] * WB) + 40.0 * c2[q] + 100.0 * c8[q]) /
+                                      (128.0 * p);
+                    cost += p * std::max(chain, bw_scale * bw);
+                }
+                if (ok && cost < best_cost) {
+                    best_cost = cost;
+                    best_w = w;
+                    best_r2 = r2;
+                    best_r8 = r8;
+                }
+            }
+    if (w_out) *w_out = best_w;
+    if (r2_out) *r2_out = best_r2;
+    if (r8_out) *r8_out = best_r8;
+    return best_cost;
+}
+
+double walk_model_cost(const HostCsr& a, const std::vector<int>& nlow, int max_k) {
+    if (max_k > kMaxK) return 1e300;
+    const int n = a.n_rows;
+    std::vector<int> lev(n, 0);
+    int nlv = 0;
+    for (int i = 0; i < n; ++i) {
+        int d = 0;
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+            if (a.ci[k] < i) d = std::max(d, lev[a.ci[k]] + 1);
+        lev[i] = d;
+        nlv = std::max(nlv, d + 1);
+    }
+    std::vector<int> c2(nlv, 0), c8(nlv, 0);
+    for (int i = 0; i < n; ++i) ++(nlow[i] <= 2 ? c2 : c8)[lev[i]];
+    const int kw = max_k <= 6 ? 6 : max_k <= 8 ? 8 : 16;
+    return walk_shape_cost(c2, c8, kw, nullptr, nullptr, nullptr, true);
+}
+
 bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, const std::vector<int>& nlow,
                         int max_k, cudaStream_t s, Link* link) {
     auto reject = [&](const char* why) {
@@ -593,35 +658,9 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     if (max_k > kw) return reject("forced record width too small");
     const int WB = wide_bytes(kw);
 
-    // (W, R2, R8) from a cost model in cycles per pseudo-level, fitted to
-    // B200 measurements (scripts/mb_real2.cu): a latency chain that grows
-    // slowly with the warps and rows per thread, or the shared-memory traffic
-    // (records staged and read back, gathers) when that is larger
+    // (W, R2, R8) from the cost model (walk_shape_cost)
     int best_w = 0, best_r2 = 0, best_r8 = 0;
-    double best_cost = 1e300;
-    for (int w : {1, 2, 3, 4, 5, 6, 8, 11, 15})
-        for (int r2 = 1; r2 <= kMaxR2; ++r2)
-            for (int r8 = 0; r8 <= kMaxR8; ++r8) {
-                if (32 + 32 * w > max_threads(r2, r8, kw) || !shape_ok(r2, r8, kw)) continue;
-                const int cap2 = 32 * w * r2, cap8 = 32 * w * r8;
-                const double chain = 220.0 + 15.0 * w + 35.0 * (r2 - 1) + 60.0 * r8;
-                double cost = 0;
-                bool ok = true;
-                for (int q = 0; q < nlv && ok; ++q) {
-                    if (c8[q] > 0 && r8 == 0) ok = false;
-                    const int p = std::max({1, (c2[q] + cap2 - 1) / cap2, r8 ? (c8[q] + cap8 - 1) / cap8 : 1,
-                                            (c2[q] * kK2Bytes + c8[q] * WB + kPseudoBytes - 1) / kPseudoBytes});
-                    const double bw = (2.0 * (c2[q] * kK2Bytes + c8[q] * WB) + 40.0 * c2[q] + 100.0 * c8[q]) /
-                                      (128.0 * p);
-                    cost += p * std::max(chain, bw);
-                }
-                if (ok && cost < best_cost) {
-                    best_cost = cost;
-                    best_w = w;
-                    best_r2 = r2;
-                    best_r8 = r8;
-                }
-            }
+    const double best_cost = walk_shape_cost(c2, c8, kw, &best_w, &best_r2, &best_r8, false);
     if (const char* e = std::getenv("SDG_WALK_SHAPE")) {  // dev override "warps,r2,r8"
         int w = 0, r2 = 0, r8 = 0;
         if (std::sscanf(e, "%d,%d,%d", &w, &r2, &r8) == 3 && w >= 1 && r2 >= 1 && r2 <= kMaxR2 && r8 >= 0 &&

@@ -114,7 +114,7 @@ AmgPrecond::AmgPrecond(CtxPtr c, const HostCsr& a, const AmgOpts& o) : Precond(s
             L.n_coarse = hl[l].n_coarse;
             L.zt.resize(A.n_rows);
             if (!exact_) {
-                L.gs.build(A, hl[l].components, cx.stream);
+                L.gs.build(A, hl[l].components, cx.stream, 0, /*allow_merge=*/true);
                 L.fast = L.gs.usable;
             }
         }
@@ -190,9 +190,9 @@ void AmgPrecond::vcycle(int lev, const double* r, double* z) {
     Level& L = levels_[lev];
     Level& C = levels_[lev + 1];
     // the next level's pre-smoother input is seeded by the restriction
-    const GsPlan* seed = (lev + 2 < num_levels() && C.fast) ? &C.gs : nullptr;
+    const GsPlan* seed = (lev + 2 < num_levels() && C.fast && !C.gs.merged) ? &C.gs : nullptr;
     if (L.fast) {
-        if (lev == 0) launch_gs_prep_pre(cx, L.gs, r);
+        if (lev == 0 || L.gs.merged) launch_gs_prep_pre(cx, L.gs, r);  // else seeded by the restriction
         launch_gs_lower(cx, L.gs, z);
         launch_restrict_warp(cx, L.a, L.pt_ptr.get(), L.pt_rows.get(), L.n_coarse, r, z, C.r.get(), seed);
         vcycle(lev + 1, C.r.get(), C.z.get());
