@@ -266,8 +266,8 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         rep = step()
-    if not rep.converged:
-        raise RuntimeError(f"warm-up solve did not converge: {rep}")
+        if not rep.converged:
+            raise RuntimeError(f"warm-up solve did not converge: {rep}")
 
     clocks = ClockSampler(local_rank)
     clocks.start()

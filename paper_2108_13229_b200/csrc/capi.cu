@@ -106,7 +106,7 @@ int sdg_context_profile(sdg_context* ctx, int family, int64_t* launches, double*
 
 const char* sdg_profile_family_name(int family) {
     static const char* names[] = {"spmv", "gs", "restrict", "prolong", "coarse",
-                                  "uzawa", "ortho", "bicg", "vec", "setup", "gsprep"};
+                                  "uzawa", "ortho", "bicg", "vec", "setup", "gsprep", "spmv_block"};
     return (family >= 0 && family < sdg::PF_COUNT) ? names[family] : "?";
 }
 

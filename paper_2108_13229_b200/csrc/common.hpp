@@ -97,7 +97,7 @@ private:
 
 // Kernel families for the live profiler (sdg_context_profile).
 enum ProfFamily {
-    PF_SPMV = 0,      // operator / block SpMV (incl. spmv_add, residual)
+    PF_SPMV = 0,      // operator SpMV over the SELL-32 copy (incl. spmv_add, residual)
     PF_GS,            // Gauss-Seidel sweeps
     PF_RESTRICT,      // fused residual + restriction
     PF_PROLONG,       // prolongation
@@ -108,6 +108,7 @@ enum ProfFamily {
     PF_VEC,           // copies, fills, axpy, dots
     PF_SETUP,         // setup-only kernels
     PF_GSPREP,        // smoother prep (upper part, fused prolongation)
+    PF_SPMV_BLOCK,    // CSR SpMV of the blocks (C', Uzawa B / C) and small operators
     PF_COUNT
 };
 
@@ -196,6 +197,13 @@ struct DevCsr {
     DevBuf<int> ci;
     DevBuf<double> v;
 
+    // optional SELL-32 copy for the operator SpMV (build_sell, kernels.cu):
+    // slice s of 32 rows stores entry t of its lane-l row at sell_off[s] + 32 t + l
+    bool sell = false;
+    int64_t sell_entries = 0;
+    DevBuf<int> sell_off, sell_len, sell_ci;
+    DevBuf<double> sell_v;
+
     void upload(const HostCsr& h, cudaStream_t s) {
         n_rows = h.n_rows;
         n_cols = h.n_cols;
@@ -204,6 +212,7 @@ struct DevCsr {
         ci.upload(h.ci, s);
         v.upload(h.v, s);
     }
+    void build_sell(const HostCsr& h, cudaStream_t s);  // kernels.cu
 };
 
 }  // namespace sdg

@@ -90,6 +90,37 @@ __global__ void k_spmv(int n, const int* __restrict__ rp, const int* __restrict_
     y[i] = add ? __dadd_rn(y_in[i], __dmul_rn(alpha, sum)) : sum;
 }
 
+// BITWISE: sparse.cpp:81-90 / 98-108 over the SELL-32 copy (DevCsr::build_sell):
+// one thread per row still sums its entries in column order, but lane l of a
+// warp reads entry t of row 32 s + l at off + 32 t + l, so every value/column
+// load of the warp is one contiguous 256 B / 128 B segment (the CSR kernel
+// above reads at the row stride).  Values and columns are streamed (evict
+// first) so x stays in L1/L2 for the gathers; three entries per step keep
+// independent loads in flight.
+__global__ void __launch_bounds__(256) k_spmv_sell(int n, const int* __restrict__ off, const int* __restrict__ len,
+                                                   const double* __restrict__ sv, const int* __restrict__ sc,
+                                                   const double* __restrict__ x, const double* __restrict__ y_in,
+                                                   double* __restrict__ y, double alpha, int add) {
+    pdl_begin();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int L = len[i];
+    const double* pv = sv + off[i >> 5] + (i & 31);
+    const int* pc = sc + off[i >> 5] + (i & 31);
+    double sum = 0.0;
+    int t = 0;
+    for (; t + 3 <= L; t += 3) {
+        const double v0 = __ldcs(pv + 32 * t), v1 = __ldcs(pv + 32 * (t + 1)), v2 = __ldcs(pv + 32 * (t + 2));
+        const int c0 = __ldcs(pc + 32 * t), c1 = __ldcs(pc + 32 * (t + 1)), c2 = __ldcs(pc + 32 * (t + 2));
+        const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2);
+        sum = __dadd_rn(sum, __dmul_rn(v0, x0));
+        sum = __dadd_rn(sum, __dmul_rn(v1, x1));
+        sum = __dadd_rn(sum, __dmul_rn(v2, x2));
+    }
+    for (; t < L; ++t) sum = __dadd_rn(sum, __dmul_rn(__ldcs(pv + 32 * t), __ldg(x + __ldcs(pc + 32 * t))));
+    y[i] = add ? __dadd_rn(y_in[i], __dmul_rn(alpha, sum)) : sum;
+}
+
 // BITWISE: precond.cpp:92-108 (sor_sweep), one CTA walking the level
 // schedule.  Lower neighbours (j < i) read the new iterate, upper ones the
 // old, in the reference's column order; the division order of
@@ -550,8 +581,15 @@ static inline int stride_blocks(Context& c, int64_t n) {
     } while (0)
 
 void launch_spmv(Context& c, const DevCsr& a, const double* x, double* y) {
-    ProfScope ps_(c, PF_SPMV, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 8.0 * a.n_rows);
+    ProfScope ps_(c, a.sell ? PF_SPMV : PF_SPMV_BLOCK,
+                  12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 8.0 * a.n_rows);
     if (a.n_rows == 0) return;
+    if (a.sell) {
+        launch_k(c, k_spmv_sell, (a.n_rows + 255) / 256, 256, 0, a.n_rows, a.sell_off.get(), a.sell_len.get(),
+                 a.sell_v.get(), a.sell_ci.get(), x, static_cast<const double*>(nullptr), y, 0.0, 0);
+        SDG_LAUNCHED(c);
+        return;
+    }
     launch_k(c, k_spmv, blocks_for(a.n_rows), kThreads, 0, a.n_rows, a.rp.get(), a.ci.get(),
                                                             a.v.get(), x, nullptr, y, 0.0, 0);
     SDG_LAUNCHED(c);
@@ -559,8 +597,15 @@ void launch_spmv(Context& c, const DevCsr& a, const double* x, double* y) {
 
 void launch_spmv_add(Context& c, const DevCsr& a, const double* x, const double* y_in,
                      double* y_out, double alpha) {
-    ProfScope ps_(c, PF_SPMV, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 16.0 * a.n_rows);
+    ProfScope ps_(c, a.sell ? PF_SPMV : PF_SPMV_BLOCK,
+                  12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 16.0 * a.n_rows);
     if (a.n_rows == 0) return;
+    if (a.sell) {
+        launch_k(c, k_spmv_sell, (a.n_rows + 255) / 256, 256, 0, a.n_rows, a.sell_off.get(), a.sell_len.get(),
+                 a.sell_v.get(), a.sell_ci.get(), x, y_in, y_out, alpha, 1);
+        SDG_LAUNCHED(c);
+        return;
+    }
     launch_k(c, k_spmv, blocks_for(a.n_rows), kThreads, 0, a.n_rows, a.rp.get(), a.ci.get(),
                                                             a.v.get(), x, y_in, y_out, alpha, 1);
     SDG_LAUNCHED(c);
@@ -786,6 +831,36 @@ void launch_bi_x_alpha(Context& c, int64_t n, BiState* st, const double* phat, d
     ProfScope ps_(c, PF_BICG, 24.0 * n);
     launch_k(c, k_bi_x_alpha, stride_blocks(c, n), kThreads, 0, n, st, phat, x);
     SDG_LAUNCHED(c);
+}
+
+void DevCsr::build_sell(const HostCsr& h, cudaStream_t s) {
+    const int n = h.n_rows;
+    const int ns = (n + 31) / 32;
+    std::vector<int> off(ns + 1, 0), len(n);
+    for (int sl = 0; sl < ns; ++sl) {
+        int w = 0;
+        for (int i = 32 * sl; i < std::min(n, 32 * sl + 32); ++i) {
+            len[i] = h.rp[i + 1] - h.rp[i];
+            w = std::max(w, len[i]);
+        }
+        if (static_cast<int64_t>(off[sl]) + 32LL * w >= (1LL << 31)) fail(SDG_EINVAL, "sell: too many entries");
+        off[sl + 1] = off[sl] + 32 * w;
+    }
+    std::vector<double> v(off[ns], 0.0);
+    std::vector<int> c(off[ns], 0);
+    for (int i = 0; i < n; ++i)
+        for (int k = h.rp[i]; k < h.rp[i + 1]; ++k) {
+            const size_t q = static_cast<size_t>(off[i / 32]) + 32 * (k - h.rp[i]) + (i % 32);
+            v[q] = h.v[k];
+            c[q] = h.ci[k];
+        }
+    sell_off.upload(off, s);
+    sell_len.upload(len, s);
+    sell_v.upload(v, s);
+    sell_ci.upload(c, s);
+    sell_entries = off[ns];
+    SDG_CUDA(cudaStreamSynchronize(s));  // host staging vectors die here
+    sell = true;
 }
 
 }  // namespace sdg

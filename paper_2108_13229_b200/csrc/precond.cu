@@ -66,6 +66,10 @@ void Context::drain_profile() {
 Matrix::Matrix(CtxPtr c, HostCsr h) : ctx(std::move(c)), host(std::move(h)) {
     host.check();
     dev.upload(host, ctx->stream);
+    // the operator SpMV of the Krylov drivers streams A once per apply: give
+    // it the coalesced SELL-32 copy (SDG_SELL=0 keeps the CSR kernel)
+    const char* e = std::getenv("SDG_SELL");
+    if (!(e && e[0] == '0') && host.n_rows >= 4096) dev.build_sell(host, ctx->stream);
 }
 
 void Matrix::ensure_schedule() {

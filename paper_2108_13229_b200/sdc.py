@@ -218,7 +218,7 @@ class Context:
     def profile(self) -> dict:
         """Per kernel family: launches, total CUDA-event ms, total algorithmic bytes."""
         out = {}
-        for f in range(11):
+        for f in range(12):
             n, ms, by = _i64(), _d(), _d()
             _check(lib().sdg_context_profile(self.h, f, C.byref(n), C.byref(ms), C.byref(by)))
             if n.value:
