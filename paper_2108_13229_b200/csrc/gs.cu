@@ -404,21 +404,73 @@ struct MergedLower {
     int groups = 0;
 };
 
+// Groups: fixed (level / k), or dynamic (dyn_cap > 0): consecutive levels
+// join the open group (at most k of them) while every row's substituted lower
+// part keeps <= dyn_cap entries, so the records stay narrow.
 bool merge_levels(const HostCsr& a, const std::vector<double>& dinv, const HostCsr& up, int k, int cap,
-                  MergedLower& out) {
+                  MergedLower& out, int dyn_cap = 0) {
     const int n = a.n_rows;
     std::vector<int> lev(n, 0);
+    int nlv = 0;
     for (int i = 0; i < n; ++i) {
         int d = 0;
         for (int e = a.rp[i]; e < a.rp[i + 1]; ++e)
             if (a.ci[e] < i) d = std::max(d, lev[a.ci[e]] + 1);
         lev[i] = d;
+        nlv = std::max(nlv, d + 1);
     }
     std::vector<int> grp(n);
     int ng = 0;
-    for (int i = 0; i < n; ++i) {
-        grp[i] = lev[i] / k;
-        ng = std::max(ng, grp[i] + 1);
+    if (dyn_cap <= 0) {
+        for (int i = 0; i < n; ++i) {
+            grp[i] = lev[i] / k;
+            ng = std::max(ng, grp[i] + 1);
+        }
+    } else {
+        std::vector<int> lptr(nlv + 1, 0), lrows(n);
+        for (int i = 0; i < n; ++i) ++lptr[lev[i] + 1];
+        for (int l = 0; l < nlv; ++l) lptr[l + 1] += lptr[l];
+        {
+            std::vector<int> fill(lptr.begin(), lptr.end() - 1);
+            for (int i = 0; i < n; ++i) lrows[fill[lev[i]]++] = i;
+        }
+        std::vector<std::vector<int>> gset(n);  // substituted lower columns (rows of the open group)
+        std::vector<int> mark(n, -1);
+        int cur = 0, in_group = 0;
+        std::vector<int> tmp;
+        auto try_level = [&](int l, bool fresh) {
+            for (int p = lptr[l]; p < lptr[l + 1]; ++p) {
+                const int i = lrows[p];
+                tmp.clear();
+                for (int e = a.rp[i]; e < a.rp[i + 1]; ++e) {
+                    const int j = a.ci[e];
+                    if (j >= i) continue;
+                    if (!fresh && grp[j] == cur) {
+                        for (int q : gset[j])
+                            if (mark[q] != i) { mark[q] = i; tmp.push_back(q); }
+                    } else if (mark[j] != i) {
+                        mark[j] = i;
+                        tmp.push_back(j);
+                    }
+                }
+                for (int q : tmp) mark[q] = -1;
+                if (!fresh && static_cast<int>(tmp.size()) > dyn_cap) return false;
+                gset[i] = tmp;
+            }
+            return true;
+        };
+        for (int l = 0; l < nlv; ++l) {
+            bool fresh = in_group == 0;
+            if (!fresh && (in_group >= k || !try_level(l, false))) {
+                ++cur;
+                in_group = 0;
+                fresh = true;
+            }
+            if (fresh) try_level(l, true);
+            for (int p = lptr[l]; p < lptr[l + 1]; ++p) grp[lrows[p]] = cur;
+            ++in_group;
+        }
+        ng = cur + 1;
     }
     // sparse accumulators (dense value + marker + touched list)
     std::vector<double> accT(n, 0.0), accG(n, 0.0);
@@ -549,30 +601,36 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     const bool try_pipe = !force_split && pipe_env && pipe_env[0] == '1';  // opt-in
     // 0. the lane chain, when the matrix is a structured finest level
     if (want_walk && build_chain(a, comps, dinv_h, s)) return finish();
-    // 0b. one walk over merged levels: the largest group size k <= 4 whose
-    //     modelled sweep (walk_model_cost, corrected form) is at least 10 %
-    //     cheaper than the plain walk.  The model ranks merged against plain
-    //     walks but not group sizes among themselves (c2 launch lists: the
-    //     Darcy levels gain most at k = 4, the velocity levels not at all once
-    //     the extra prep of a merged coarse level is counted), hence the rule.
-    //     SDG_GS_MERGE=k forces the group size, 1 disables.
+    // 0b. one walk over merged levels: the first candidate, in the order
+    //     (dynamic groups of <= 4 levels with <= 8 entries per row, fixed
+    //     k = 4, 3, 2), whose modelled sweep (walk_model_cost, corrected form)
+    //     is at least 10 % cheaper than the plain walk.  The model ranks merged
+    //     against plain walks but not candidates among themselves (c2 launch
+    //     lists: the Darcy levels gain most with 4-level groups, the velocity
+    //     levels not at all once the extra prep of a merged coarse level is
+    //     counted), hence the fixed order.  SDG_GS_MERGE=k forces fixed k
+    //     (with SDG_GS_MERGE_CAP=c: dynamic groups of <= k levels, <= c
+    //     entries), 1 disables.
     if (want_walk && allow_merge && !force_split && !try_pipe) {
         const char* me = std::getenv("SDG_GS_MERGE");
+        const char* ce = std::getenv("SDG_GS_MERGE_CAP");
         const int kforce = me ? std::atoi(me) : 0;
         if (kforce != 1) {
             const double base_cost = walk_model_cost(a, nlow, max_k);
             int best_k = 1;
             MergedLower bm;
-            const std::vector<int> ks = kforce > 1 ? std::vector<int>{kforce} : std::vector<int>{4, 3, 2};
-            for (int k : ks) {
+            std::vector<std::pair<int, int>> cands = {{4, 8}, {4, 0}, {3, 0}, {2, 0}};  // (k, dynamic cap)
+            if (kforce > 1) cands = {{kforce, ce ? std::atoi(ce) : 0}};
+            for (const auto& kc : cands) {
                 MergedLower m;
-                if (!merge_levels(a, dinv_h, up, k, 16, m)) continue;
+                if (!merge_levels(a, dinv_h, up, kc.first, 16, m, kc.second)) continue;
                 const double c = walk_model_cost(m.g, m.nlow, m.max_k);
                 if (std::getenv("SDG_DEBUG"))
-                    std::fprintf(stderr, "[sdg gs merge] n=%d k=%d groups=%d max_k=%d cost=%.0f (unmerged %.0f)\n",
-                                 n, k, m.groups, m.max_k, c, base_cost);
+                    std::fprintf(stderr,
+                                 "[sdg gs merge] n=%d k=%d cap=%d groups=%d max_k=%d cost=%.0f (unmerged %.0f)\n", n,
+                                 kc.first, kc.second, m.groups, m.max_k, c, base_cost);
                 if ((kforce > 1 && c < 1e300) || c <= 0.9 * base_cost) {
-                    best_k = k;
+                    best_k = kc.first;
                     bm = std::move(m);
                     break;
                 }
