@@ -104,6 +104,8 @@ int sdg_context_profile(sdg_context* ctx, int family, int64_t* launches, double*
     });
 }
 
+extern "C" int sdg_debug_walk_timeline(unsigned long long* out, int max) { return sdg::walk_timeline(out, max); }
+
 const char* sdg_profile_family_name(int family) {
     static const char* names[] = {"spmv", "gs", "restrict", "prolong", "coarse",
                                   "uzawa", "ortho", "bicg", "vec", "setup", "gsprep", "spmv_block"};

@@ -139,6 +139,17 @@ struct Context {
     cudaEvent_t take_event();
     void drain_profile();  // folds recorded events into the per-family sums
 
+    // A second stream for work that overlaps the main one (BlockPrecond
+    // td_bgs).  side_begin: side waits for everything issued on `stream` so
+    // far and launches go to side; side_end: launches go back to the main
+    // stream (no wait); side_join: the main stream waits for the side work.
+    // Events only, so this also works under graph capture.
+    cudaStream_t side = nullptr, main_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    void side_begin();
+    void side_end();
+    void side_join();
+
     explicit Context(int dev);
     ~Context();
     void sync() { SDG_CUDA(cudaStreamSynchronize(stream)); }

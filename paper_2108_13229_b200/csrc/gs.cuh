@@ -140,6 +140,9 @@ private:
                     cudaStream_t s, Link* link = nullptr);
 };
 
+// dev aid (built with -DSDG_WALK_TL): walk kernel timeline, 4 words per launch
+int walk_timeline(unsigned long long* out, int max);
+
 // modelled cycles of one walk sweep over a (gs_walk.cu); 1e300 if it cannot walk
 double walk_model_cost(const HostCsr& a, const std::vector<int>& nlow, int max_k);
 double walk_shape_cost(const std::vector<int>& c2, const std::vector<int>& c8, int kw, int* w_out, int* r2_out,

@@ -62,6 +62,16 @@ __device__ long long g_walk_trace[1024 * 16 * 4];
 #define WALK_CLK(L, k)
 #endif
 
+#ifdef SDG_WALK_TL  // dev aid: kernel timeline {start, after pdl wait, end, smid | n_levels << 16}
+__device__ unsigned long long g_walk_tl[4096 * 4];
+__device__ unsigned g_walk_tl_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 constexpr int kBars = 32;  // chunk mbarriers (chunks in flight at most)
 constexpr int kK2Bytes = 48;
 constexpr int kMaxK = 16;
@@ -465,6 +475,16 @@ __global__ void __launch_bounds__(max_threads(R2, R8, KW), 1) k_gs_walk(WalkPair
     const int tid = threadIdx.x;
     const int nl = a.n_levels, nc = a.n_chunks;
     const int zero_slot = a.ring, dummy = a.ring + 1;
+#ifdef SDG_WALK_TL
+    __shared__ unsigned tl_slot;
+    if (tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        tl_slot = atomicAdd(&g_walk_tl_n, 1u) % 4096u;
+        g_walk_tl[tl_slot * 4 + 0] = gtimer();
+        g_walk_tl[tl_slot * 4 + 3] = smid | (static_cast<unsigned long long>(nl) << 16);
+    }
+#endif
 
     for (int l = tid; l <= nl + 1; l += blockDim.x) meta[l] = a.meta_g[l];
     for (int c = tid; c < nc; c += blockDim.x) ctab[c] = a.chunk_g[c];
@@ -513,7 +533,14 @@ __global__ void __launch_bounds__(max_threads(R2, R8, KW), 1) k_gs_walk(WalkPair
             peer_flag = cluster_addr(flags + 2, rank ^ 1u);
         }
         walk_consumer<R2, R8, KW, PIPE>(a, meta, stage, nullrec, zr, flags, peer_zr, peer_flag, peer_pbar, pbars);
+#ifdef SDG_WALK_TL
+        if (tid == 32) g_walk_tl[tl_slot * 4 + 2] = gtimer();
+#endif
     } else if (tid == 0) {
+#ifdef SDG_WALK_TL
+        pdl_wait();
+        g_walk_tl[tl_slot * 4 + 1] = gtimer();
+#endif
         walk_producer(a, bars, flags, ctab, stage, pbars);
     }
     // no CTA of a pipe leaves while its peer may still store into it
@@ -956,6 +983,20 @@ WalkArgs walk_args(const GsPlan& g, double* z_new) {
                     z_new, g.walk_role, g.walk_n_peer, g.walk_pbar_bytes, g.walk_peer_bytes.get()};
 }
 }  // namespace
+
+#ifdef SDG_WALK_TL
+int walk_timeline(unsigned long long* out, int max) {
+    unsigned n = 0;
+    cudaMemcpyFromSymbol(&n, g_walk_tl_n, sizeof(n));
+    const int m = std::min<int>(std::min<unsigned>(n, 4096u), max);
+    cudaMemcpyFromSymbol(out, g_walk_tl, sizeof(unsigned long long) * 4 * m);
+    unsigned z = 0;
+    cudaMemcpyToSymbol(g_walk_tl_n, &z, sizeof(z));
+    return m;
+}
+#else
+int walk_timeline(unsigned long long*, int) { return 0; }
+#endif
 
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new) {
     WalkPair pair{};

@@ -121,6 +121,29 @@ __global__ void __launch_bounds__(256) k_spmv_sell(int n, const int* __restrict_
     y[i] = add ? __dadd_rn(y_in[i], __dmul_rn(alpha, sum)) : sum;
 }
 
+// z[i] -= sum_k K[k n + i] w[k]  (K column-major n x m, w staged in shared
+// memory; consecutive threads read consecutive rows of a column: coalesced)
+__global__ void __launch_bounds__(256) k_colmajor_gemv_sub(int n, int m, const double* __restrict__ kmat,
+                                                           const double* __restrict__ w, double* __restrict__ z) {
+    pdl_begin();
+    extern __shared__ double ws[];
+    for (int k = threadIdx.x; k < m; k += blockDim.x) ws[k] = w[k];
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* col = kmat + i;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int k = 0;
+    for (; k + 4 <= m; k += 4) {
+        a0 = fma(__ldcs(col + static_cast<size_t>(k) * n), ws[k], a0);
+        a1 = fma(__ldcs(col + static_cast<size_t>(k + 1) * n), ws[k + 1], a1);
+        a2 = fma(__ldcs(col + static_cast<size_t>(k + 2) * n), ws[k + 2], a2);
+        a3 = fma(__ldcs(col + static_cast<size_t>(k + 3) * n), ws[k + 3], a3);
+    }
+    for (; k < m; ++k) a0 = fma(__ldcs(col + static_cast<size_t>(k) * n), ws[k], a0);
+    z[i] -= (a0 + a1) + (a2 + a3);
+}
+
 // BITWISE: precond.cpp:92-108 (sor_sweep), one CTA walking the level
 // schedule.  Lower neighbours (j < i) read the new iterate, upper ones the
 // old, in the reference's column order; the division order of
@@ -635,6 +658,13 @@ void launch_prolong(Context& c, int n, const int* agg, const double* z, const do
     ProfScope ps_(c, PF_PROLONG, 20.0 * n + 8.0 * n);
     if (n == 0) return;
     launch_k(c, k_prolong, blocks_for(n), kThreads, 0, n, agg, z, zc, out);
+    SDG_LAUNCHED(c);
+}
+
+void launch_colmajor_gemv_sub(Context& c, int n, int m, const double* kmat, const double* w, double* z) {
+    ProfScope ps_(c, PF_COARSE, 8.0 * n * m + 8.0 * m + 16.0 * n);
+    if (n == 0 || m == 0) return;
+    launch_k(c, k_colmajor_gemv_sub, (n + 255) / 256, 256, static_cast<size_t>(m) * 8, n, m, kmat, w, z);
     SDG_LAUNCHED(c);
 }
 

@@ -33,9 +33,36 @@ Context::~Context() {
         cudaEventDestroy(r.b);
     }
     for (auto e : event_pool) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     if (cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(cusolver));
     if (stream) cudaStreamDestroy(stream);
 }
+
+void Context::side_begin() {
+    if (!side) {
+        int lo = 0, hi = 0;
+        SDG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SDG_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
+        SDG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        SDG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    if (main_stream) fail(SDG_EINVAL, "side_begin: already on the side stream");
+    SDG_CUDA(cudaEventRecord(ev_fork, stream));
+    SDG_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    main_stream = stream;
+    stream = side;
+}
+
+void Context::side_end() {
+    if (!main_stream) fail(SDG_EINVAL, "side_end: not on the side stream");
+    SDG_CUDA(cudaEventRecord(ev_join, side));
+    stream = main_stream;
+    main_stream = nullptr;
+}
+
+void Context::side_join() { SDG_CUDA(cudaStreamWaitEvent(stream, ev_join, 0)); }
 
 cudaEvent_t Context::take_event() {
     if (!event_pool.empty()) {
@@ -269,7 +296,11 @@ BlockPrecond::BlockPrecond(CtxPtr c, int kind, const HostCsr& matrix, int n_v, i
         fail(SDG_EDIM, "block preconditioner: pm sub-block size mismatch");
     if (!first_ || !pm_) fail(SDG_EDIM, "block preconditioner: missing sub-preconditioner");
     Context& cx = *ctx_;
-    if (kind_ == SDG_TD_BGS) c_prime_.upload(submatrix(matrix, n_ff, n, 0, n_ff), cx.stream);
+    if (kind_ == SDG_TD_BGS) {
+        const HostCsr cp = submatrix(matrix, n_ff, n, 0, n_ff);
+        c_prime_.upload(cp, cx.stream);
+        setup_interface_split(cp);
+    }
     if (kind_ == SDG_PV_BGS) {
         c_.upload(submatrix(matrix, n_v_, n_ff, 0, n_v_), cx.stream);
         c1_prime_.upload(submatrix(matrix, n_ff, n, 0, n_v_), cx.stream);
@@ -278,9 +309,51 @@ BlockPrecond::BlockPrecond(CtxPtr c, int kind, const HostCsr& matrix, int n_v, i
     cx.sync();
 }
 
+// td_bgs: z_pm = P_D'(r_pm - C' z_ff).  P_D' (one AMG V-cycle from zero:
+// Gauss-Seidel sweeps, restriction, coarse solve, prolongation) is linear, and
+// C' is nonzero only in the interface rows G of the porous block, so
+//   z_pm = P_D' r_pm - K w,   K = P_D' restricted to the columns G,  w = (C' z_ff)_G.
+// P_D' r_pm does not wait for the free-flow solve: it runs on the side stream
+// while the Uzawa V-cycle runs on the main one; after the join one GEMV with
+// the precomputed K (|G| applies of P_D' at setup) finishes the block.  Equal
+// to precond.cpp:339-345 in exact arithmetic.  Used when K fits
+// kSplitBudget bytes; SDG_TD_SPLIT=0 disables.
+void BlockPrecond::setup_interface_split(const HostCsr& cp) {
+    constexpr double kSplitBudget = 2.0 * 1024 * 1024 * 1024;
+    const char* e = std::getenv("SDG_TD_SPLIT");
+    if (e && e[0] == '0') return;
+    std::vector<int> rows;
+    for (int i = 0; i < cp.n_rows; ++i)
+        if (cp.rp[i + 1] > cp.rp[i]) rows.push_back(i);
+    const int m = static_cast<int>(rows.size());
+    if (m == 0 || static_cast<double>(n_ppm_) * m * 8.0 > kSplitBudget) return;
+    Context& cx = *ctx_;
+    HostCsr cg(m, cp.n_cols);
+    for (int k = 0; k < m; ++k) {
+        const int i = rows[k];
+        for (int q = cp.rp[i]; q < cp.rp[i + 1]; ++q) {
+            cg.ci.push_back(cp.ci[q]);
+            cg.v.push_back(cp.v[q]);
+        }
+        cg.rp[k + 1] = static_cast<int>(cg.ci.size());
+    }
+    c_gamma_.upload(cg, cx.stream);
+    w_gamma_.resize(m);
+    k_gamma_.resize(static_cast<size_t>(n_ppm_) * m);
+    DevBuf<double> unit(n_ppm_);
+    for (int k = 0; k < m; ++k) {
+        launch_fill(cx, unit.get(), 0.0, n_ppm_);
+        const double one = 1.0;
+        SDG_CUDA(cudaMemcpyAsync(unit.get() + rows[k], &one, sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+        pm_->apply_uncounted(unit.get(), k_gamma_.get() + static_cast<size_t>(k) * n_ppm_);
+        SDG_CUDA(cudaStreamSynchronize(cx.stream));  // `one` is a host stack value
+    }
+    n_gamma_ = m;
+}
+
 int64_t BlockPrecond::setup_memory_doubles() const {
     return first_->setup_memory_doubles() + pm_->setup_memory_doubles() + c_prime_.nnz + c_.nnz +
-           c1_prime_.nnz;
+           c1_prime_.nnz + static_cast<int64_t>(n_ppm_) * n_gamma_;
 }
 
 int64_t BlockPrecond::work_per_apply() const {
@@ -297,6 +370,22 @@ void BlockPrecond::do_apply(const double* r, double* z) {
         pm_->apply(r + n_ff, z + n_ff);
         break;
     case SDG_TD_BGS:  // precond.cpp:339-345
+        if (n_gamma_ > 0) {  // see setup_interface_split
+            cx.side_begin();
+            try {
+                pm_->apply(r + n_ff, z + n_ff);
+            } catch (...) {
+                cx.side_end();
+                cx.side_join();
+                throw;
+            }
+            cx.side_end();
+            first_->apply(r, z);
+            launch_spmv(cx, c_gamma_, z, w_gamma_.get());
+            cx.side_join();
+            launch_colmajor_gemv_sub(cx, n_ppm_, n_gamma_, k_gamma_.get(), w_gamma_.get(), z + n_ff);
+            break;
+        }
         first_->apply(r, z);
         launch_spmv_add(cx, c_prime_, z, r + n_ff, tmp_.get(), -1.0);
         pm_->apply(tmp_.get(), z + n_ff);

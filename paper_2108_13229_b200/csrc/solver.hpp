@@ -47,6 +47,8 @@ public:
         do_apply(r, z);
     }
     int64_t applications() const { return applications_.load(std::memory_order_relaxed); }
+    // setup-time applies (BlockPrecond interface split) that are not counted
+    void apply_uncounted(const double* r, double* z) { do_apply(r, z); }
     virtual int64_t setup_memory_doubles() const { return 0; }
     virtual int64_t work_per_apply() const { return 0; }
     virtual double omega() const { return std::nan(""); }
@@ -157,6 +159,12 @@ private:
     PrecondPtr first_, pm_;
     DevCsr c_prime_, c_, c1_prime_;
     DevBuf<double> tmp_;
+    // td_bgs interface split (setup_interface_split)
+    void setup_interface_split(const HostCsr& cp);
+    int n_gamma_ = 0;
+    DevCsr c_gamma_;               // the interface rows of C'
+    DevBuf<double> w_gamma_;       // (C' z_ff) on those rows
+    DevBuf<double> k_gamma_;       // P_D' e_g for every interface row g, column-major
 };
 
 // Krylov drivers on device vectors; host control flow mirrors krylov.cpp.
