@@ -245,6 +245,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
     const int stride = 32 * nw;
     const int n_levels = a.n_levels;
     const unsigned stage_s = smem_addr(stage), null_s = smem_addr(nullrec), zr_s = smem_addr(zr);
+    const unsigned dummy_s = zr_s + 8u * dummy;
     double* const z_new = a.z_new;
     int* progress = flags;
     const int* landed = flags + 1;
@@ -369,7 +370,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
         for (int r = 0; r < R2; ++r) {
             const double acc = fma(v2[r][1], z2[r][1], fma(v2[r][0], z2[r][0], x.b2[r]));
             stsd(x.wa2[r], acc);
-            stsd(x.pa2[r], acc);
+            if (x.pa2[r] != dummy_s) stsd(x.pa2[r], acc);  // most rows are not pinned
             if (PIPE && x.ex2[r]) st_async_f64(x.ex2[r], acc, peer_pbar + 8u * L);
             if (!(SDG_WALK_EXP & 2) && x.rid2[r] >= 0) z_new[x.rid2[r]] = acc;
         }
@@ -388,7 +389,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
                 for (int j = 0; j + j2 < KW / 2; j += 2 * j2) qq[j] += qq[j + j2];
             const double acc = qq[0];
             stsd(x.wa8[r], acc);
-            stsd(x.pa8[r], acc);
+            if (x.pa8[r] != dummy_s) stsd(x.pa8[r], acc);
             if (!(SDG_WALK_EXP & 2) && x.rid8[r] >= 0) z_new[x.rid8[r]] = acc;
         }
         WALK_CLK(L, 1);
