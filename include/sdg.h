@@ -172,6 +172,15 @@ int sdg_identity_create(sdg_context* ctx, int n, sdg_precond** out);
 /* ground_dof (precond.cpp:375-392) applied on the host to a CSR copy. */
 int sdg_ground_dof_host(int n, const int* rowptr, const int* col, double* val_inout, int dof);
 
+/* Host check of the fast smoother's level merging (no GPU): one forward
+ * Gauss-Seidel sweep (precond.cpp:92-108, omega = 1, z_old may be NULL = 0)
+ * evaluated in the merged form the device walk uses, with groups of k
+ * dependency levels (dyn_cap > 0: dynamic groups of <= k levels whose rows
+ * keep <= dyn_cap entries).  *groups receives the group count.  Equal to the
+ * plain sweep up to rounding. */
+int sdg_gs_merged_sweep_host(int n, const int* rowptr, const int* col, const double* val, int k, int dyn_cap,
+                             const double* r, const double* z_old, double* z_new, int* groups);
+
 /* The whole MonolithicDriver::build_preconditioner wiring (bench.cpp:121-182)
  * for kind td_bj / td_bgs in one call: D' = ground_dof(A[pm,pm]), V labels
  * u = 0 / v = 1, Uzawa(AMG_V) on [v | p_ff], AMG on D'.  v_max_levels /

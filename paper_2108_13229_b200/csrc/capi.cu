@@ -235,6 +235,17 @@ int sdg_identity_create(sdg_context* ctx, int n, sdg_precond** out) {
     });
 }
 
+int sdg_gs_merged_sweep_host(int n, const int* rowptr, const int* col, const double* val, int k, int dyn_cap,
+                             const double* r, const double* z_old, double* z_new, int* groups) {
+    return guard([&] {
+        sdg::HostCsr h = make_csr(n, n, rowptr, col, val);
+        require_diagonal(h, "sor_sweep");
+        const int g = sdg::gs_merged_sweep_host(h, std::max(1, k), dyn_cap, r, z_old, z_new);
+        if (g < 0) sdg::fail(SDG_EINVAL, "gs merge: a merged row needs more than 16 entries");
+        if (groups) *groups = g;
+    });
+}
+
 int sdg_ground_dof_host(int n, const int* rowptr, const int* col, double* val_inout, int dof) {
     return guard([&] {
         sdg::HostCsr h = make_csr(n, n, rowptr, col, val_inout);

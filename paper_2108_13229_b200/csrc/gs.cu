@@ -542,6 +542,38 @@ bool merge_levels(const HostCsr& a, const std::vector<double>& dinv, const HostC
 
 }  // namespace
 
+// Host evaluation of one merged forward sweep (checker of merge_levels, used
+// by the CPU tests through sdg_gs_merged_sweep_host): b' = W r - WU z_old,
+// then z_i = b'_i - sum_j G_ij z_j in row order (G refers to earlier groups
+// only).  Returns the number of groups, or -1 when a row exceeds 16 entries.
+int gs_merged_sweep_host(const HostCsr& a, int k, int dyn_cap, const double* r, const double* z_old,
+                         double* z_new) {
+    const int n = a.n_rows;
+    std::vector<double> dinv(n, 0.0);
+    HostCsr up(n, n);
+    for (int i = 0; i < n; ++i) {
+        for (int e = a.rp[i]; e < a.rp[i + 1]; ++e) {
+            if (a.ci[e] == i) dinv[i] = 1.0 / a.v[e];
+            if (a.ci[e] > i) {
+                up.ci.push_back(a.ci[e]);
+                up.v.push_back(a.v[e]);
+            }
+        }
+        up.rp[i + 1] = static_cast<int>(up.ci.size());
+    }
+    MergedLower m;
+    if (!merge_levels(a, dinv, up, k, 16, m, dyn_cap)) return -1;
+    for (int i = 0; i < n; ++i) {
+        double b = 0.0;
+        for (int e = m.w.rp[i]; e < m.w.rp[i + 1]; ++e) b += m.w.v[e] * r[m.w.ci[e]];
+        if (z_old)
+            for (int e = m.wu.rp[i]; e < m.wu.rp[i + 1]; ++e) b -= m.wu.v[e] * z_old[m.wu.ci[e]];
+        for (int e = m.g.rp[i]; e < m.g.rp[i + 1]; ++e) b -= m.g.v[e] * z_new[m.g.ci[e]];
+        z_new[i] = b;
+    }
+    return m.groups;
+}
+
 // ---------------------------------------------------------------------------
 // plan
 

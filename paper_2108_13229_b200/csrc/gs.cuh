@@ -140,6 +140,11 @@ private:
                     cudaStream_t s, Link* link = nullptr);
 };
 
+// host check of level merging (gs.cu): one merged forward sweep; returns the
+// number of groups (-1: a row needs more than 16 entries)
+int gs_merged_sweep_host(const HostCsr& a, int k, int dyn_cap, const double* r, const double* z_old,
+                         double* z_new);
+
 // dev aid (built with -DSDG_WALK_TL): walk kernel timeline, 4 words per launch
 int walk_timeline(unsigned long long* out, int max);
 

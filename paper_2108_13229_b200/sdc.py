@@ -133,6 +133,7 @@ def lib():
         p("sdg_block_create", _i, [_i, _vp, _i, _i, _i, _vp, _vp, P(_vp)])
         p("sdg_identity_create", _i, [_vp, _i, P(_vp)])
         p("sdg_ground_dof_host", _i, [_i, _ip, _ip, _dp, _i])
+        p("sdg_gs_merged_sweep_host", _i, [_i, _ip, _ip, _dp, _i, _i, _dp, _vp, _dp, P(_i)])
         p("sdg_td_create", _i, [_vp, _i, _i, _i, _i, _i, _i, _i, _d, P(_vp)])
         p("sdg_precond_destroy", _i, [_vp])
         p("sdg_precond_rows", _i, [_vp])
@@ -387,6 +388,22 @@ def ground_dof(a: SparseMatrix, dof: int = 0) -> SparseMatrix:
     vals = a.values.copy()
     _check(lib().sdg_ground_dof_host(a.n_rows, a.row_offsets, a.col_indices, vals, dof))
     return SparseMatrix(a.n_rows, a.n_cols, a.row_offsets.copy(), a.col_indices.copy(), vals)
+
+
+def gs_merged_sweep_host(a: SparseMatrix, r, k: int, dyn_cap: int = 0, z_old=None):
+    """Host check of the smoother's level merging (gs.cu merge_levels): one
+    forward Gauss-Seidel sweep (omega = 1) in the merged form the device walk
+    evaluates, groups of k dependency levels (dyn_cap > 0: dynamic groups).
+    Returns (z_new, number of groups).  Runs without a GPU."""
+    r = _f64(r)
+    if r.size != a.n_rows or a.n_rows != a.n_cols:
+        raise ValueError("gs_merged_sweep_host: dimension mismatch")
+    zo = None if z_old is None else _f64(z_old).copy()
+    z = np.zeros(a.n_rows)
+    g = C.c_int(0)
+    _check(lib().sdg_gs_merged_sweep_host(a.n_rows, a.row_offsets, a.col_indices, a.values, int(k), int(dyn_cap), r,
+                                          None if zo is None else zo.ctypes.data, z, C.byref(g)))
+    return z, g.value
 
 
 def sor_sweep(a: SparseMatrix, z, r, omega: float) -> np.ndarray:

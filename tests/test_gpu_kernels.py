@@ -112,8 +112,11 @@ def test_amg_on_system_blocks(ref):
 
 
 @pytest.mark.parametrize("mode", [{"SDG_GS_SPLIT": "1"}, {"SDG_GS_PIPE": "1"}, {"SDG_GS_WALK": "0"},
-                                  {"SDG_GS_BANDS": "4"}],
-                         ids=["label-block-walks", "2-cta-pipe", "cluster-kernel", "cluster-4-bands"])
+                                  {"SDG_GS_BANDS": "4"}, {"SDG_GS_MERGE": "1"}, {"SDG_GS_MERGE": "2"},
+                                  {"SDG_GS_MERGE": "4"}, {"SDG_GS_MERGE": "4", "SDG_GS_MERGE_CAP": "8"},
+                                  {"SDG_TD_SPLIT": "0"}, {"SDG_SELL": "0"}],
+                         ids=["label-block-walks", "2-cta-pipe", "cluster-kernel", "cluster-4-bands", "no-merge",
+                              "merge-2", "merge-4", "merge-dynamic", "no-interface-split", "csr-spmv"])
 def test_smoother_paths_match_reference(ref, golden, monkeypatch, mode):
     """The other lower-solve plans (one walk per u/v block with a coupling
     step; the u/v blocks walked concurrently on a 2-CTA cluster; the banded
@@ -134,6 +137,29 @@ def test_smoother_paths_match_reference(ref, golden, monkeypatch, mode):
                                int(g["n_vel"]), int(g["n_pff"]), int(g["n_ppm"]))
     p = sdc.TdPreconditioner(system, "td_bgs", omega_override=float(g["omega"]))
     assert rel_l2(p.apply(g["apply_r"]), g["apply_z"]) < 1e-10
+
+
+def test_c2_merge_and_interface_split_agree(monkeypatch):
+    """The c2 bench system: the td_bgs apply with the interface split and the
+    merged walks (defaults) against the plain sequential apply with unmerged
+    walks, and merged AMG V-cycles against the bitwise Gauss-Seidel path."""
+    from paper_2108_13229_b200 import scenarios
+    cfg = scenarios.CONFIGS["c2"]
+    s = scenarios.build_system(cfg)
+    r = np.random.default_rng(7).standard_normal(s.n_total())
+    fast = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
+    z_fast = fast.apply(r)
+    monkeypatch.setenv("SDG_TD_SPLIT", "0")
+    monkeypatch.setenv("SDG_GS_MERGE", "1")
+    plain = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels, omega_override=fast.omega())
+    assert rel_l2(z_fast, plain.apply(r)) < 1e-11
+    D = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
+    x = r[: D.n_rows]
+    monkeypatch.setenv("SDG_GS_MERGE", "4")
+    merged = sdc.AmgPreconditioner(D, sdc.AmgOptions(max_levels=cfg.d_max_levels))
+    monkeypatch.setenv("SDG_GS_EXACT", "1")
+    exact = sdc.AmgPreconditioner(D, sdc.AmgOptions(max_levels=cfg.d_max_levels))
+    assert rel_l2(merged.apply(x), exact.apply(x)) < 1e-11
 
 
 def check_linear(p, seed, n, tol=1e-13):

@@ -170,3 +170,32 @@ def test_partitioned_subproblems_bitwise(ref, n, k):
     assert np.array_equal(sdc.darcy_velocity_trace(cfg, p, pg), ref.darcy_velocity_trace(n, k, p, pg))
     with pytest.raises(ValueError):
         sdc.assemble_stokes(cfg, vg[:-1])
+
+
+@pytest.mark.parametrize("block,k,cap", [("V", 2, 0), ("V", 4, 8), ("D", 2, 0), ("D", 4, 0), ("D", 4, 8)])
+def test_gs_level_merging_equals_reference_sweep(ref, block, k, cap):
+    """The merged form of the fast smoother (groups of k dependency levels,
+    substituted inside each group: gs.cu merge_levels), evaluated on the host,
+    against the reference sor_sweep (precond.cpp:92-108) from zero (pre-smoother)
+    and from an old iterate (post-smoother), c1 blocks."""
+    from oracle.refpy import Csr
+    s = ref.assemble(50)
+    A = to_sdc(s.a)
+    if block == "V":
+        a = sdc.submatrix(A, 0, s.n_vel, 0, s.n_vel)
+    else:
+        a = sdc.ground_dof(sdc.submatrix(A, s.n_ff, s.n, s.n_ff, s.n))
+    ra = Csr(a.n_rows, a.n_cols, a.row_offsets, a.col_indices, a.values)
+    r = ref.random_vector(a.n_rows, 21)
+    z_old = ref.random_vector(a.n_rows, 22)
+    z, groups = sdc.gs_merged_sweep_host(a, r, k, cap)
+    want = ref.sor_sweep(ra, np.zeros(a.n_rows), r, 1.0)
+    assert np.linalg.norm(z - want) <= 1e-12 * np.linalg.norm(want)
+    z2, _ = sdc.gs_merged_sweep_host(a, r, k, cap, z_old=z_old)
+    want2 = ref.sor_sweep(ra, z_old, r, 1.0)
+    assert np.linalg.norm(z2 - want2) <= 1e-12 * np.linalg.norm(want2)
+    z1, g1 = sdc.gs_merged_sweep_host(a, r, 1)  # k = 1: the plain level walk
+    assert np.linalg.norm(z1 - want) <= 1e-12 * np.linalg.norm(want)
+    assert groups < g1 if (cap == 0 or block == "D") else groups <= g1
+    if cap == 0:
+        assert groups == -(-g1 // k)
