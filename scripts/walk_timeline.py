@@ -1,12 +1,12 @@
 """Dev helper (library built with -DSDG_WALK_TL): globaltimer timeline of the
-walk kernels of a few device-resident td_bgs applies on c2."""
+walk kernels of a few device-resident td_bgs applies (config argv[1], default c2)."""
 import os, sys
 import ctypes as C
 sys.path.insert(0, os.getcwd())
 import numpy as np
 import torch
 from paper_2108_13229_b200 import scenarios, sdc
-cfg = scenarios.CONFIGS["c2"]
+cfg = scenarios.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 s = scenarios.build_system(cfg)
 ctx = sdc.default_context()
 p = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels, ctx=ctx)
