@@ -647,7 +647,12 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
         const char* me = std::getenv("SDG_GS_MERGE");
         const char* ce = std::getenv("SDG_GS_MERGE_CAP");
         const int kforce = me ? std::atoi(me) : 0;
-        if (kforce != 1) {
+        // merging pays where a level is latency-bound, i.e. narrow; wide levels
+        // (> kMergeRows rows on average, c3+) are throughput-bound and only get
+        // wider records, so they are not even evaluated (setup time at c4)
+        constexpr int kMergeRows = 200;
+        const int depth = lower_schedule(a).n_levels();
+        if (kforce != 1 && (kforce > 1 || static_cast<int64_t>(depth) * kMergeRows >= n)) {
             const double base_cost = walk_model_cost(a, nlow, max_k);
             int best_k = 1;
             MergedLower bm;
