@@ -340,14 +340,15 @@ void BlockPrecond::setup_interface_split(const HostCsr& cp) {
     c_gamma_.upload(cg, cx.stream);
     w_gamma_.resize(m);
     k_gamma_.resize(static_cast<size_t>(n_ppm_) * m);
-    DevBuf<double> unit(n_ppm_);
-    for (int k = 0; k < m; ++k) {
+    DevBuf<double> unit(n_ppm_), one(1);
+    one.upload(std::vector<double>{1.0}, cx.stream);
+    for (int k = 0; k < m; ++k) {  // column k of K = P_D' e_{rows[k]}
         launch_fill(cx, unit.get(), 0.0, n_ppm_);
-        const double one = 1.0;
-        SDG_CUDA(cudaMemcpyAsync(unit.get() + rows[k], &one, sizeof(double), cudaMemcpyHostToDevice, cx.stream));
+        SDG_CUDA(cudaMemcpyAsync(unit.get() + rows[k], one.get(), sizeof(double), cudaMemcpyDeviceToDevice,
+                                 cx.stream));
         pm_->apply_uncounted(unit.get(), k_gamma_.get() + static_cast<size_t>(k) * n_ppm_);
-        SDG_CUDA(cudaStreamSynchronize(cx.stream));  // `one` is a host stack value
     }
+    cx.sync();
     n_gamma_ = m;
 }
 
