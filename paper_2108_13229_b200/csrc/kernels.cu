@@ -319,23 +319,60 @@ __global__ void k_set_identity(int n, double* dense) {
 
 // Block b owns elements [b*chunk, min(n,(b+1)*chunk)); warp w dots vectors
 // w, w+8, ... of X against y over that chunk.
-__global__ void k_multidot(int64_t n, int k, const double* __restrict__ X, int64_t ldx,
-                           const double* __restrict__ y, int64_t chunk, double* partials,
-                           unsigned* ticket, double* __restrict__ out) {
+// out[v] = X[v] . y for v < k.  One 1024-thread block per SM owns a chunk of
+// rows; its threads walk the chunk once per group of kDotGroup vectors with
+// that many independent accumulators, two rows per step (16 loads in flight
+// per thread), and fold them in a fixed order.  The last block folds the
+// per-block partials one vector per warp (deterministic, no block barriers).
+constexpr int kDotGroup = 8;
+constexpr int kDotThreads = 1024;
+
+__global__ void __launch_bounds__(kDotThreads) k_multidot(int64_t n, int k, const double* __restrict__ X,
+                                                          int64_t ldx, const double* __restrict__ y, int64_t chunk,
+                                                          double* partials, unsigned* ticket,
+                                                          double* __restrict__ out) {
     pdl_begin();
     __shared__ bool am_last;
-    __shared__ double red[kThreads / 32];
+    __shared__ double red[kDotThreads / 32][kDotGroup];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int64_t b0 = blockIdx.x * chunk;
     const int64_t b1 = min(n, b0 + chunk);
-    for (int vv = warp; vv < k; vv += nwarps) {
-        const double* xv = X + vv * ldx;
-        double s = 0.0;
-        for (int64_t i = b0 + lane; i < b1; i += 32) s = fma(__ldg(xv + i), __ldg(y + i), s);
-        s = warp_sum(s);
-        if (lane == 0) partials[blockIdx.x * kMaxDotVecs + vv] = s;
+    for (int g0 = 0; g0 < k; g0 += kDotGroup) {
+        double acc[kDotGroup];
+#pragma unroll
+        for (int g = 0; g < kDotGroup; ++g) acc[g] = 0.0;
+        const int ng = min(kDotGroup, k - g0);
+        int64_t i = b0 + threadIdx.x;
+        for (; i + blockDim.x < b1; i += 2 * blockDim.x) {
+            const double y0 = __ldg(y + i), y1 = __ldg(y + i + blockDim.x);
+            double x0[kDotGroup], x1[kDotGroup];
+#pragma unroll
+            for (int g = 0; g < kDotGroup; ++g) {
+                x0[g] = g < ng ? __ldcs(X + (g0 + g) * ldx + i) : 0.0;
+                x1[g] = g < ng ? __ldcs(X + (g0 + g) * ldx + i + blockDim.x) : 0.0;
+            }
+#pragma unroll
+            for (int g = 0; g < kDotGroup; ++g) acc[g] = fma(x1[g], y1, fma(x0[g], y0, acc[g]));
+        }
+        if (i < b1) {
+            const double y0 = __ldg(y + i);
+#pragma unroll
+            for (int g = 0; g < kDotGroup; ++g)
+                if (g < ng) acc[g] = fma(__ldcs(X + (g0 + g) * ldx + i), y0, acc[g]);
+        }
+#pragma unroll
+        for (int g = 0; g < kDotGroup; ++g) {
+            const double t = warp_sum(acc[g]);
+            if (lane == 0) red[warp][g] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x < ng) {
+            double t = 0.0;
+            for (int w = 0; w < nwarps; ++w) t += red[w][threadIdx.x];
+            partials[blockIdx.x * kMaxDotVecs + g0 + threadIdx.x] = t;
+        }
+        __syncthreads();
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned t = atomicAdd(ticket, 1u);
@@ -344,20 +381,13 @@ __global__ void k_multidot(int64_t n, int k, const double* __restrict__ X, int64
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-    for (int vv = 0; vv < k; ++vv) {
+    for (int vv = warp; vv < k; vv += nwarps) {
         double s = 0.0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
-            s += __ldcg(partials + b * kMaxDotVecs + vv);
+        for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(partials + b * kMaxDotVecs + vv);
         s = warp_sum(s);
-        if (lane == 0) red[warp] = s;
-        __syncthreads();
-        if (warp == 0) {
-            double x = lane < nwarps ? red[lane] : 0.0;
-            x = warp_sum(x);
-            if (lane == 0) out[vv] = x;
-        }
-        __syncthreads();
+        if (lane == 0) out[vv] = s;
     }
+    __syncthreads();
     if (threadIdx.x == 0) *ticket = 0u;
 }
 
@@ -373,6 +403,7 @@ __global__ void k_multi_axpy(int64_t n, int k, const double* __restrict__ X, int
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         double wi = w[i];
+#pragma unroll 8
         for (int vv = 0; vv < k; ++vv) wi = fma(-hs[vv], __ldg(X + vv * ldx + i), wi);
         w[i] = wi;
         if (NORM) acc[0] = fma(wi, wi, acc[0]);
@@ -741,13 +772,13 @@ void launch_multidot(Context& c, ReduceWs& ws, int64_t n, int k, const double* X
     ProfScope ps_(c, PF_ORTHO, 8.0 * (k + 1) * (double)n);
     if (k <= 0) return;
     if (k > kMaxDotVecs || ws.max_vals < kMaxDotVecs) fail(SDG_EINVAL, "multidot: too many vectors");
-    int nb = reduce_blocks(static_cast<int>(std::min<int64_t>(n, 1 << 30)), c.num_sms);
-    nb = std::min(nb, ws.max_blocks);
+    // one block per SM, fewer when the rows are few
+    int nb = static_cast<int>(std::min<int64_t>(c.num_sms, (n + 4 * kDotThreads - 1) / (4 * kDotThreads)));
+    nb = std::max(1, std::min(nb, ws.max_blocks));
     const int64_t chunk = std::max<int64_t>(1, (n + nb - 1) / nb);
     nb = static_cast<int>((n + chunk - 1) / chunk);
     if (nb < 1) nb = 1;
-    launch_k(c, k_multidot, nb, kThreads, 0, n, k, X, ldx, y, chunk, ws.partials.get(),
-                                              ws.ticket.get(), out);
+    launch_k(c, k_multidot, nb, kDotThreads, 0, n, k, X, ldx, y, chunk, ws.partials.get(), ws.ticket.get(), out);
     SDG_LAUNCHED(c);
 }
 
@@ -763,8 +794,8 @@ void launch_multi_axpy(Context& c, int64_t n, int k, const double* X, int64_t ld
 void launch_multi_axpy_norm2(Context& c, ReduceWs& ws, int64_t n, int k, const double* X,
                              int64_t ldx, const double* h, double* w, double* out) {
     ProfScope ps_(c, PF_ORTHO, 8.0 * (k + 2) * (double)n);
-    const int nb = std::min(reduce_blocks(static_cast<int>(std::min<int64_t>(n, 1 << 30)), c.num_sms),
-                            ws.max_blocks);
+    // as many blocks as the plain multi_axpy (the norm fold reads one partial per block)
+    const int nb = std::min(stride_blocks(c, n), ws.max_blocks);
     launch_k(c, k_multi_axpy<true>, nb, kThreads, 0, n, k, X, ldx, h, w, ws.partials.get(),
                                                       ws.ticket.get(), out);
     SDG_LAUNCHED(c);

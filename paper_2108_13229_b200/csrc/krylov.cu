@@ -88,7 +88,7 @@ SolveOut pd_gmres(Matrix& A, Precond* P, const double* b, double* x, double tol_
     DevBuf<double> basis(static_cast<size_t>(ld) * (m_cap + 1));
     DevBuf<double> r(n), z(n), w(n), best_x(n), dd(4 * 64);
     ReduceWs ws;
-    ws.init(reduce_blocks(n, c.num_sms), 64, c.stream);
+    ws.init(std::max(reduce_blocks(n, c.num_sms), 8 * c.num_sms), 64, c.stream);
     double* h1 = dd.get();
     double* h2 = dd.get() + 64;
     double* sc = dd.get() + 128;   // [0] = ||w||, [1] = beta, [2] = ||r||^2
