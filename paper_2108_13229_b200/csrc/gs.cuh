@@ -7,22 +7,20 @@
 //   lower (latency-bound): the exact lexicographic recurrence
 //         z_i = b_i - sum_{j<i} (a_ij / d_i) z_j.
 //
-// The lower solve is a banded, pipelined level walk on one thread-block
-// cluster.  Rows are split into B bands (horizontal strips of the grid for
-// the lexicographic MAC / TPFA orderings, cut at the same relative height in
-// every labelled component); CTA b owns band b and walks the dependency
-// levels of the band-local lower triangle.  Values needed by later bands are
-// pushed into their shared memory with DSMEM st.async packets that complete
-// single-use mbarriers there; a band waits for a packet before the level that
-// reads it, so bands run as a skewed pipeline and the whole sweep keeps the
-// lexicographic order exactly.  Inside a CTA each
-// level's packed segment (b, scaled lower coefficients, ring slots, row ids)
-// is streamed into shared memory by TMA bulk copies (cp.async.bulk +
-// mbarrier) several levels ahead by a producer warp, and the band's recent z
-// values live in a shared-memory ring; the per-level critical path is one
-// barrier + shared-memory gathers + a short FMA tree.  Splitting into bands
-// spreads the shared-memory and L2 traffic of a sweep over B SMs, which is
-// what bounds a single-CTA walk (scripts/mb_levels.cu).
+// The lower solve is chosen per matrix by GsPlan::build, in this order:
+//   * a merged single-CTA walk (gs.cu merge_levels): k dependency levels per
+//     group, rows substituted inside a group, prep b' = W r - WU z_old;
+//   * a single-CTA walk (gs_walk.cu): the level-ordered records streamed into
+//     shared memory by TMA bulk copies from a producer thread, recent z values
+//     in a shared-memory ring, per level gathers -> FMAs -> ring store ->
+//     named-barrier hand-off;
+//   * one such walk per labelled block (u, v) in sequence with a coupling
+//     step, when the whole matrix does not fit one CTA's shared memory;
+//   * the banded cluster kernel (gs.cu k_gs_cluster): B bands on a
+//     thread-block cluster, values crossing bands pushed with DSMEM st.async
+//     packets completing single-use mbarriers, bands as a skewed pipeline.
+// Opt-in experiments: the 2-CTA pipe (SDG_GS_PIPE=1) and the lane chain
+// (SDG_GS_CHAIN=1|2).  Every variant keeps the exact lexicographic order.
 //
 // Arithmetic is reassociated versus the reference (upper part first, 1/d
 // folded into the coefficients), so results agree to rounding; the BITWISE

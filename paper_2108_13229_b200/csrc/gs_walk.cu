@@ -689,9 +689,11 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     // (W, R2, R8) from the cost model (walk_shape_cost)
     int best_w = 0, best_r2 = 0, best_r8 = 0;
     const double best_cost = walk_shape_cost(c2, c8, kw, &best_w, &best_r2, &best_r8, false);
-    if (const char* e = std::getenv("SDG_WALK_SHAPE")) {  // dev override "warps,r2,r8"
-        int w = 0, r2 = 0, r8 = 0;
-        if (std::sscanf(e, "%d,%d,%d", &w, &r2, &r8) == 3 && w >= 1 && r2 >= 1 && r2 <= kMaxR2 && r8 >= 0 &&
+    if (const char* e = std::getenv("SDG_WALK_SHAPE")) {  // dev override "warps,r2,r8[,rows]" (rows: only that n)
+        int w = 0, r2 = 0, r8 = 0, only_n = 0;
+        const int got = std::sscanf(e, "%d,%d,%d,%d", &w, &r2, &r8, &only_n);
+        if (got == 4 && only_n != n) w = 0;
+        if (got >= 3 && w >= 1 && r2 >= 1 && r2 <= kMaxR2 && r8 >= 0 &&
             r8 <= kMaxR8) {
             bool ok = 32 + 32 * w <= max_threads(r2, r8, kw) && shape_ok(r2, r8, kw);
             for (int q = 0; q < nlv; ++q) ok = ok && (r8 > 0 || c8[q] == 0);

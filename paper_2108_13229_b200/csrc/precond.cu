@@ -372,18 +372,23 @@ void BlockPrecond::do_apply(const double* r, double* z) {
         break;
     case SDG_TD_BGS:  // precond.cpp:339-345
         if (n_gamma_ > 0) {  // see setup_interface_split
-            cx.side_begin();
+            // fork unless this apply is itself running on the side stream
+            // (a td_bgs nested in another one): then the same split, in order
+            const bool fork = cx.main_stream == nullptr;
+            if (fork) cx.side_begin();
             try {
                 pm_->apply(r + n_ff, z + n_ff);
             } catch (...) {
-                cx.side_end();
-                cx.side_join();
+                if (fork) {
+                    cx.side_end();
+                    cx.side_join();
+                }
                 throw;
             }
-            cx.side_end();
+            if (fork) cx.side_end();
             first_->apply(r, z);
             launch_spmv(cx, c_gamma_, z, w_gamma_.get());
-            cx.side_join();
+            if (fork) cx.side_join();
             launch_colmajor_gemv_sub(cx, n_ppm_, n_gamma_, k_gamma_.get(), w_gamma_.get(), z + n_ff);
             break;
         }
