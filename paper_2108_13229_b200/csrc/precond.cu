@@ -316,18 +316,41 @@ BlockPrecond::BlockPrecond(CtxPtr c, int kind, const HostCsr& matrix, int n_v, i
 // P_D' r_pm does not wait for the free-flow solve: it runs on the side stream
 // while the Uzawa V-cycle runs on the main one; after the join one GEMV with
 // the precomputed K (|G| applies of P_D' at setup) finishes the block.  Equal
-// to precond.cpp:339-345 in exact arithmetic.  Used when K fits
-// kSplitBudget bytes; SDG_TD_SPLIT=0 disables.
+// to precond.cpp:339-345 in exact arithmetic.  Used when K fits kSplitBudget
+// bytes and streaming it is modelled at < 70 % of one measured P_D' apply;
+// SDG_TD_SPLIT=0 disables, =1 skips the time test.
 void BlockPrecond::setup_interface_split(const HostCsr& cp) {
-    constexpr double kSplitBudget = 2.0 * 1024 * 1024 * 1024;
+    constexpr double kSplitBudget = 16.0 * 1024 * 1024 * 1024;  // bytes of K at most
+    constexpr double kGemvBytesPerSec = 5.0e12;                  // K streamed once per apply
     const char* e = std::getenv("SDG_TD_SPLIT");
     if (e && e[0] == '0') return;
     std::vector<int> rows;
     for (int i = 0; i < cp.n_rows; ++i)
         if (cp.rp[i + 1] > cp.rp[i]) rows.push_back(i);
     const int m = static_cast<int>(rows.size());
-    if (m == 0 || static_cast<double>(n_ppm_) * m * 8.0 > kSplitBudget) return;
+    const double kbytes = static_cast<double>(n_ppm_) * m * 8.0;
+    if (m == 0 || kbytes > kSplitBudget) return;
     Context& cx = *ctx_;
+    // worth it only when streaming K costs clearly less than the porous
+    // V-cycle it takes off the critical path: time one apply
+    {
+        DevBuf<double> x(n_ppm_), y(n_ppm_);
+        launch_fill(cx, x.get(), 1.0, n_ppm_);
+        pm_->apply_uncounted(x.get(), y.get());  // warm-up (plans, caches)
+        cudaEvent_t a, b;
+        SDG_CUDA(cudaEventCreate(&a));
+        SDG_CUDA(cudaEventCreate(&b));
+        SDG_CUDA(cudaEventRecord(a, cx.stream));
+        pm_->apply_uncounted(x.get(), y.get());
+        SDG_CUDA(cudaEventRecord(b, cx.stream));
+        SDG_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        const bool force = e && e[0] == '1';
+        if (!force && kbytes / kGemvBytesPerSec > 0.7e-3 * ms) return;
+    }
     HostCsr cg(m, cp.n_cols);
     for (int k = 0; k < m; ++k) {
         const int i = rows[k];
