@@ -122,8 +122,15 @@ __global__ void __launch_bounds__(256) k_spmv_sell(int n, const int* __restrict_
 }
 
 // z[i] -= sum_k K[k n + i] w[k]  (K column-major n x m, w staged in shared
-// memory; consecutive threads read consecutive rows of a column: coalesced).
-// (An 8-way column split with a fixed-order fold measured no faster at c2.)
+// memory).  The sum of a row is four interleaved chains a_c over the columns
+// k = c (mod 4) (the tail m mod 4 columns continue a_0), folded as
+// (a0 + a1) + (a2 + a3).  Each chain runs on its own lane (4 lanes per row,
+// 8 rows per warp: every load instruction reads 4 columns x 64 contiguous
+// bytes), 8 loads in flight per lane, and the fold is two xor-shuffles in the
+// same association, so the result does not depend on the launch shape.
+// (An 8-way column split with a different fold changed the BiCGSTAB count at
+// c2 by rounding alone; one lane per row with 4 loads in flight left the
+// GEMV latency-bound: 27 us for 33 MB at c2.)
 template <bool STREAM>
 __device__ __forceinline__ double ld_k(const double* p) {
     return STREAM ? __ldcs(p) : __ldg(p);
@@ -136,19 +143,28 @@ __global__ void __launch_bounds__(256) k_colmajor_gemv_sub(int n, int m, const d
     extern __shared__ double ws[];
     for (int k = threadIdx.x; k < m; k += blockDim.x) ws[k] = w[k];
     __syncthreads();
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double* col = kmat + i;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int k = 0;
-    for (; k + 4 <= m; k += 4) {
-        a0 = fma(ld_k<STREAM>(col + static_cast<size_t>(k) * n), ws[k], a0);
-        a1 = fma(ld_k<STREAM>(col + static_cast<size_t>(k + 1) * n), ws[k + 1], a1);
-        a2 = fma(ld_k<STREAM>(col + static_cast<size_t>(k + 2) * n), ws[k + 2], a2);
-        a3 = fma(ld_k<STREAM>(col + static_cast<size_t>(k + 3) * n), ws[k + 3], a3);
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = g >> 2, c = g & 3;
+    double a = 0.0;
+    if (i < n) {
+        const double* col = kmat + i;
+        const int m4 = m & ~3;
+        int k = c;
+        constexpr int U = 8;
+        for (; k + 4 * (U - 1) < m4; k += 4 * U) {
+            double v[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) v[j] = ld_k<STREAM>(col + static_cast<size_t>(k + 4 * j) * n);
+#pragma unroll
+            for (int j = 0; j < U; ++j) a = fma(v[j], ws[k + 4 * j], a);
+        }
+        for (; k < m4; k += 4) a = fma(ld_k<STREAM>(col + static_cast<size_t>(k) * n), ws[k], a);
+        if (c == 0)
+            for (k = m4; k < m; ++k) a = fma(ld_k<STREAM>(col + static_cast<size_t>(k) * n), ws[k], a);
     }
-    for (; k < m; ++k) a0 = fma(ld_k<STREAM>(col + static_cast<size_t>(k) * n), ws[k], a0);
-    z[i] -= (a0 + a1) + (a2 + a3);
+    const double s01 = a + __shfl_xor_sync(0xffffffffu, a, 1);       // lane c=0: a0 + a1, c=2: a2 + a3
+    const double s = s01 + __shfl_xor_sync(0xffffffffu, s01, 2);     // c=0: (a0 + a1) + (a2 + a3)
+    if (i < n && c == 0) z[i] -= s;
 }
 
 // BITWISE: precond.cpp:92-108 (sor_sweep), one CTA walking the level
@@ -704,9 +720,9 @@ void launch_colmajor_gemv_sub(Context& c, int n, int m, const double* kmat, cons
     if (n == 0 || m == 0) return;
     const size_t smem = static_cast<size_t>(m) * 8;
     if (8.0 * n * m > 40e6)
-        launch_k(c, k_colmajor_gemv_sub<true>, (n + 255) / 256, 256, smem, n, m, kmat, w, z);
+        launch_k(c, k_colmajor_gemv_sub<true>, (4 * n + 255) / 256, 256, smem, n, m, kmat, w, z);
     else
-        launch_k(c, k_colmajor_gemv_sub<false>, (n + 255) / 256, 256, smem, n, m, kmat, w, z);
+        launch_k(c, k_colmajor_gemv_sub<false>, (4 * n + 255) / 256, 256, smem, n, m, kmat, w, z);
     SDG_LAUNCHED(c);
 }
 
