@@ -26,6 +26,7 @@
 #include "gs.cuh"
 #include "launch.cuh"
 #include "ptx.cuh"
+#include "rowdot.cuh"
 
 #include <cooperative_groups.h>
 
@@ -70,7 +71,8 @@ __global__ void k_gs_couple(int rows, int r0, const int* __restrict__ rp, const 
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows) return;
     double acc = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) acc = fma(v[k], z[ci[k]], acc);
+    row_fold<8>(ci, v, rp[i], rp[i + 1], [&](int j) { return z[j]; },
+                [&](double a, double x) { acc = fma(a, x, acc); });
     packed[bidx[r0 + i]] += acc;
 }
 
@@ -84,14 +86,11 @@ __global__ void k_gs_prep_post(int n, const int* __restrict__ urp, const int* __
     if (i >= n) return;
     double s = r[i];
     const int e = urp[i + 1];
-    if (zc) {
-        for (int k = urp[i]; k < e; ++k) {
-            const int j = uci[k];
-            s = fma(-uv[k], z[j] + zc[agg[j]], s);
-        }
-    } else if (z) {
-        for (int k = urp[i]; k < e; ++k) s = fma(-uv[k], z[uci[k]], s);
-    }
+    auto f = [&](double a, double x) { s = fma(-a, x, s); };
+    if (zc)
+        row_fold<8>(uci, uv, urp[i], e, [&](int j) { return z[j] + zc[agg[j]]; }, f);
+    else if (z)
+        row_fold<8>(uci, uv, urp[i], e, [&](int j) { return z[j]; }, f);
     packed[bidx[i]] = s * dinv[i];
 }
 
@@ -341,8 +340,12 @@ __device__ __forceinline__ double warp_shfl(double x, int src) {
     return __shfl_sync(0xffffffffu, x, src);
 }
 
-// BITWISE with precond.cpp:241-244: one warp per aggregate, lanes compute the
-// fine residuals, lane 0 accumulates them in ascending fine-row order.
+// BITWISE with precond.cpp:241-244: kRestrictGroup lanes per aggregate
+// (aggregates hold ~4-8 fine rows), the lanes compute the fine residuals
+// (row loads issued up front, rowdot.cuh), lane 0 of the group accumulates
+// them in ascending fine-row order.
+constexpr int kRestrictGroup = 8;
+
 __global__ void k_restrict_warp(int n_coarse, const int* __restrict__ pt_ptr,
                                 const int* __restrict__ pt_rows, const int* __restrict__ rp,
                                 const int* __restrict__ ci, const double* __restrict__ v,
@@ -350,29 +353,34 @@ __global__ void k_restrict_warp(int n_coarse, const int* __restrict__ pt_ptr,
                                 double* __restrict__ rc, const double* __restrict__ next_dinv,
                                 const int* __restrict__ next_bidx, double* __restrict__ next_packed) {
     pdl_begin();
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= n_coarse) return;
-    const int q0 = pt_ptr[warp], q1 = pt_ptr[warp + 1];
+    constexpr int G = kRestrictGroup;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ag = t / G, lane = t % G;
+    const bool live = ag < n_coarse;
+    const int q0 = live ? pt_ptr[ag] : 0, q1 = live ? pt_ptr[ag + 1] : 0;
+    // every group of the warp takes part in the shuffles of the longest one
+    const int rounds = __reduce_max_sync(0xffffffffu, (q1 - q0 + G - 1) / G);
     double acc = 0.0;
-    for (int base = q0; base < q1; base += 32) {
+    for (int b = 0; b < rounds; ++b) {
+        const int base = q0 + b * G;
         double res = 0.0;
         if (base + lane < q1) {
             const int i = pt_rows[base + lane];
             double sum = 0.0;
-            const int ke = rp[i + 1];
-            for (int k = rp[i]; k < ke; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], z[ci[k]]));
+            row_fold<8>(ci, v, rp[i], rp[i + 1], [&](int j) { return z[j]; },
+                        [&](double a, double x) { sum = __dadd_rn(sum, __dmul_rn(a, x)); });
             res = __dadd_rn(r[i], __dmul_rn(-1.0, sum));
         }
-        const int cnt = min(32, q1 - base);
-        for (int k = 0; k < cnt; ++k) {
-            const double x = warp_shfl(res, k);
-            acc = __dadd_rn(acc, x);
+        const int cnt = q1 - base;
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const double x = __shfl_sync(0xffffffffu, res, k, G);
+            if (k < cnt) acc = __dadd_rn(acc, x);
         }
     }
-    if (lane == 0) {
-        rc[warp] = acc;
-        if (next_packed) next_packed[next_bidx[warp]] = acc * next_dinv[warp];
+    if (live && lane == 0) {
+        rc[ag] = acc;
+        if (next_packed) next_packed[next_bidx[ag]] = acc * next_dinv[ag];
     }
 }
 
@@ -1352,7 +1360,7 @@ void launch_restrict_warp(Context& c, const DevCsr& a, const int* pt_ptr, const 
                       4.0 * (n_coarse + 1) + 8.0 * n_coarse);
     if (n_coarse == 0) return;
     const int threads = 256;
-    const int blocks = static_cast<int>((static_cast<int64_t>(n_coarse) * 32 + threads - 1) / threads);
+    const int blocks = static_cast<int>((static_cast<int64_t>(n_coarse) * kRestrictGroup + threads - 1) / threads);
     launch_k(c, k_restrict_warp, blocks, threads, 0, 
         n_coarse, pt_ptr, pt_rows, a.rp.get(), a.ci.get(), a.v.get(), r, z, rc,
         next ? next->dinv.get() : nullptr, next ? next->bidx.get() : nullptr,

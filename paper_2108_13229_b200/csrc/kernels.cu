@@ -1,6 +1,7 @@
 // Device kernels of the hot path.  See kernels.cuh for the contracts.
 #include "kernels.cuh"
 #include "launch.cuh"
+#include "rowdot.cuh"
 
 #include <algorithm>
 #include <string>
@@ -85,8 +86,8 @@ __global__ void k_spmv(int n, const int* __restrict__ rp, const int* __restrict_
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double sum = 0.0;
-    const int e = rp[i + 1];
-    for (int k = rp[i]; k < e; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], x[ci[k]]));
+    row_fold<8>(ci, v, rp[i], rp[i + 1], [&](int j) { return x[j]; },
+                [&](double a, double xv) { sum = __dadd_rn(sum, __dmul_rn(a, xv)); });
     y[i] = add ? __dadd_rn(y_in[i], __dmul_rn(alpha, sum)) : sum;
 }
 
@@ -297,8 +298,8 @@ __global__ void k_uzawa_p(int n, const int* __restrict__ rp, const int* __restri
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double sum = 0.0;
-    const int e = rp[i + 1];
-    for (int k = rp[i]; k < e; ++k) sum = __dadd_rn(sum, __dmul_rn(v[k], zv[ci[k]]));
+    row_fold<8>(ci, v, rp[i], rp[i + 1], [&](int j) { return zv[j]; },
+                [&](double a, double x) { sum = __dadd_rn(sum, __dmul_rn(a, x)); });
     z_p[i] = __dmul_rn(omega, __dsub_rn(sum, r_p[i]));
 }
 
