@@ -125,27 +125,32 @@ __global__ void __launch_bounds__(256) k_spmv_sell(int n, const int* __restrict_
 // z[i] -= sum_k K[k n + i] w[k]  (K column-major n x m, w staged in shared
 // memory).  The sum of a row is four interleaved chains a_c over the columns
 // k = c (mod 4) (the tail m mod 4 columns continue a_0), folded as
-// (a0 + a1) + (a2 + a3).  Each chain runs on its own lane (4 lanes per row,
-// 8 rows per warp: every load instruction reads 4 columns x 64 contiguous
-// bytes), 8 loads in flight per lane, and the fold is two xor-shuffles in the
-// same association, so the result does not depend on the launch shape.
-// (An 8-way column split with a different fold changed the BiCGSTAB count at
-// c2 by rounding alone; one lane per row with 4 loads in flight left the
-// GEMV latency-bound: 27 us for 33 MB at c2.)
+// (a0 + a1) + (a2 + a3).  Warp c of a group of four computes chain c for 32
+// consecutive rows (every load instruction reads 256 contiguous bytes of one
+// column), 8 loads in flight per lane, and the fold goes through shared
+// memory in the same association, so the result does not depend on the
+// launch shape.  (An 8-way column split with a different fold changed the
+// BiCGSTAB count at c2 by rounding alone; one lane per row with 4 loads in
+// flight left the GEMV latency-bound: 27 us for 33 MB at c2.)
 template <bool STREAM>
 __device__ __forceinline__ double ld_k(const double* p) {
     return STREAM ? __ldcs(p) : __ldg(p);
 }
 
+constexpr int kGemvRowBlocks = 2;  // 32-row blocks per CTA (4 warps each)
+
 template <bool STREAM>  // STREAM: K too large to stay in L2, read once per apply (evict first)
-__global__ void __launch_bounds__(256) k_colmajor_gemv_sub(int n, int m, const double* __restrict__ kmat,
-                                                           const double* __restrict__ w, double* __restrict__ z) {
+__global__ void __launch_bounds__(128 * kGemvRowBlocks)
+    k_colmajor_gemv_sub(int n, int m, const double* __restrict__ kmat, const double* __restrict__ w,
+                        double* __restrict__ z) {
     pdl_begin();
     extern __shared__ double ws[];
+    __shared__ double part[4 * kGemvRowBlocks][32];
     for (int k = threadIdx.x; k < m; k += blockDim.x) ws[k] = w[k];
     __syncthreads();
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i = g >> 2, c = g & 3;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = warp & 3, rb = warp >> 2;
+    const int i = (blockIdx.x * kGemvRowBlocks + rb) * 32 + lane;
     double a = 0.0;
     if (i < n) {
         const double* col = kmat + i;
@@ -163,9 +168,12 @@ __global__ void __launch_bounds__(256) k_colmajor_gemv_sub(int n, int m, const d
         if (c == 0)
             for (k = m4; k < m; ++k) a = fma(ld_k<STREAM>(col + static_cast<size_t>(k) * n), ws[k], a);
     }
-    const double s01 = a + __shfl_xor_sync(0xffffffffu, a, 1);       // lane c=0: a0 + a1, c=2: a2 + a3
-    const double s = s01 + __shfl_xor_sync(0xffffffffu, s01, 2);     // c=0: (a0 + a1) + (a2 + a3)
-    if (i < n && c == 0) z[i] -= s;
+    part[warp][lane] = a;
+    __syncthreads();
+    if (c == 0 && i < n) {
+        const double* p = &part[4 * rb][lane];
+        z[i] -= (p[0] + p[32]) + (p[64] + p[96]);
+    }
 }
 
 // BITWISE: precond.cpp:92-108 (sor_sweep), one CTA walking the level
@@ -721,9 +729,9 @@ void launch_colmajor_gemv_sub(Context& c, int n, int m, const double* kmat, cons
     if (n == 0 || m == 0) return;
     const size_t smem = static_cast<size_t>(m) * 8;
     if (8.0 * n * m > 40e6)
-        launch_k(c, k_colmajor_gemv_sub<true>, (4 * n + 255) / 256, 256, smem, n, m, kmat, w, z);
+        launch_k(c, k_colmajor_gemv_sub<true>, (n + 32 * kGemvRowBlocks - 1) / (32 * kGemvRowBlocks), 128 * kGemvRowBlocks, smem, n, m, kmat, w, z);
     else
-        launch_k(c, k_colmajor_gemv_sub<false>, (4 * n + 255) / 256, 256, smem, n, m, kmat, w, z);
+        launch_k(c, k_colmajor_gemv_sub<false>, (n + 32 * kGemvRowBlocks - 1) / (32 * kGemvRowBlocks), 128 * kGemvRowBlocks, smem, n, m, kmat, w, z);
     SDG_LAUNCHED(c);
 }
 

@@ -20,4 +20,8 @@ SDG_PROFILER_RANGE=1 timeout 900 ncu --profile-from-start off --set full --clock
     -k regex:k_gs_walk -s 4 -c 1 -o gpurun_out/r/gs_walk_v0 python scripts/prof_apply.py c2 > gpurun_out/r/ncu_gs.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmv_sell -s 30 -c 1 -o gpurun_out/r/spmv_c3 \
     python bench.py --config c3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/r/ncu_spmv.log 2>&1
+# the interface GEMV at c3 (K = 250,000 x 500 fp64 = 1 GB, streamed once per apply)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_colmajor_gemv_sub -s 20 -c 1 -o gpurun_out/r/gemv_c3 \
+    python bench.py --config c3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/r/ncu_gemv.log 2>&1
+timeout 1200 python bench.py --config c4 --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/r/bench_c4.json 2> gpurun_out/r/bench_c4.err
 ls -la gpurun_out/r

@@ -37,7 +37,7 @@ def details(rep):
 
 
 os.makedirs(DST, exist_ok=True)
-for f in ("bench.json", "bench_ref.json", "bench_c3.json", "pytest_gpu.log", "smoke.log"):
+for f in ("bench.json", "bench_ref.json", "bench_c3.json", "bench_c4.json", "pytest_gpu.log", "smoke.log"):
     if os.path.exists(os.path.join(SRC, f)):
         shutil.copy(os.path.join(SRC, f), os.path.join(DST, f))
 shutil.copy(os.path.join(SRC, "launches.csv"), os.path.join(DST, "launches_c2.csv"))
@@ -50,7 +50,8 @@ if walks:
                      "dram_bytes_per_launch": b,
                      "source": "profiles/r01/apply_dram_c2.csv (ncu --profile-from-start off --metrics "
                                "dram__bytes_read.sum,dram__bytes_write.sum over one apply; caches cold per launch)"}
-for name, rep, fam in (("ncu_gs_walk_v0.json", "gs_walk_v0.ncu-rep", None), ("ncu_spmv_c3.json", "spmv_c3.ncu-rep", "spmv")):
+for name, rep, fam in (("ncu_gs_walk_v0.json", "gs_walk_v0.ncu-rep", None), ("ncu_spmv_c3.json", "spmv_c3.ncu-rep", "spmv"),
+                       ("ncu_gemv_c3.json", "gemv_c3.ncu-rep", "gemv")):
     p = os.path.join(SRC, rep)
     if not os.path.exists(p):
         continue
@@ -67,7 +68,9 @@ for name, rep, fam in (("ncu_gs_walk_v0.json", "gs_walk_v0.ncu-rep", None), ("nc
             if h in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
                 tot += float(v.replace(",", "")) * scale
-        traffic[fam] = {"kernel": "k_spmv_sell (operator SpMV, SELL-32), c3, one launch", "dram_bytes_per_launch": tot,
+        what = {"spmv": "k_spmv_sell (operator SpMV, SELL-32), c3, one launch",
+                "gemv": "k_colmajor_gemv_sub (td_bgs interface GEMV, K 250,000 x 500), c3, one launch"}[fam]
+        traffic[fam] = {"kernel": what, "dram_bytes_per_launch": tot,
                         "source": f"profiles/r01/{name} (ncu --set full)"}
 with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
     json.dump(traffic, f, indent=2)
