@@ -80,6 +80,7 @@ struct GsPlan {
     std::vector<DevCsr> couple;
     bool pipe = false;   // two parts walked concurrently on a 2-CTA cluster (no coupling step)
     int walk_role = 0;   // WalkArgs::role of a pipe part
+    int walk_roles = 0;  // WalkArgs::roles (small / wide rows on separate warps)
     int walk_import_base = 0;  // first import slot of a walk (pipe role 2)
     int walk_n_peer = 0, walk_pbar_bytes = 0;
     DevBuf<int> walk_peer_bytes;  // pipe role 2: bytes the peer pushes at each of its levels

@@ -234,15 +234,19 @@ struct WalkRows {
 // stores, global z), turn level L+1's raw record words into addresses, load
 // level L+2's raw records; then the level hand-off.  The critical path per
 // level is gathers -> FMAs -> ring store -> hand-off.
-template <int R2, int R8, int KW, bool PIPE>
+template <int R2, int R8, int KW, bool PIPE, bool ROLES>
 __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* meta, const unsigned char* stage,
                                               const unsigned char* nullrec, double* zr, int* flags,
                                               unsigned peer_zr, unsigned peer_flag, unsigned peer_pbar,
                                               uint64_t* pbars_l) {
     const int mask = a.ring - 1, dummy = a.ring + 1;
-    const int nw = (blockDim.x >> 5) - 1;
-    const int t0 = threadIdx.x - 32;  // (warp - 1) * 32 + lane
-    const int stride = 32 * nw;
+    const int nw = (blockDim.x >> 5) - 1;  // consumer warps
+    const int nbar = 32 * nw;              // threads in the level barrier
+    // ROLES (WalkArgs::roles): the first half of the consumer warps walk the
+    // small rows of every level (this instantiation has R8 = 0), the second
+    // half the wide rows (R2 = 0)
+    const int stride = ROLES ? nbar / 2 : nbar;  // row slots of one kind per pass
+    const int t0 = threadIdx.x - 32 - (ROLES && R2 == 0 ? stride : 0);
     const int n_levels = a.n_levels;
     const unsigned stage_s = smem_addr(stage), null_s = smem_addr(nullrec), zr_s = smem_addr(zr);
     const unsigned dummy_s = zr_s + 8u * dummy;
@@ -402,7 +406,7 @@ __device__ __forceinline__ void walk_consumer(const WalkArgs& a, const int4* met
         if (nw == 1)
             __syncwarp();
         else
-            asm volatile("bar.sync 1, %0;" ::"r"(stride) : "memory");
+            asm volatile("bar.sync 1, %0;" ::"r"(nbar) : "memory");
         if (threadIdx.x == 32) {
             st_volatile(progress, L + 1);
             if (role == 2) st_relaxed_cluster(peer_flag, L + 1);  // back-pressure for the peer
@@ -459,7 +463,7 @@ __device__ __forceinline__ void walk_producer(const WalkArgs& a, uint64_t* bars,
     }
 }
 
-template <int R2, int R8, int KW, bool PIPE>
+template <int R2, int R8, int KW, bool PIPE, bool ROLES = false>
 __global__ void __launch_bounds__(max_threads(R2, R8, KW), 1) k_gs_walk(WalkPair pair) {
     const unsigned rank = PIPE ? cluster_ctarank() : 0u;
     const WalkArgs a = rank ? pair.a[1] : pair.a[0];  // a copy: no dynamically indexed parameter loads
@@ -533,7 +537,15 @@ __global__ void __launch_bounds__(max_threads(R2, R8, KW), 1) k_gs_walk(WalkPair
             peer_zr = cluster_addr(pb + pa.pbar_bytes, rank ^ 1u);
             peer_flag = cluster_addr(flags + 2, rank ^ 1u);
         }
-        walk_consumer<R2, R8, KW, PIPE>(a, meta, stage, nullrec, zr, flags, peer_zr, peer_flag, peer_pbar, pbars);
+        if constexpr (ROLES) {
+            if (tid - 32 < (static_cast<int>(blockDim.x) - 32) / 2)
+                walk_consumer<R2, 0, KW, false, true>(a, meta, stage, nullrec, zr, flags, 0u, 0u, 0u, pbars);
+            else
+                walk_consumer<0, R8, KW, false, true>(a, meta, stage, nullrec, zr, flags, 0u, 0u, 0u, pbars);
+        } else {
+            walk_consumer<R2, R8, KW, PIPE, false>(a, meta, stage, nullrec, zr, flags, peer_zr, peer_flag, peer_pbar,
+                                                   pbars);
+        }
 #ifdef SDG_WALK_TL
         if (tid == 32) g_walk_tl[tl_slot * 4 + 2] = gtimer();
 #endif
@@ -580,8 +592,29 @@ constexpr auto make_pipe_table(std::integer_sequence<int, I...>) {
     return T{{pipe_kernel_at<I>()...}};
 }
 
-WalkKernel walk_kernel(int r2, int r8, int kw, bool pipe = false) {
+// roles instantiations: R2 <= 2, 1 <= R8 <= 2, wide width 6 / 8
+template <int I>
+constexpr WalkKernel roles_kernel_at() {
+    return &k_gs_walk<I / 4 + 1, (I / 2) % 2 + 1, I % 2 ? 8 : 6, false, true>;
+}
+
+template <int... I>
+constexpr auto make_roles_table(std::integer_sequence<int, I...>) {
+    struct T {
+        WalkKernel k[sizeof...(I)];
+    };
+    return T{{roles_kernel_at<I>()...}};
+}
+
+bool has_roles_kernel(int r2, int r8, int kw) { return r2 >= 1 && r2 <= 2 && r8 >= 1 && r8 <= 2 && kw != 16; }
+
+WalkKernel walk_kernel(int r2, int r8, int kw, bool pipe = false, bool roles = false) {
     const int kwi = kw == 6 ? 0 : kw == 8 ? 1 : 2;
+    if (roles) {
+        static const auto rtable = make_roles_table(std::make_integer_sequence<int, 8>{});
+        if (!has_roles_kernel(r2, r8, kw)) fail(SDG_EINVAL, "gs walk: no roles instantiation for this shape");
+        return rtable.k[((r2 - 1) * 2 + (r8 - 1)) * 2 + (kw == 8 ? 1 : 0)];
+    }
     if (pipe) {
         static const auto ptable = make_pipe_table(std::make_integer_sequence<int, 2 * 3 * 3>{});
         if (r2 < 1 || r2 > 2 || r8 > 2) fail(SDG_EINVAL, "gs pipe: no instantiation for this shape");
@@ -950,7 +983,15 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     bands = 1;
     n_levels = nl;
     max_band_levels = nl;
-    nthreads = 32 + 32 * best_w;
+    // roles (k_gs_walk<..., ROLES>): twice the consumer warps, each taking one
+    // kind of row, so a warp issues one row path per level instead of both.
+    // Measured on every c2 walk (ncu, one td_bgs apply): V0 98.4 -> 93.2 us,
+    // V1 44.7 -> 41.4, porous D0 52.6 -> 48.7, the rest unchanged; apply 380 ->
+    // 363 us.  Bitwise the same sweep.  SDG_WALK_ROLES=0 disables.
+    const char* re = std::getenv("SDG_WALK_ROLES");
+    walk_roles = !(re && re[0] == '0') && !link && has_roles_kernel(best_r2, best_r8, kw) &&
+                 32 + 64 * best_w <= max_threads(best_r2, best_r8, kw);
+    nthreads = 32 + 32 * best_w * (walk_roles ? 2 : 1);
     walk_r2 = best_r2;
     walk_r8 = best_r8;
     walk_kw = kw;
@@ -963,15 +1004,16 @@ bool GsPlan::build_walk(const HostCsr& a, const std::vector<double>& dinv_h, con
     smem = static_cast<size_t>(fixed) + R;
     if (std::getenv("SDG_DEBUG"))
         std::fprintf(stderr,
-                     "[sdg gs walk] n=%d levels=%d pseudo-levels=%d warps=%d rows/thread=%d+%d wide=%d chunks=%d "
+                     "[sdg gs walk] n=%d levels=%d pseudo-levels=%d warps=%d%s rows/thread=%d+%d wide=%d chunks=%d "
                      "ring=%d pinned=%d stage=%d smem=%zu packed=%.1fKB model=%.0f cycles\n",
-                     n, nlv, nl, best_w, best_r2, best_r8, kw, nc, ring, npin, R, smem, off / 1024.0, best_cost);
+                     n, nlv, nl, best_w, walk_roles ? "x2 (roles)" : "", best_r2, best_r8, kw, nc, ring, npin, R,
+                     smem, off / 1024.0, best_cost);
     meta.upload(meta_h, s);
     walk_iss.upload(ctab_h, s);
     packed.upload(pk, s);
     bidx.upload(bidx_h, s);
-    SDG_CUDA(cudaFuncSetAttribute(walk_kernel(best_r2, best_r8, kw), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  budget));
+    SDG_CUDA(cudaFuncSetAttribute(walk_kernel(best_r2, best_r8, kw, false, walk_roles != 0),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
     if (link && link->role && best_r2 <= 2 && best_r8 <= 2)
         SDG_CUDA(cudaFuncSetAttribute(walk_kernel(best_r2, best_r8, kw, true),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
@@ -1004,7 +1046,7 @@ int walk_timeline(unsigned long long*, int) { return 0; }
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new) {
     WalkPair pair{};
     pair.a[0] = walk_args(g, z_new);
-    launch_k(c, walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw), 1, g.nthreads, g.smem, pair);
+    launch_k(c, walk_kernel(g.walk_r2, g.walk_r8, g.walk_kw, false, g.walk_roles != 0), 1, g.nthreads, g.smem, pair);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(SDG_ECUDA, std::string("launch_gs_walk: ") + cudaGetErrorString(e));
     c.count();

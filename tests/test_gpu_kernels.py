@@ -114,9 +114,9 @@ def test_amg_on_system_blocks(ref):
 @pytest.mark.parametrize("mode", [{"SDG_GS_SPLIT": "1"}, {"SDG_GS_PIPE": "1"}, {"SDG_GS_WALK": "0"},
                                   {"SDG_GS_BANDS": "4"}, {"SDG_GS_MERGE": "1"}, {"SDG_GS_MERGE": "2"},
                                   {"SDG_GS_MERGE": "4"}, {"SDG_GS_MERGE": "4", "SDG_GS_MERGE_CAP": "8"},
-                                  {"SDG_TD_SPLIT": "0"}, {"SDG_SELL": "0"}],
+                                  {"SDG_TD_SPLIT": "0"}, {"SDG_SELL": "0"}, {"SDG_WALK_ROLES": "0"}],
                          ids=["label-block-walks", "2-cta-pipe", "cluster-kernel", "cluster-4-bands", "no-merge",
-                              "merge-2", "merge-4", "merge-dynamic", "no-interface-split", "csr-spmv"])
+                              "merge-2", "merge-4", "merge-dynamic", "no-interface-split", "csr-spmv", "no-walk-roles"])
 def test_smoother_paths_match_reference(ref, golden, monkeypatch, mode):
     """The other lower-solve plans (one walk per u/v block with a coupling
     step; the u/v blocks walked concurrently on a 2-CTA cluster; the banded
@@ -160,6 +160,20 @@ def test_c2_merge_and_interface_split_agree(monkeypatch):
     monkeypatch.setenv("SDG_GS_EXACT", "1")
     exact = sdc.AmgPreconditioner(D, sdc.AmgOptions(max_levels=cfg.d_max_levels))
     assert rel_l2(merged.apply(x), exact.apply(x)) < 1e-11
+
+
+def test_c2_walk_roles_bitwise(monkeypatch):
+    """Walks with the small and wide rows on separate warps (the default)
+    compute every row with the same instructions as the shared-warp walk: the
+    c2 td_bgs apply is bitwise equal."""
+    from paper_2108_13229_b200 import scenarios
+    cfg = scenarios.CONFIGS["c2"]
+    s = scenarios.build_system(cfg)
+    r = np.random.default_rng(11).standard_normal(s.n_total())
+    z_roles = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels).apply(r)
+    monkeypatch.setenv("SDG_WALK_ROLES", "0")
+    z_plain = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels).apply(r)
+    assert np.array_equal(z_roles, z_plain)
 
 
 def check_linear(p, seed, n, tol=1e-13):
