@@ -147,6 +147,7 @@ struct Context {
     cudaStream_t side = nullptr, main_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     void side_begin();
+    void side_continue(cudaEvent_t after);  // like side_begin, but side waits for `after` only
     void side_end();
     void side_join();
 

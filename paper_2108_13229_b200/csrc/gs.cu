@@ -1300,7 +1300,7 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
     SDG_GS_CHECK();
 }
 
-void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
+void launch_gs_lower(Context& c, const GsPlan& g, double* z_new, cudaEvent_t mark) {
     if (g.pipe) {
         ProfScope ps_(c, PF_GS, g.packed_bytes() + 8.0 * g.n);
         launch_gs_pipe(c, g, z_new);
@@ -1316,7 +1316,7 @@ void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
                     const_cast<double*>(g.packed.get()));
                 SDG_GS_CHECK();
             }
-            launch_gs_lower(c, *g.parts[k], z_new + g.part_r0[k]);
+            launch_gs_lower(c, *g.parts[k], z_new + g.part_r0[k], k + 1 == g.parts.size() ? mark : nullptr);
         }
         return;
     }
@@ -1328,6 +1328,7 @@ void launch_gs_lower(Context& c, const GsPlan& g, double* z_new) {
         return;
     }
     if (g.walk) {
+        if (mark) SDG_CUDA(cudaEventRecord(mark, c.stream));
         launch_gs_walk(c, g, z_new);
         return;
     }

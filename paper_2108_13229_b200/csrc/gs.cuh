@@ -111,6 +111,15 @@ struct GsPlan {
         return static_cast<double>(packed_ptr ? part_doubles : packed.size() + chain_coef.size()) * 8.0;
     }
     const double* records() const { return packed_ptr ? packed_ptr : packed.get(); }
+    // a plain walk, or label-block walks: launch_gs_lower can record its mark
+    // after the last write to packed (prep, coupling steps) and before the last walk
+    bool can_mark() const {
+        if (pipe || merged) return false;
+        if (parts.empty()) return walk && !chain;
+        for (const auto& p : parts)
+            if (!p->walk || p->chain || !p->parts.empty() || p->merged) return false;
+        return true;
+    }
 
     // optional inputs / outputs of build_walk for the parts of a pipe
     struct Link {
@@ -158,7 +167,9 @@ void launch_gs_prep_pre(Context& c, const GsPlan& g, const double* r);
 void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const double* z,
                          const double* zc, const int* agg);
 // the level walk; writes z_new (natural order)
-void launch_gs_lower(Context& c, const GsPlan& g, double* z_new);
+// mark: recorded on the stream right before the last walk of the sweep is
+// launched, i.e. once every packed b of the sweep is final (GsPlan::can_mark)
+void launch_gs_lower(Context& c, const GsPlan& g, double* z_new, cudaEvent_t mark = nullptr);
 // lane-chain variant (plans with chain == true; gs_chain.cu)
 void launch_gs_chain(Context& c, const GsPlan& g, double* z_new);
 // single-CTA variant (plans with walk == true; gs_walk.cu)

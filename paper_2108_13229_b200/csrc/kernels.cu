@@ -91,6 +91,19 @@ __global__ void k_spmv(int n, const int* __restrict__ rp, const int* __restrict_
     y[i] = add ? __dadd_rn(y_in[i], __dmul_rn(alpha, sum)) : sum;
 }
 
+// k_spmv (add = 0) with x[j] = packed[bidx[j]] (BlockPrecond::setup_early_w)
+__global__ void k_spmv_packed(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                              const double* __restrict__ v, const int* __restrict__ bidx,
+                              const double* __restrict__ packed, double* __restrict__ y) {
+    pdl_begin();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double sum = 0.0;
+    row_fold<8>(ci, v, rp[i], rp[i + 1], [&](int j) { return packed[bidx[j]]; },
+                [&](double a, double xv) { sum = __dadd_rn(sum, __dmul_rn(a, xv)); });
+    y[i] = sum;
+}
+
 // BITWISE: sparse.cpp:81-90 / 98-108 over the SELL-32 copy (DevCsr::build_sell):
 // one thread per row still sums its entries in column order, but lane l of a
 // warp reads entry t of row 32 s + l at off + 32 t + l, so every value/column
@@ -665,6 +678,14 @@ static inline int stride_blocks(Context& c, int64_t n) {
         if (e_ != cudaSuccess)                                             \
             ::sdg::fail(SDG_ECUDA, std::string(__func__) + ": " + cudaGetErrorString(e_)); \
     } while (0)
+
+void launch_spmv_packed(Context& c, const DevCsr& a, const int* bidx, const double* packed, double* y) {
+    ProfScope ps_(c, PF_SPMV_BLOCK, 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 12.0 * a.n_cols + 8.0 * a.n_rows);
+    if (a.n_rows == 0) return;
+    launch_k(c, k_spmv_packed, blocks_for(a.n_rows), kThreads, 0, a.n_rows, a.rp.get(), a.ci.get(), a.v.get(), bidx,
+             packed, y);
+    SDG_LAUNCHED(c);
+}
 
 void launch_spmv(Context& c, const DevCsr& a, const double* x, double* y) {
     ProfScope ps_(c, a.sell ? PF_SPMV : PF_SPMV_BLOCK,

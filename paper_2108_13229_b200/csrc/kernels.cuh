@@ -38,6 +38,8 @@ int reduce_blocks(int n, int num_sms);
 // ---- sparse -------------------------------------------------------------
 // BITWISE spmv / spmv_add: y = A x, or y_out = y_in + alpha (A x).
 void launch_spmv(Context& c, const DevCsr& a, const double* x, double* y);
+// y = A x with x[j] read as packed[bidx[j]] (a Gauss-Seidel walk's staged b), CSR order
+void launch_spmv_packed(Context& c, const DevCsr& a, const int* bidx, const double* packed, double* y);
 void launch_spmv_add(Context& c, const DevCsr& a, const double* x, const double* y_in,
                      double* y_out, double alpha);
 // BITWISE forward SOR sweep over a level schedule; z_old may be null (zero).

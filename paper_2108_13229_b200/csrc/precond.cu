@@ -55,6 +55,14 @@ void Context::side_begin() {
     stream = side;
 }
 
+void Context::side_continue(cudaEvent_t after) {
+    if (!side) fail(SDG_EINVAL, "side_continue: no side stream yet");
+    if (main_stream) fail(SDG_EINVAL, "side_continue: already on the side stream");
+    SDG_CUDA(cudaStreamWaitEvent(side, after, 0));
+    main_stream = stream;
+    stream = side;
+}
+
 void Context::side_end() {
     if (!main_stream) fail(SDG_EINVAL, "side_end: not on the side stream");
     SDG_CUDA(cudaEventRecord(ev_join, side));
@@ -228,7 +236,7 @@ void AmgPrecond::vcycle(int lev, const double* r, double* z) {
         launch_restrict_warp(cx, L.a, L.pt_ptr.get(), L.pt_rows.get(), L.n_coarse, r, z, C.r.get(), seed);
         vcycle(lev + 1, C.r.get(), C.z.get());
         launch_gs_prep_post(cx, L.gs, r, z, C.z.get(), L.agg.get());  // fused prolongation
-        launch_gs_lower(cx, L.gs, z);
+        launch_gs_lower(cx, L.gs, z, lev == 0 ? post_mark : nullptr);
         return;
     }
     launch_gs_levels(cx, L.a, L.lvl_ptr.get(), L.lvl_rows.get(), L.n_sched, r, nullptr, z, 1.0);
@@ -300,6 +308,7 @@ BlockPrecond::BlockPrecond(CtxPtr c, int kind, const HostCsr& matrix, int n_v, i
         const HostCsr cp = submatrix(matrix, n_ff, n, 0, n_ff);
         c_prime_.upload(cp, cx.stream);
         setup_interface_split(cp);
+        if (n_gamma_ > 0) setup_early_w(matrix);
     }
     if (kind_ == SDG_PV_BGS) {
         c_.upload(submatrix(matrix, n_v_, n_ff, 0, n_v_), cx.stream);
@@ -375,6 +384,43 @@ void BlockPrecond::setup_interface_split(const HostCsr& cp) {
     n_gamma_ = m;
 }
 
+// Early interface correction.  w = (C' z_ff)_G reads z_v only in the columns
+// of C' (the interface velocities v(i,0), assembly.cpp:142-149, 274-275).
+// When those rows have no lower entries in V, the finest post-smoother of the
+// Uzawa V-cycle gives them z = b = (r - U z_old)/d, which sits in the walk's
+// packed buffer before the walk starts, and nothing after the V-cycle changes
+// z_v (precond.cpp:296-298 only writes z_p).  So w and z_pm -= K w run on the
+// side stream from the post-smoother's mark on, overlapping its walk, instead
+// of after the join.  w is summed in the order of launch_spmv (bitwise equal).
+void BlockPrecond::setup_early_w(const HostCsr& matrix) {
+    const char* e = std::getenv("SDG_TD_EARLY");
+    if (e && e[0] == '0') return;
+    auto* uz = dynamic_cast<UzawaPrecond*>(first_.get());
+    if (!uz) return;
+    AmgPrecond& amg = uz->inner_mut();
+    const GsPlan* plan = amg.markable_post_plan();
+    if (!plan || amg.post_mark) return;
+    const HostCsr cp = submatrix(matrix, n_v_ + n_pff_, matrix.n_rows, 0, n_v_ + n_pff_);
+    for (int i = 0; i < cp.n_rows; ++i)
+        for (int q = cp.rp[i]; q < cp.rp[i + 1]; ++q) {
+            const int j = cp.ci[q];
+            if (j >= n_v_) return;  // C' reads a free-flow pressure
+            for (int k = matrix.rp[j]; k < matrix.rp[j + 1]; ++k)
+                if (matrix.ci[k] < j) return;  // z_v(j) depends on the walk
+        }
+    SDG_CUDA(cudaEventCreateWithFlags(&early_ev_, cudaEventDisableTiming));
+    amg.post_mark = early_ev_;
+    early_plan_ = plan;
+}
+
+BlockPrecond::~BlockPrecond() {
+    if (early_ev_) {
+        if (auto* uz = dynamic_cast<UzawaPrecond*>(first_.get()))
+            if (uz->inner_mut().post_mark == early_ev_) uz->inner_mut().post_mark = nullptr;
+        cudaEventDestroy(early_ev_);
+    }
+}
+
 int64_t BlockPrecond::setup_memory_doubles() const {
     return first_->setup_memory_doubles() + pm_->setup_memory_doubles() + c_prime_.nnz + c_.nnz +
            c1_prime_.nnz + static_cast<int64_t>(n_ppm_) * n_gamma_;
@@ -410,6 +456,15 @@ void BlockPrecond::do_apply(const double* r, double* z) {
             }
             if (fork) cx.side_end();
             first_->apply(r, z);
+            if (fork && early_ev_) {  // see setup_early_w
+                cx.side_continue(early_ev_);
+                launch_spmv_packed(cx, c_gamma_, early_plan_->bidx.get(), early_plan_->packed.get(),
+                                   w_gamma_.get());
+                launch_colmajor_gemv_sub(cx, n_ppm_, n_gamma_, k_gamma_.get(), w_gamma_.get(), z + n_ff);
+                cx.side_end();
+                cx.side_join();
+                break;
+            }
             launch_spmv(cx, c_gamma_, z, w_gamma_.get());
             if (fork) cx.side_join();
             launch_colmajor_gemv_sub(cx, n_ppm_, n_gamma_, k_gamma_.get(), w_gamma_.get(), z + n_ff);

@@ -87,6 +87,14 @@ public:
     int num_levels() const { return static_cast<int>(levels_.size()); }
     int level_rows(int l) const { return levels_[l].a.n_rows; }
     int64_t level_nnz(int l) const { return levels_[l].a.nnz; }
+    // the finest level's post-smoother: its plan (null unless it is a walk
+    // that can record a mark) and the event recorded once its packed b values
+    // are final (BlockPrecond's early interface correction)
+    const GsPlan* markable_post_plan() const {
+        return !levels_.empty() && levels_[0].fast && num_levels() > 1 && levels_[0].gs.can_mark() ? &levels_[0].gs
+                                                                                                    : nullptr;
+    }
+    cudaEvent_t post_mark = nullptr;
 
 protected:
     void do_apply(const double* r, double* z) override;
@@ -127,6 +135,7 @@ public:
     }
     int64_t work_per_apply() const override { return inner_->work_per_apply() + c_.nnz + n_p_; }
     const AmgPrecond& inner() const { return *inner_; }
+    AmgPrecond& inner_mut() { return *inner_; }
 
 protected:
     void do_apply(const double* r, double* z) override;
@@ -165,6 +174,14 @@ private:
     DevCsr c_gamma_;               // the interface rows of C'
     DevBuf<double> w_gamma_;       // (C' z_ff) on those rows
     DevBuf<double> k_gamma_;       // P_D' e_g for every interface row g, column-major
+    // early correction: w and z_pm -= K w on the side stream as soon as the
+    // Uzawa V-cycle's finest post-smoother has its packed b (setup_early_w)
+    void setup_early_w(const HostCsr& matrix);
+    cudaEvent_t early_ev_ = nullptr;
+    const GsPlan* early_plan_ = nullptr;
+
+public:
+    ~BlockPrecond() override;
 };
 
 // Krylov drivers on device vectors; host control flow mirrors krylov.cpp.

@@ -114,9 +114,11 @@ def test_amg_on_system_blocks(ref):
 @pytest.mark.parametrize("mode", [{"SDG_GS_SPLIT": "1"}, {"SDG_GS_PIPE": "1"}, {"SDG_GS_WALK": "0"},
                                   {"SDG_GS_BANDS": "4"}, {"SDG_GS_MERGE": "1"}, {"SDG_GS_MERGE": "2"},
                                   {"SDG_GS_MERGE": "4"}, {"SDG_GS_MERGE": "4", "SDG_GS_MERGE_CAP": "8"},
-                                  {"SDG_TD_SPLIT": "0"}, {"SDG_SELL": "0"}, {"SDG_WALK_ROLES": "0"}],
+                                  {"SDG_TD_SPLIT": "0"}, {"SDG_SELL": "0"}, {"SDG_WALK_ROLES": "0"},
+                                  {"SDG_TD_EARLY": "0"}],
                          ids=["label-block-walks", "2-cta-pipe", "cluster-kernel", "cluster-4-bands", "no-merge",
-                              "merge-2", "merge-4", "merge-dynamic", "no-interface-split", "csr-spmv", "no-walk-roles"])
+                              "merge-2", "merge-4", "merge-dynamic", "no-interface-split", "csr-spmv", "no-walk-roles",
+                              "late-interface-gemv"])
 def test_smoother_paths_match_reference(ref, golden, monkeypatch, mode):
     """The other lower-solve plans (one walk per u/v block with a coupling
     step; the u/v blocks walked concurrently on a 2-CTA cluster; the banded
@@ -174,6 +176,24 @@ def test_c2_walk_roles_bitwise(monkeypatch):
     monkeypatch.setenv("SDG_WALK_ROLES", "0")
     z_plain = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels).apply(r)
     assert np.array_equal(z_roles, z_plain)
+
+
+@pytest.mark.parametrize("split", ["0", "1"], ids=["whole-v0-walk", "label-block-walks"])
+def test_c2_early_interface_correction_bitwise(monkeypatch, split):
+    """td_bgs with the interface GEMV started on the side stream from the
+    Uzawa post-smoother's mark (the default) against the GEMV after the join:
+    bitwise equal, for a whole V0 walk and for label-block walks."""
+    from paper_2108_13229_b200 import scenarios
+    monkeypatch.setenv("SDG_GS_SPLIT", split)
+    cfg = scenarios.CONFIGS["c2"]
+    s = scenarios.build_system(cfg)
+    r = np.random.default_rng(5).standard_normal(s.n_total())
+    early = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
+    z_early = [early.apply(r), early.apply(2.0 * r)]
+    monkeypatch.setenv("SDG_TD_EARLY", "0")
+    late = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels, omega_override=early.omega())
+    z_late = [late.apply(r), late.apply(2.0 * r)]
+    assert all(np.array_equal(a, b) for a, b in zip(z_early, z_late))
 
 
 def check_linear(p, seed, n, tol=1e-13):
