@@ -9,9 +9,13 @@ public host-pointer C-ABI call (sdg_bicgstab / sdg_pd_gmres: host->device copy
 of b and device->host copy of x inside the timed region).  One step = one full
 preconditioned solve of the workload's system.
 
-Workload (N=1): BASELINE.json configs[1] = "c2": 160 x 160 cells per
-subdomain (102,720 DoF), log-normal K, BiCGSTAB with td_bgs(Uzawa(AMG_V),
-AMG_D').  Other configs are parity cases (tests/) and can be run with --config.
+Workload (N=1): BASELINE.json configs[2] = "c3": 500 x 500 cells per
+subdomain (1,001,000 DoF), K = 1e-2, GMRES(50) with td_bgs(Uzawa(AMG_V),
+AMG_D'), 3 AMG levels -- the largest configuration that runs on one GPU and is
+pinned against the reference at full size (165 = 165 iterations,
+tests/test_gpu_solvers.py).  c4 (one bench step = ten implicit-Euler solves,
+minutes) and c5 (partitioned, 16 M DoF) run with --config; c1/c2 are parity
+cases.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -43,10 +47,11 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--ref-threads", type=int, default=64,
+                    help="reference arm: concurrent reference samples (capped at the usable host cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-solves", type=int, default=1)
     ap.add_argument("--coupling-iterations", type=int, default=0,
                     help="config 5: cap the Dirichlet-Neumann loop (0 = run to convergence)")
     ap.add_argument("--sharded", action="store_true",
@@ -138,10 +143,10 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def workload_desc(cfg, s):
+def workload_desc(cfg, n_dof):
     solver = {"bicgstab": "BiCGSTAB", "gmres50": "GMRES(50)", "pdgmres": "PD-GMRES"}[cfg.solver]
     k = "log-normal K (log10 K ~ N(0,1), seed 13229)" if cfg.lognormal else f"K={cfg.permeability:g}"
-    return (f"{cfg.name}: {cfg.n}x{cfg.n} cells per subdomain, {s.n_total():,} DoF, {k}, {solver} + "
+    return (f"{cfg.name}: {cfg.n}x{cfg.n} cells per subdomain, {n_dof:,} DoF, {k}, {solver} + "
             f"td_bgs(Uzawa(AMG_V), AMG_D'), AMG levels V{cfg.v_max_levels}/D{cfg.d_max_levels}, tol 1e-8*||b||")
 
 
@@ -159,77 +164,179 @@ def solve_host(sdc, cfg, s, p, b, tol):
     return sdc.pd_gmres(s.matrix, p, b, tol, 4000, ctrl)
 
 
-def reference_solve(R, rs, rtd, cfg, b, tol):
-    if cfg.solver == "bicgstab":
-        return R.bicgstab(rs.a, b, tol, 20000, precond=rtd)
-    if cfg.solver == "gmres50":
-        return R.pd_gmres(rs.a, b, tol, 4000, precond=rtd, m_init=50, m_min=50, m_max=50)
-    return R.pd_gmres(rs.a, b, tol, 4000, precond=rtd)
-
-
-def ref_system(s):
-    from oracle.refpy import Csr, System
-    return System(s.n_total(), s.n_u, s.n_vel, s.n_pff, s.n_ppm,
-                  Csr(s.n_total(), s.n_total(), s.matrix.row_offsets, s.matrix.col_indices, s.matrix.values), s.rhs)
-
-
-def cpu_baseline(cfg, s, tol, solves):
-    """The reference's own CPU solver (oracle/_ref) on the same system, 1 core."""
+def host_cpu():
+    """CPU model and core counts of this host (for the cpu_baseline records)."""
+    model = None
     try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        usable = os.cpu_count()
+    return {"cpu_model": model, "host_logical_cpus": os.cpu_count(), "usable_cpus": usable}
+
+
+def ref_system_for(R, cfg):
+    """The workload's system on the reference side.  Uniform K, stationary
+    (c1, c2u, c3): the reference's own assemble_monolithic (oracle harness
+    ref_system_new) -- no repo code is loaded.  The log-normal field (c2, c4)
+    is an extension the reference cannot express: the repo's host assembly,
+    bitwise the reference's for uniform K (tests/test_host.py), builds it."""
+    from oracle.refpy import Csr, System
+    if not cfg.lognormal and math.isinf(cfg.dt):
+        return R.assemble(cfg.n, permeability=cfg.permeability), "reference assemble_monolithic (oracle/_ref)"
+    from paper_2108_13229_b200 import scenarios
+    s = scenarios.build_system(cfg)
+    n = s.n_total()
+    return (System(n, s.n_u, s.n_vel, s.n_pff, s.n_ppm,
+                   Csr(n, n, s.matrix.row_offsets, s.matrix.col_indices, s.matrix.values), s.rhs),
+            "repo host assembly (log-normal K extension; bitwise the reference for uniform K)")
+
+
+def ref_sample(R, rm, rtd, cfg, b, tol):
+    """One bounded step of the reference CPU path on the workload: for
+    GMRES(50) its first restart cycle (krylov.cpp:80-167 with max_restarts = 1:
+    50 Arnoldi steps, the cycle-end update and the true residual); for
+    BiCGSTAB / PD-GMRES the whole solve."""
+    if cfg.solver == "bicgstab":
+        return R.bicgstab(rm, b, tol, 20000, precond=rtd)
+    if cfg.solver == "gmres50":
+        return R.pd_gmres(rm, b, tol, 1, precond=rtd, m_init=50, m_min=50, m_max=50)
+    return R.pd_gmres(rm, b, tol, 4000, precond=rtd)
+
+
+SAMPLE_DESC = {"gmres50": "the first GMRES(50) restart cycle (50 Arnoldi steps + cycle end)",
+               "bicgstab": "one full BiCGSTAB solve", "pdgmres": "one full PD-GMRES solve"}
+
+
+class RefSetup:
+    """The reference's td_bgs setup (amg_setup + coarse lu_factor + power
+    iteration) on its own system, started in a background thread: the ctypes
+    call releases the GIL, so it overlaps the GPU measurement (c3's coarse
+    lu_factor alone takes minutes on one core)."""
+
+    def __init__(self, cfg):
         from oracle.refpy import RefLib
-        R = RefLib()
-    except Exception as e:  # pragma: no cover - only when the oracle was not built
+        self.cfg = cfg
+        self.R = RefLib()
+        self.error = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        try:
+            t0 = time.perf_counter()
+            self.rs, self.assembly = ref_system_for(self.R, self.cfg)
+            self.assembly_s = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            self.rtd = self.R.td(self.rs, "td_bgs", self.cfg.v_max_levels, self.cfg.d_max_levels)
+            self.setup_s = time.perf_counter() - t0
+        except Exception as e:  # reported in the JSON line
+            self.error = f"{type(e).__name__}: {e}"
+
+    def wait(self):
+        self.t.join()
+        if self.error:
+            raise RuntimeError(self.error)
+        return self
+
+
+def cpu_baseline(setup: RefSetup):
+    """The reference's own CPU path (oracle/_ref, single-threaded C++) on the
+    workload, 1 core: one bounded sample (ref_sample) after its setup."""
+    try:
+        st = setup.wait()
+    except Exception as e:  # pragma: no cover - only when the oracle was not built / failed
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
-    rs = ref_system(s)
-    t0 = time.perf_counter()
-    rtd = R.td(rs, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
-    setup = time.perf_counter() - t0
-    its, secs = 0, 0.0
-    for _ in range(solves):
+    cfg, R, rs = st.cfg, st.R, st.rs
+    from oracle.refpy import RefMatrix
+    tol = 1e-8 * float(np.linalg.norm(rs.rhs))
+    with RefMatrix(R, rs.a) as rm:
         t0 = time.perf_counter()
-        _, rep = reference_solve(R, rs, rtd, cfg, s.rhs, tol)
-        secs += time.perf_counter() - t0
-        its += rep.iterations
-    return {"value": s.n_total() * its / secs, "unit": UNIT, "cores": 1, "kind": "reference",
-            "sample": f"{solves} full solve(s) of {cfg.name} ({its // solves} iterations each) with the compiled "
-                      f"reference (oracle/_ref, single-threaded), setup {setup:.2f} s excluded",
-            "solve_s": secs / solves, "iterations": its // solves, "setup_s": setup}
+        _, rep = ref_sample(R, rm, st.rtd, cfg, rs.rhs, tol)
+        secs = time.perf_counter() - t0
+    return {"value": rs.n * rep.iterations / secs, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{SAMPLE_DESC[cfg.solver]} of {cfg.name} by the compiled reference (oracle/_ref, "
+                      f"single-threaded), {rep.iterations} iterations; setup {st.setup_s:.1f} s excluded "
+                      f"(run in a background thread beside the GPU measurement)",
+            "sample_s": secs, "iterations": rep.iterations, "setup_s": st.setup_s, "system": st.assembly,
+            **host_cpu()}
 
 
 def run_reference(args):
+    """The reference arm: the unmodified reference CPU path (oracle/_ref,
+    compiled from /root/reference by oracle/Makefile) on the same workload,
+    on all usable host cores -- independent concurrent samples sharing one
+    setup (a Preconditioner is const and reentrant, operator.hpp:30-33), the
+    way the reference's own bench runs independent cells on a thread pool
+    (bench.cpp:438-457).  Rank 0 only."""
     rank, local_rank, world = dist_env()
     if rank != 0:
         return 0
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.refpy import RefMatrix
     from paper_2108_13229_b200 import scenarios
-    from oracle.refpy import RefLib
     cfg = scenarios.CONFIGS[args.config]
-    s = scenarios.build_system(cfg)
-    tol = 1e-8 * float(np.linalg.norm(s.rhs))
-    R = RefLib()
-    rs = ref_system(s)
-    t0 = time.perf_counter()
-    rtd = R.td(rs, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
-    setup = time.perf_counter() - t0
+    st = RefSetup(cfg).wait()
+    R, rs = st.R, st.rs
+    tol = 1e-8 * float(np.linalg.norm(rs.rhs))
+    cpu = host_cpu()
+    threads = max(1, min(cpu["usable_cpus"] or 1, args.ref_threads))
+    rms = [RefMatrix(R, rs.a) for _ in range(threads)]
+
+    def batch():
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            reps = list(ex.map(lambda rm: ref_sample(R, rm, st.rtd, cfg, rs.rhs, tol)[1], rms))
+        return sum(r.iterations for r in reps)
+
     for _ in range(args.warmup):
-        reference_solve(R, rs, rtd, cfg, s.rhs, tol)
+        batch()
     times, its = [], []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        _, rep = reference_solve(R, rs, rtd, cfg, s.rhs, tol)
+        its.append(batch())
         times.append(time.perf_counter() - t0)
-        its.append(rep.iterations)
-    value = s.n_total() * sum(its) / sum(times)
+    for rm in rms:
+        rm.close()
+    value = rs.n * sum(its) / sum(times)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_desc(cfg, s), "dof": s.n_total(), "nnz": s.matrix.nnz(),
-                       "iterations": its, "setup_s": setup},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
-                             "sample": f"each step = 1 full solve of {cfg.name} by the compiled reference "
-                                       f"(single-threaded C++; its solver uses one core)"},
+            "config": {"workload": workload_desc(cfg, rs.n), "dof": rs.n, "nnz": rs.a.nnz(),
+                       "iterations_per_step": its, "setup_s": st.setup_s, "system": st.assembly},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"each step = {threads} concurrent samples ({SAMPLE_DESC[cfg.solver]} of "
+                                       f"{cfg.name}) by the compiled reference, one per core, sharing one setup",
+                             **cpu},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def roofline_entry(prof, fam, peak, peak_kind, step_ms, traffic):
+    """Achieved algorithmic bytes per launch / mean launch time of one kernel
+    family (CUDA events around every launch on its own stream, one profiled
+    solve), against the measured HBM peak."""
+    f = prof[fam]
+    per_launch_ms = f["ms"] / f["launches"]
+    per_launch_bytes = f["bytes"] / f["launches"]
+    ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    t = traffic.get(fam)
+    return {"kernel": fam, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "peak_source": peak_kind, "traffic": t["dram_bytes_per_launch"] if t else None,
+            "traffic_note": (t["kernel"] + "; " + t["source"]) if t else None,
+            "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms, "launches": f["launches"],
+            "share_of_kernel_time": f["ms"] / sum(v["ms"] for v in prof.values()),
+            # two streams overlap (td_bgs: the porous V-cycle runs beside the
+            # Uzawa one), so family shares of the step can add up to more than 1
+            "share_of_step": f["ms"] / step_ms}
 
 
 def run_ours(args):
@@ -243,6 +350,8 @@ def run_ours(args):
     from paper_2108_13229_b200 import scenarios, sdc
 
     cfg = scenarios.CONFIGS[args.config]
+    # the reference's own setup for the cpu_baseline, beside the GPU work
+    ref_setup = RefSetup(cfg) if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     t0 = time.perf_counter()
     s = scenarios.build_system(cfg)
     assembly_s = time.perf_counter() - t0
@@ -300,7 +409,8 @@ def run_ours(args):
     x_host = x_dev.cpu().numpy()
     true_res = float(np.linalg.norm(s.rhs - sdc.spmv(s.matrix, x_host)))
 
-    # e2e through the public host-pointer C-ABI call
+    # e2e through the public host-pointer C-ABI call (sdg_pd_gmres / sdg_bicgstab):
+    # H2D of b from pinned memory and D2H of x inside the timed region
     e2e = None
     if not args.no_e2e:
         b_pin = torch.from_numpy(s.rhs.copy()).pin_memory()
@@ -318,31 +428,24 @@ def run_ours(args):
         e2e = {"value": e_work / e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                "ms_per_step": 1e3 * e_s / args.steps, "timing": "host wall clock around the synchronous C-ABI call"}
 
-    # live per-kernel-family profile of one more solve (CUDA events on the library stream)
+    # live per-kernel-family profile of one more solve (CUDA events on the
+    # stream each kernel is launched on)
     ctx.set_profiling(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
     step()
+    with torch.cuda.stream(stream):
+        e1.record(stream)
+    torch.cuda.synchronize()
+    prof_step_ms = e0.elapsed_time(e1)
     prof = ctx.profile()
     ctx.set_profiling(False)
     peak, peak_kind = measured_peak_gbs()
-
-    def roof(fam):
-        f = prof[fam]
-        per_launch_ms = f["ms"] / f["launches"]
-        per_launch_bytes = f["bytes"] / f["launches"]
-        ach = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
-        t = traffic.get(fam)
-        return {"kernel": fam, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "peak_source": peak_kind,
-                "traffic": t["dram_bytes_per_launch"] if t else None,
-                "traffic_note": t["kernel"] + "; " + t["source"] if t else None,
-                "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms, "launches": f["launches"],
-                "share_of_step": f["ms"] / sum(v["ms"] for v in prof.values())}
-
-    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     traffic = {}
-    try:
+    try:  # DRAM bytes per launch from the committed ncu --set full captures (profiles/)
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f)
+            traffic = {k: v for k, v in json.load(f).items() if v.get("config") == cfg.name}
     except Exception:
         pass
     dominant = max(prof, key=lambda k: prof[k]["ms"])
@@ -350,23 +453,27 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg, s), "dof": n, "nnz": s.matrix.nnz(),
+        "config": {"workload": workload_desc(cfg, n), "dof": n, "nnz": s.matrix.nnz(),
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                    "l2": "flushed between timed solves (256 MiB write, outside the event pair)",
                    "iterations": iters, "setup_s": setup_s, "assembly_s": assembly_s,
                    "hierarchy_v": hier_v, "hierarchy_d": hier_d, "omega": p.omega(),
+                   "fast_paths": sorted(p.features()),
                    "true_residual_rel": true_res / float(np.linalg.norm(s.rhs))},
         "solve_ms": total_ms / args.steps,
-        "roofline": roof(dominant),
-        "spmv_roofline": roof("spmv") if "spmv" in prof else None,
+        "roofline": roofline_entry(prof, dominant, peak, peak_kind, prof_step_ms, traffic),
+        "other_rooflines": {k: roofline_entry(prof, k, peak, peak_kind, prof_step_ms, traffic)
+                            for k in ("spmv", "gs_wave", "coarse", "iface", "ortho")
+                            if k in prof and k != dominant},
         "kernel_profile": {k: {"launches": v["launches"], "ms": v["ms"], "GBps": v["bytes"] / v["ms"] / 1e6}
                            for k, v in prof.items()},
+        "profiled_solve_ms": prof_step_ms,
         "gpu_launches": launches,
         "clocks": clk,
         "e2e": e2e,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, s, tol, args.cpu_sample_solves)
+    if ref_setup is not None:
+        line["cpu_baseline"] = cpu_baseline(ref_setup)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -467,7 +574,7 @@ def run_transient(args):
         "metric": METRIC, "value": work / (total_ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg, s1) + f", implicit Euler dt={cfg.dt} x{cfg.steps}, warm-started",
+        "config": {"workload": workload_desc(cfg, s1.n_total()) + f", implicit Euler dt={cfg.dt} x{cfg.steps}, warm-started",
                    "dof": n, "nnz": s1.matrix.nnz(), "parallelism": "single GPU",
                    "l2": f"inputs exceed the 126 MB L2 (matrix {12 * s1.matrix.nnz() / 1e6:.0f} MB)",
                    "iterations_per_time_step": iters[-1], "setup_s": setup_s, "assembly_s": assembly_s,
@@ -629,7 +736,7 @@ def run_sharded(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg, s), "dof": n, "nnz": s.matrix.nnz(),
+        "config": {"workload": workload_desc(cfg, s.n_total()), "dof": n, "nnz": s.matrix.nnz(),
                    "parallelism": f"horizontal strips x{world} (processor-block GS inside strips, NCCL halos)",
                    "l2": "flushed between timed solves (256 MiB write, outside the event pair)",
                    "iterations": iters, "setup_s": setup_s, "omega": p.omega(), "local_rows": ds.n_local()},

@@ -128,8 +128,9 @@ int64_t sdg_context_launches(sdg_context* ctx);
  * (SURVEY.md §8(d) byte model); sdg_context_profile folds them per kernel
  * family.  Enabling clears previous totals.  Families: 0 spmv, 1 gs,
  * 2 restrict, 3 prolong, 4 coarse, 5 uzawa, 6 ortho, 7 bicg, 8 vec, 9 setup,
- * 10 gsprep. */
-#define SDG_PROF_FAMILIES 11
+ * 10 gsprep, 11 spmv_block, 12 gs_wave (the multi-SM wavefront smoother of
+ * the structured finest levels), 13 iface (td_bgs interface GEMV). */
+#define SDG_PROF_FAMILIES 14
 int sdg_context_set_profiling(sdg_context* ctx, int enable);
 int sdg_context_profile(sdg_context* ctx, int family, int64_t* launches, double* total_ms,
                         double* total_bytes);
@@ -211,6 +212,16 @@ int sdg_precond_hierarchy(const sdg_precond* p, int which, int* n_levels, int* r
                           int64_t* nnz, int capacity);
 /* Use CUDA-graph capture for device applies (default on). */
 int sdg_precond_set_graphs(sdg_precond* p, int enable);
+/* Which fast paths a handle runs (diagnostic / test query; no reference
+ * counterpart).  Bits: the td_bgs interface split, the early interface
+ * correction (both BlockPrecond), the multi-SM wavefront smoother on the
+ * finest velocity / porous level (an AMG or Uzawa handle reports its own
+ * finest level in SDG_FEAT_WAVE_V). */
+#define SDG_FEAT_SPLIT 1
+#define SDG_FEAT_EARLY 2
+#define SDG_FEAT_WAVE_V 4
+#define SDG_FEAT_WAVE_D 8
+int sdg_precond_features(const sdg_precond* p, int* features);
 
 /* ---- Krylov solvers (krylov.cpp) ----------------------------------------
  * precond may be NULL (identity, krylov.cpp:19-25).  x starts at zero

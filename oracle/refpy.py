@@ -322,27 +322,35 @@ class RefLib:
             return 3, precond.h
         raise TypeError(precond)
 
-    def pd_gmres(self, a: Csr, b, tol_abs, max_restarts, precond=None, m_init=3, m_min=3,
+    def pd_gmres(self, a, b, tol_abs, max_restarts, precond=None, m_init=3, m_min=3,
                  m_step=5, m_max=53, hist_cap=1 << 16):
+        """`a`: a Csr (copied into a reference SparseMatrix for the call) or a
+        RefMatrix handle (borrowed, as LinearOperator::from_matrix does)."""
         kind, ph = self._precond_args(precond)
         x = np.empty(a.n_rows)
         it, fr, cv, wt, hl = _i(), _d(), _i(), _d(), _i()
         hist = np.empty(hist_cap)
-        with self.matrix(a) as m:
+        with self._borrow(a) as m:
             self._check(self.L.ref_pd_gmres(m.h, kind, ph, _f64(b), tol_abs, max_restarts, m_init, m_min,
                                             m_step, m_max, x, C.byref(it), C.byref(fr), C.byref(cv),
                                             C.byref(wt), hist, hist_cap, C.byref(hl)))
         return x, SolveReport(it.value, fr.value, bool(cv.value), wt.value, hist[: min(hl.value, hist_cap)].copy())
 
-    def bicgstab(self, a: Csr, b, tol_abs, max_iters, precond=None, hist_cap=1 << 16):
+    def bicgstab(self, a, b, tol_abs, max_iters, precond=None, hist_cap=1 << 16):
         kind, ph = self._precond_args(precond)
         x = np.empty(a.n_rows)
         it, fr, cv, wt, hl = _i(), _d(), _i(), _d(), _i()
         hist = np.empty(hist_cap)
-        with self.matrix(a) as m:
+        with self._borrow(a) as m:
             self._check(self.L.ref_bicgstab(m.h, kind, ph, _f64(b), tol_abs, max_iters, x, C.byref(it),
                                             C.byref(fr), C.byref(cv), C.byref(wt), hist, hist_cap, C.byref(hl)))
         return x, SolveReport(it.value, fr.value, bool(cv.value), wt.value, hist[: min(hl.value, hist_cap)].copy())
+
+    def _borrow(self, a):
+        if isinstance(a, RefMatrix):
+            import contextlib
+            return contextlib.nullcontext(a)
+        return self.matrix(a)
 
     def power_iteration(self, a: Csr, tol_rel, max_iters, seed):
         v, it, cv = _d(), _i(), _i()
@@ -358,11 +366,19 @@ class RefMatrix:
         self.h = _vp()
         lib._check(lib.L.ref_matrix_new(a.n_rows, a.n_cols, _i32(a.rowptr), _i32(a.col), _f64(a.val), C.byref(self.h)))
 
+    @property
+    def n_rows(self) -> int:
+        return self.a.n_rows
+
     def __enter__(self):
         return self
 
     def __exit__(self, *exc):
-        self.lib.L.ref_matrix_free(self.h)
+        self.close()
+
+    def close(self):
+        if self.h:
+            self.lib.L.ref_matrix_free(self.h)
         self.h = None
 
 

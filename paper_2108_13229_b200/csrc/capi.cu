@@ -105,10 +105,14 @@ int sdg_context_profile(sdg_context* ctx, int family, int64_t* launches, double*
 }
 
 extern "C" int sdg_debug_walk_timeline(unsigned long long* out, int max) { return sdg::walk_timeline(out, max); }
+extern "C" int sdg_debug_wave_timeline(unsigned long long* out, int max_bands) {
+    return sdg::wave_timeline_copy(out, max_bands);
+}
 
 const char* sdg_profile_family_name(int family) {
     static const char* names[] = {"spmv", "gs", "restrict", "prolong", "coarse",
-                                  "uzawa", "ortho", "bicg", "vec", "setup", "gsprep", "spmv_block"};
+                                  "uzawa", "ortho", "bicg", "vec", "setup", "gsprep", "spmv_block",
+                                  "gs_wave", "iface"};
     return (family >= 0 && family < sdg::PF_COUNT) ? names[family] : "?";
 }
 
@@ -326,6 +330,28 @@ int sdg_precond_hierarchy(const sdg_precond* p, int which, int* n_levels, int* r
             rows[l] = amg->level_rows(l);
             nnz[l] = amg->level_nnz(l);
         }
+    });
+}
+
+int sdg_precond_features(const sdg_precond* p, int* features) {
+    return guard([&] {
+        need(p, "sdg_precond_features");
+        need(features, "sdg_precond_features");
+        int f = 0;
+        auto amg_of = [](const sdg::PrecondPtr& q) -> const sdg::AmgPrecond* {
+            if (const sdg::AmgPrecond* a = as_amg(q)) return a;
+            if (auto* uz = dynamic_cast<sdg::UzawaPrecond*>(q.get())) return &uz->inner();
+            return nullptr;
+        };
+        if (auto* blk = dynamic_cast<sdg::BlockPrecond*>(p->p.get())) {
+            if (blk->interface_split()) f |= SDG_FEAT_SPLIT;
+            if (blk->early_correction()) f |= SDG_FEAT_EARLY;
+            if (const sdg::AmgPrecond* a = amg_of(blk->first()); a && a->finest_wave()) f |= SDG_FEAT_WAVE_V;
+            if (const sdg::AmgPrecond* a = amg_of(blk->pm()); a && a->finest_wave()) f |= SDG_FEAT_WAVE_D;
+        } else if (const sdg::AmgPrecond* a = amg_of(p->p); a && a->finest_wave()) {
+            f |= SDG_FEAT_WAVE_V;
+        }
+        *features = f;
     });
 }
 

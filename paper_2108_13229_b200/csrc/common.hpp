@@ -109,6 +109,8 @@ enum ProfFamily {
     PF_SETUP,         // setup-only kernels
     PF_GSPREP,        // smoother prep (upper part, fused prolongation)
     PF_SPMV_BLOCK,    // CSR SpMV of the blocks (C', Uzawa B / C) and small operators
+    PF_GS_WAVE,       // Gauss-Seidel lower solve of the structured finest levels (multi-SM wavefront)
+    PF_IFACE,         // td_bgs interface correction z_pm -= K w (column-major GEMV)
     PF_COUNT
 };
 
@@ -146,6 +148,7 @@ struct Context {
     // Events only, so this also works under graph capture.
     cudaStream_t side = nullptr, main_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t step_ev[2] = {nullptr, nullptr};  // GMRES: Arnoldi read-back done (krylov.cu)
     void side_begin();
     void side_continue(cudaEvent_t after);  // like side_begin, but side waits for `after` only
     void side_end();

@@ -635,12 +635,24 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
         upper.upload(up, s);
         SDG_CUDA(cudaStreamSynchronize(s));
     };
-    const char* split_env = std::getenv("SDG_GS_SPLIT");  // test knob: sequential label-block walks
+    // test knobs (SDG_GS_SPLIT, SDG_GS_PIPE, SDG_GS_MERGE, SDG_GS_WAVE) apply to
+    // every matrix, or only to those with SDG_GS_KNOB_ROWS rows
+    const char* knob_rows = std::getenv("SDG_GS_KNOB_ROWS");
+    const bool knobs = !knob_rows || std::atoi(knob_rows) == n;
+    auto knob = [&](const char* name) { return knobs ? std::getenv(name) : nullptr; };
+    const char* split_env = knob("SDG_GS_SPLIT");  // sequential label-block walks
     const bool force_split = split_env && split_env[0] == '1';
-    const char* pipe_env = std::getenv("SDG_GS_PIPE");
+    const char* pipe_env = knob("SDG_GS_PIPE");
     const bool try_pipe = !force_split && pipe_env && pipe_env[0] == '1';  // opt-in
-    // 0. the lane chain, when the matrix is a structured finest level
-    if (want_walk && build_chain(a, comps, dinv_h, s)) return finish();
+    const char* wave_env = knob("SDG_GS_WAVE");
+    const bool wave_off = wave_env && wave_env[0] == '0';
+    row_has_lower.assign(n, 0);
+    for (int i = 0; i < n; ++i) row_has_lower[i] = nlow[i] > 0;
+    // 0. the multi-SM wavefront, when the matrix is a structured finest level
+    // (the knobs that force another plan skip it)
+    if (want_walk && !wave_off && !force_split && !try_pipe && !knob("SDG_GS_MERGE") &&
+        build_wave(a, comps, dinv_h, s))
+        return finish();
     // 0b. one walk over merged levels: the first candidate, in the order
     //     (dynamic groups of <= 4 levels with <= 8 entries per row, fixed
     //     k = 4, 3, 2), whose modelled sweep (walk_model_cost, corrected form)
@@ -652,8 +664,8 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     //     (with SDG_GS_MERGE_CAP=c: dynamic groups of <= k levels, <= c
     //     entries), 1 disables.
     if (want_walk && allow_merge && !force_split && !try_pipe) {
-        const char* me = std::getenv("SDG_GS_MERGE");
-        const char* ce = std::getenv("SDG_GS_MERGE_CAP");
+        const char* me = knob("SDG_GS_MERGE");
+        const char* ce = knob("SDG_GS_MERGE_CAP");
         const int kforce = me ? std::atoi(me) : 0;
         // merging pays where a level is latency-bound, i.e. narrow; wide levels
         // (> kMergeRows rows on average, c3+) are throughput-bound and only get
@@ -1320,13 +1332,18 @@ void launch_gs_lower(Context& c, const GsPlan& g, double* z_new, cudaEvent_t mar
         }
         return;
     }
-    ProfScope ps_(c, PF_GS, g.packed_bytes() + 8.0 * g.n);
-    if (g.n == 0) return;
-    if (g.chain) {
-        launch_gs_chain(c, g, z_new);
+    if (g.wave) {
+        // algorithmic bytes: the band records (b and the scaled lower
+        // coefficients, [band][block][field][step][lane] incl. the skew
+        // padding) streamed once, z written once, lane 0's south row read once
+        ProfScope ps_(c, PF_GS_WAVE, g.packed_bytes() + 8.0 * g.n + 16.0 * g.wave_nx * g.wave_bands);
+        if (mark) SDG_CUDA(cudaEventRecord(mark, c.stream));
+        launch_gs_wave(c, g, z_new);
         SDG_GS_CHECK();
         return;
     }
+    ProfScope ps_(c, PF_GS, g.packed_bytes() + 8.0 * g.n);
+    if (g.n == 0) return;
     if (g.walk) {
         if (mark) SDG_CUDA(cudaEventRecord(mark, c.stream));
         launch_gs_walk(c, g, z_new);

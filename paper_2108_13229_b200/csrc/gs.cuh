@@ -19,8 +19,10 @@
 //   * the banded cluster kernel (gs.cu k_gs_cluster): B bands on a
 //     thread-block cluster, values crossing bands pushed with DSMEM st.async
 //     packets completing single-use mbarriers, bands as a skewed pipeline.
-// Opt-in experiments: the 2-CTA pipe (SDG_GS_PIPE=1) and the lane chain
-// (SDG_GS_CHAIN=1|2).  Every variant keeps the exact lexicographic order.
+// Structured finest levels (MAC velocity, 5-point TPFA) take the multi-SM
+// wavefront instead (gs_wave.cu, tried first; SDG_GS_WAVE=0 disables).
+// Opt-in experiment: the 2-CTA pipe (SDG_GS_PIPE=1).  Every variant keeps
+// the exact lexicographic order.
 //
 // Arithmetic is reassociated versus the reference (upper part first, 1/d
 // folded into the coefficients), so results agree to rounding; the BITWISE
@@ -84,13 +86,17 @@ struct GsPlan {
     int walk_import_base = 0;  // first import slot of a walk (pipe role 2)
     int walk_n_peer = 0, walk_pbar_bytes = 0;
     DevBuf<int> walk_peer_bytes;  // pipe role 2: bytes the peer pushes at each of its levels
-    // lane-chain lower solve of a structured finest level (gs_chain.cu)
-    bool chain = false;
-    int chain_kind = 0;                  // 1: 5-point grid, 2: MAC velocity (u then v)
-    int chain_nx = 0, chain_ny = 0;      // grid columns (m for MAC) / lanes
-    int chain_steps = 0, chain_bands = 0;
-    size_t chain_smem = 0;
-    DevBuf<double> chain_coef;           // static scaled lower coefficients, [field][band][step][lane]
+    // multi-SM wavefront lower solve of a structured finest level (gs_wave.cu);
+    // its records (b and the scaled lower coefficients) live in `packed`
+    bool wave = false;
+    int wave_kind = 0;                   // 1: 5-point grid, 2: MAC velocity (u and v rows in one pass)
+    int wave_nx = 0, wave_ny = 0;        // grid columns (m for MAC) / grid rows
+    int wave_bands = 0, wave_blocks = 0;
+    size_t wave_smem = 0;
+    DevBuf<unsigned long long> wave_ticket;  // band tickets handed out (gs_wave.cu)
+    DevBuf<double> wave_bnd;                 // band boundary rows, two parities, sentinel until written
+    // per row: 1 when it has entries left of the diagonal (its lower solve reads other rows)
+    std::vector<unsigned char> row_has_lower;
     // level merging (gs.cu, merge_levels): groups of k consecutive dependency
     // levels are walked as one; rows inside a group are substituted into each
     // other, so the walk reads only earlier groups and the prep computes the
@@ -108,16 +114,16 @@ struct GsPlan {
     void build(const HostCsr& a, const std::vector<int>& components, cudaStream_t s,
                int bands_hint = 0, bool allow_merge = false);
     double packed_bytes() const {
-        return static_cast<double>(packed_ptr ? part_doubles : packed.size() + chain_coef.size()) * 8.0;
+        return static_cast<double>(packed_ptr ? part_doubles : packed.size()) * 8.0;
     }
     const double* records() const { return packed_ptr ? packed_ptr : packed.get(); }
     // a plain walk, or label-block walks: launch_gs_lower can record its mark
     // after the last write to packed (prep, coupling steps) and before the last walk
     bool can_mark() const {
         if (pipe || merged) return false;
-        if (parts.empty()) return walk && !chain;
+        if (parts.empty()) return (walk || wave) && !merged;
         for (const auto& p : parts)
-            if (!p->walk || p->chain || !p->parts.empty() || p->merged) return false;
+            if (!p->walk || !p->parts.empty() || p->merged) return false;
         return true;
     }
 
@@ -138,8 +144,8 @@ struct GsPlan {
     };
 
 private:
-    bool build_chain(const HostCsr& a, const std::vector<int>& comps, const std::vector<double>& dinv_h,
-                     cudaStream_t s);
+    bool build_wave(const HostCsr& a, const std::vector<int>& comps, const std::vector<double>& dinv_h,
+                    cudaStream_t s);
     bool build_parts(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
                      cudaStream_t s);
     bool build_pipe(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
@@ -170,8 +176,10 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
 // mark: recorded on the stream right before the last walk of the sweep is
 // launched, i.e. once every packed b of the sweep is final (GsPlan::can_mark)
 void launch_gs_lower(Context& c, const GsPlan& g, double* z_new, cudaEvent_t mark = nullptr);
-// lane-chain variant (plans with chain == true; gs_chain.cu)
-void launch_gs_chain(Context& c, const GsPlan& g, double* z_new);
+// multi-SM wavefront variant (plans with wave == true; gs_wave.cu)
+void launch_gs_wave(Context& c, const GsPlan& g, double* z_new);
+// dev aid (SDG_WAVE_TL=1): per band {start, first block, end, waiting ns} of the last wave launch
+int wave_timeline_copy(unsigned long long* out, int max_bands);
 // single-CTA variant (plans with walk == true; gs_walk.cu)
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new);
 // the two parts of a pipe on a 2-CTA cluster (gs_walk.cu)

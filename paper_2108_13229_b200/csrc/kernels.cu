@@ -746,9 +746,19 @@ void launch_prolong(Context& c, int n, const int* agg, const double* z, const do
 }
 
 void launch_colmajor_gemv_sub(Context& c, int n, int m, const double* kmat, const double* w, double* z) {
-    ProfScope ps_(c, PF_COARSE, 8.0 * n * m + 8.0 * m + 16.0 * n);
+    ProfScope ps_(c, PF_IFACE, 8.0 * n * m + 8.0 * m + 16.0 * n);
     if (n == 0 || m == 0) return;
     const size_t smem = static_cast<size_t>(m) * 8;
+    // w is staged in shared memory: raise the dynamic limit once per instantiation
+    // (callers keep m <= kColmajorMaxGamma, setup_interface_split)
+    if (m > kColmajorMaxGamma) fail(SDG_EINVAL, "colmajor_gemv_sub: too many interface columns");
+    static const bool attr = [] {
+        const int lim = kColmajorMaxGamma * 8;
+        SDG_CUDA(cudaFuncSetAttribute(k_colmajor_gemv_sub<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+        SDG_CUDA(cudaFuncSetAttribute(k_colmajor_gemv_sub<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+        return true;
+    }();
+    (void)attr;
     if (8.0 * n * m > 40e6)
         launch_k(c, k_colmajor_gemv_sub<true>, (n + 32 * kGemvRowBlocks - 1) / (32 * kGemvRowBlocks), 128 * kGemvRowBlocks, smem, n, m, kmat, w, z);
     else

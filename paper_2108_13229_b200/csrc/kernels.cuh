@@ -55,6 +55,8 @@ void launch_prolong(Context& c, int n, const int* agg, const double* z, const do
 // Dense coarse solve y = Ainv x (row-major Ainv).
 void launch_dense_gemv(Context& c, int n, const double* ainv, const double* x, double* y);
 // z -= K w, K column-major n x m (td_bgs interface response, BlockPrecond)
+// z -= K w, K column-major n x m; w is staged in shared memory, so m is bounded
+constexpr int kColmajorMaxGamma = 24576;
 void launch_colmajor_gemv_sub(Context& c, int n, int m, const double* kmat, const double* w, double* z);
 // BITWISE Uzawa pressure step: z_p[i] = omega (sum_k C_ik z_v[k] - r_p[i]).
 void launch_uzawa_pressure(Context& c, const DevCsr& cm, const double* z_v, const double* r_p,

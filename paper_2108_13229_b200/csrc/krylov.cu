@@ -70,6 +70,43 @@ inline void read_back(Context& c, double* host, const double* dev, int count) {
 
 }  // namespace
 
+// Per-matrix GMRES workspace (basis, work vectors, reduction scratch), kept
+// across solves, and one captured graph per Arnoldi step index: step i is
+// precond apply -> SpMV -> CGS2 (multi-dot, multi-axpy, twice, the second
+// fused with the norm) -> scale into basis vector i + 1, and it reads and
+// writes only this workspace, so the graphs replay for every solve with the
+// same preconditioner.
+struct GmresWork {
+    int n = 0, m_cap = 0;
+    int64_t ld = 0;
+    DevBuf<double> basis, r, z, w, best_x, dd;
+    ReduceWs ws;
+    std::vector<cudaGraphExec_t> exec;
+    std::vector<int64_t> exec_launches;
+    const Precond* graph_p = nullptr;
+    GmresWork(int n_, int m_cap_, Context& c)
+        : n(n_), m_cap(m_cap_), ld((static_cast<int64_t>(n_) + 31) / 32 * 32),
+          basis(static_cast<size_t>(ld) * (m_cap_ + 1)), r(n_), z(n_), w(n_), best_x(n_), dd(4 * 64),
+          exec(m_cap_, nullptr), exec_launches(m_cap_, 0) {
+        ws.init(std::max(reduce_blocks(n_, c.num_sms), 8 * c.num_sms), 64, c.stream);
+    }
+    void drop_graphs() {
+        for (auto& e : exec)
+            if (e) {
+                cudaGraphExecDestroy(e);
+                e = nullptr;
+            }
+        graph_p = nullptr;
+    }
+    ~GmresWork() { drop_graphs(); }
+};
+
+namespace {
+
+bool graphs_enabled(const Context& c);
+
+}  // namespace
+
 SolveOut pd_gmres(Matrix& A, Precond* P, const double* b, double* x, double tol_abs,
                   int max_restarts, Restart ctrl) {
     Context& c = *A.ctx;
@@ -82,21 +119,71 @@ SolveOut pd_gmres(Matrix& A, Precond* P, const double* b, double* x, double tol_
     SolveOut out;
     EventTimer timer(c.stream);
     double* host = c.pinned->as<double>();         // 0..255: reads
-    double* host_up = host + 256;                  // 256..: uploads
+    double* host_up = host + 256;                  // 256..511: uploads
+    double* host_step = host + 1024;               // 1024..1535: Arnoldi read-backs, two slots
 
-    const int64_t ld = (static_cast<int64_t>(n) + 31) / 32 * 32;
-    DevBuf<double> basis(static_cast<size_t>(ld) * (m_cap + 1));
-    DevBuf<double> r(n), z(n), w(n), best_x(n), dd(4 * 64);
-    ReduceWs ws;
-    ws.init(std::max(reduce_blocks(n, c.num_sms), 8 * c.num_sms), 64, c.stream);
-    double* h1 = dd.get();
-    double* h2 = dd.get() + 64;
-    double* sc = dd.get() + 128;   // [0] = ||w||, [1] = beta, [2] = ||r||^2
-    double* yv = dd.get() + 192;
+    if (!A.gm_work || A.gm_work->n != n || A.gm_work->m_cap < m_cap)
+        A.gm_work = std::make_shared<GmresWork>(n, std::max(m_cap, A.gm_work ? A.gm_work->m_cap : 0), c);
+    GmresWork& W = *A.gm_work;
+    const int64_t ld = W.ld;
+    double* basis = W.basis.get();
+    double *r = W.r.get(), *z = W.z.get(), *w = W.w.get(), *best_x = W.best_x.get();
+    ReduceWs& ws = W.ws;
+    double* h1 = W.dd.get();
+    double* h2 = W.dd.get() + 64;
+    double* sc = W.dd.get() + 128;   // [0] = ||w||, [1] = beta, [2] = ||r||^2
+    double* yv = W.dd.get() + 192;
+
+    // Arnoldi step i (krylov.cpp:99-118, CGS2 form) and the read-back of its
+    // Hessenberg column into pinned slot `slot`
+    auto enqueue_step = [&](int i) {
+        const double* vi = basis + ld * i;
+        precond_apply(c, P, vi, z, n);
+        launch_spmv(c, A.dev, z, w);
+        launch_multidot(c, ws, n, i + 1, basis, ld, w, h1);
+        launch_multi_axpy(c, n, i + 1, basis, ld, h1, w);
+        launch_multidot(c, ws, n, i + 1, basis, ld, w, h2);
+        launch_multi_axpy_norm2(c, ws, n, i + 1, basis, ld, h2, w, sc);
+        launch_scale_by_inv(c, n, w, sc, basis + ld * (i + 1));
+    };
+    const bool use_graph = graphs_enabled(c);
+    if (use_graph && W.graph_p != P) W.drop_graphs();
+    auto run_step = [&](int i, int slot) {
+        if (use_graph) {
+            if (!W.exec[i]) {
+                const int64_t l0 = c.launches.load();
+                cudaGraph_t g = nullptr;
+                SDG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+                try {
+                    enqueue_step(i);
+                } catch (...) {
+                    cudaStreamEndCapture(c.stream, &g);
+                    if (g) cudaGraphDestroy(g);
+                    throw;
+                }
+                SDG_CUDA(cudaStreamEndCapture(c.stream, &g));
+                SDG_CUDA(cudaGraphInstantiate(&W.exec[i], g, 0));
+                cudaGraphDestroy(g);
+                W.exec_launches[i] = c.launches.load() - l0;
+                c.launches.fetch_sub(W.exec_launches[i]);
+                if (P) P->add_applications(-1);  // counted at replay
+                W.graph_p = P;
+            }
+            SDG_CUDA(cudaGraphLaunch(W.exec[i], c.stream));
+            c.count(static_cast<int>(W.exec_launches[i]));
+            if (P) P->add_applications(1);
+        } else {
+            enqueue_step(i);
+        }
+        // h1 | h2 | ||w||: ordered before the next step's kernels overwrite them
+        SDG_CUDA(cudaMemcpyAsync(host_step + 256 * slot, W.dd.get(), sizeof(double) * 129, cudaMemcpyDeviceToHost,
+                                 c.stream));
+        SDG_CUDA(cudaEventRecord(c.step_ev[slot], c.stream));
+    };
 
     launch_fill(c, x, 0.0, n);
-    launch_copy(c, r.get(), b, n);
-    launch_norm2sq(c, ws, n, r.get(), sc + 2);
+    launch_copy(c, r, b, n);
+    launch_norm2sq(c, ws, n, r, sc + 2);
     read_back(c, host, sc + 2, 1);
     double res_norm = std::sqrt(host[0]);
     out.history.push_back(res_norm);
@@ -108,7 +195,7 @@ SolveOut pd_gmres(Matrix& A, Precond* P, const double* b, double* x, double tol_
     }
 
     double prev_cycle_res = res_norm;
-    launch_copy(c, best_x.get(), x, n);
+    launch_copy(c, best_x, x, n);
     double best_res = res_norm;
     bool trust_estimate = true;
 
@@ -122,26 +209,25 @@ SolveOut pd_gmres(Matrix& A, Precond* P, const double* b, double* x, double tol_
         g[0] = beta;
         host_up[0] = beta;
         SDG_CUDA(cudaMemcpyAsync(sc + 1, host_up, sizeof(double), cudaMemcpyHostToDevice, c.stream));
-        launch_scale_by_inv(c, n, r.get(), sc + 1, basis.get());
+        launch_scale_by_inv(c, n, r, sc + 1, basis);
 
         int used = 0;
         bool basis_exhausted = false;
+        // Step i + 1 is enqueued before step i's column is read back: it does
+        // not depend on the host's Givens update, so the GPU never waits for
+        // the host.  When step i ends the cycle, step i + 1 was speculative:
+        // it wrote only basis vector i + 2 and the work vectors, which the
+        // cycle end does not read (it reads basis 0..used-1 and overwrites w, z).
+        run_step(0, 0);
         for (int i = 0; i < m; ++i) {
-            const double* vi = basis.get() + ld * i;
-            precond_apply(c, P, vi, z.get(), n);
-            launch_spmv(c, A.dev, z.get(), w.get());
-            launch_multidot(c, ws, n, i + 1, basis.get(), ld, w.get(), h1);
-            launch_multi_axpy(c, n, i + 1, basis.get(), ld, h1, w.get());
-            launch_multidot(c, ws, n, i + 1, basis.get(), ld, w.get(), h2);
-            launch_multi_axpy_norm2(c, ws, n, i + 1, basis.get(), ld, h2, w.get(), sc);
-            launch_scale_by_inv(c, n, w.get(), sc, basis.get() + ld * (i + 1));
-            SDG_CUDA(cudaMemcpyAsync(host, dd.get(), sizeof(double) * 129, cudaMemcpyDeviceToHost, c.stream));
-            c.sync();
+            if (i + 1 < m) run_step(i + 1, (i + 1) & 1);
+            SDG_CUDA(cudaEventSynchronize(c.step_ev[i & 1]));
+            const double* hs = host_step + 256 * (i & 1);
             for (int k = 0; k <= i; ++k) {
-                hij(k, i) += host[k];
-                hij(k, i) += host[64 + k];
+                hij(k, i) += hs[k];
+                hij(k, i) += hs[64 + k];
             }
-            const double wn = host[128];
+            const double wn = hs[128];
             hij(i + 1, i) = wn;
             for (int k = 0; k < i; ++k) {
                 const double t0 = cs[k] * hij(k, i) + sn[k] * hij(k + 1, i);
@@ -150,7 +236,10 @@ SolveOut pd_gmres(Matrix& A, Precond* P, const double* b, double* x, double tol_
                 hij(k + 1, i) = t1;
             }
             const double denom = std::hypot(hij(i, i), hij(i + 1, i));
-            if (denom == 0.0) fail(SDG_ESINGULAR, "pd_gmres: singular Hessenberg block");
+            if (denom == 0.0) {
+                c.sync();
+                fail(SDG_ESINGULAR, "pd_gmres: singular Hessenberg block");
+            }
             cs[i] = hij(i, i) / denom;
             sn[i] = hij(i + 1, i) / denom;
             hij(i, i) = denom;
@@ -169,26 +258,30 @@ SolveOut pd_gmres(Matrix& A, Precond* P, const double* b, double* x, double tol_
             }
         }
 
+        if (used < m && P) P->add_applications(-1);  // the speculative step is not an apply of krylov.cpp
         std::vector<double> y(used, 0.0);
         for (int i = used - 1; i >= 0; --i) {
             double s = g[i];
             for (int j = i + 1; j < used; ++j) s -= hij(i, j) * y[j];
-            if (hij(i, i) == 0.0) fail(SDG_ESINGULAR, "pd_gmres: singular Hessenberg block");
+            if (hij(i, i) == 0.0) {
+                c.sync();
+                fail(SDG_ESINGULAR, "pd_gmres: singular Hessenberg block");
+            }
             y[i] = s / hij(i, i);
         }
         std::copy(y.begin(), y.end(), host_up);
         SDG_CUDA(cudaMemcpyAsync(yv, host_up, sizeof(double) * std::max(used, 1),
                                  cudaMemcpyHostToDevice, c.stream));
-        launch_lincomb(c, n, used, basis.get(), ld, yv, w.get());
-        precond_apply(c, P, w.get(), z.get(), n);
-        launch_add_inplace(c, n, x, z.get());
-        launch_spmv_add(c, A.dev, x, b, r.get(), -1.0);  // r = b - A x
-        launch_norm2sq(c, ws, n, r.get(), sc + 2);
+        launch_lincomb(c, n, used, basis, ld, yv, w);
+        precond_apply(c, P, w, z, n);
+        launch_add_inplace(c, n, x, z);
+        launch_spmv_add(c, A.dev, x, b, r, -1.0);  // r = b - A x
+        launch_norm2sq(c, ws, n, r, sc + 2);
         read_back(c, host, sc + 2, 1);
         res_norm = std::sqrt(host[0]);
         if (res_norm < best_res) {
             best_res = res_norm;
-            launch_copy(c, best_x.get(), x, n);
+            launch_copy(c, best_x, x, n);
         }
         if (trust_estimate && used < m && res_norm > tol_abs) trust_estimate = false;
         const double rate =
@@ -199,7 +292,7 @@ SolveOut pd_gmres(Matrix& A, Precond* P, const double* b, double* x, double tol_
     }
 
     if (best_res < res_norm) {
-        launch_copy(c, x, best_x.get(), n);
+        launch_copy(c, x, best_x, n);
         res_norm = best_res;
     }
     out.history.push_back(res_norm);
@@ -294,6 +387,7 @@ SolveOut bicgstab(Matrix& A, Precond* P, const double* b, double* x, double tol_
         cudaGraphDestroy(g);
         W.graph_launches = c.launches.load() - l0;
         c.launches.fetch_sub(W.graph_launches);
+        if (P) P->add_applications(-2);  // counted at replay
         W.graph_p = P;
         W.graph_x = x;
     }
@@ -301,6 +395,7 @@ SolveOut bicgstab(Matrix& A, Precond* P, const double* b, double* x, double tol_
         if (use_graph) {
             SDG_CUDA(cudaGraphLaunch(W.exec, c.stream));
             c.count(static_cast<int>(W.graph_launches));
+            if (P) P->add_applications(2);
         } else {
             enqueue_iteration();
         }

@@ -24,6 +24,7 @@ Context::Context(int dev) : device(dev) {
     SDG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     SDG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     pinned = std::make_unique<PinnedBuf>(64 * 1024);
+    for (auto& e : step_ev) SDG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (const char* e = std::getenv("SDG_PDL")) pdl = e[0] != '0';
 }
 
@@ -33,6 +34,8 @@ Context::~Context() {
         cudaEventDestroy(r.b);
     }
     for (auto e : event_pool) cudaEventDestroy(e);
+    for (auto e : step_ev)
+        if (e) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
@@ -338,7 +341,7 @@ void BlockPrecond::setup_interface_split(const HostCsr& cp) {
         if (cp.rp[i + 1] > cp.rp[i]) rows.push_back(i);
     const int m = static_cast<int>(rows.size());
     const double kbytes = static_cast<double>(n_ppm_) * m * 8.0;
-    if (m == 0 || kbytes > kSplitBudget) return;
+    if (m == 0 || kbytes > kSplitBudget || m > kColmajorMaxGamma) return;
     Context& cx = *ctx_;
     // worth it only when streaming K costs clearly less than the porous
     // V-cycle it takes off the critical path: time one apply
@@ -400,13 +403,16 @@ void BlockPrecond::setup_early_w(const HostCsr& matrix) {
     AmgPrecond& amg = uz->inner_mut();
     const GsPlan* plan = amg.markable_post_plan();
     if (!plan || amg.post_mark) return;
+    // the premise is checked on the matrix the post-smoother's plan was built
+    // from (the Uzawa's own V, level 0 of its AMG), not on the block of
+    // `matrix`: the two need not be equal for an arbitrary Uzawa handle
+    if (plan->n != n_v_ || plan->row_has_lower.size() != static_cast<size_t>(n_v_)) return;
     const HostCsr cp = submatrix(matrix, n_v_ + n_pff_, matrix.n_rows, 0, n_v_ + n_pff_);
     for (int i = 0; i < cp.n_rows; ++i)
         for (int q = cp.rp[i]; q < cp.rp[i + 1]; ++q) {
             const int j = cp.ci[q];
-            if (j >= n_v_) return;  // C' reads a free-flow pressure
-            for (int k = matrix.rp[j]; k < matrix.rp[j + 1]; ++k)
-                if (matrix.ci[k] < j) return;  // z_v(j) depends on the walk
+            if (j >= n_v_) return;                 // C' reads a free-flow pressure
+            if (plan->row_has_lower[j]) return;    // z_v(j) depends on the lower solve
         }
     SDG_CUDA(cudaEventCreateWithFlags(&early_ev_, cudaEventDisableTiming));
     amg.post_mark = early_ev_;
@@ -458,9 +464,15 @@ void BlockPrecond::do_apply(const double* r, double* z) {
             first_->apply(r, z);
             if (fork && early_ev_) {  // see setup_early_w
                 cx.side_continue(early_ev_);
-                launch_spmv_packed(cx, c_gamma_, early_plan_->bidx.get(), early_plan_->packed.get(),
-                                   w_gamma_.get());
-                launch_colmajor_gemv_sub(cx, n_ppm_, n_gamma_, k_gamma_.get(), w_gamma_.get(), z + n_ff);
+                try {
+                    launch_spmv_packed(cx, c_gamma_, early_plan_->bidx.get(), early_plan_->packed.get(),
+                                       w_gamma_.get());
+                    launch_colmajor_gemv_sub(cx, n_ppm_, n_gamma_, k_gamma_.get(), w_gamma_.get(), z + n_ff);
+                } catch (...) {
+                    cx.side_end();
+                    cx.side_join();
+                    throw;
+                }
                 cx.side_end();
                 cx.side_join();
                 break;

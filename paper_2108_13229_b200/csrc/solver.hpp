@@ -15,7 +15,8 @@
 
 namespace sdg {
 
-struct BiWork;  // krylov.cu: cached BiCGSTAB workspace + captured iteration graph
+struct BiWork;     // krylov.cu: cached BiCGSTAB workspace + captured iteration graph
+struct GmresWork;  // krylov.cu: cached GMRES basis / workspace + captured Arnoldi-step graphs
 
 // A device CSR plus its host copy (setup extracts blocks from it) and, on
 // demand, the Gauss-Seidel level schedule.
@@ -29,6 +30,7 @@ struct Matrix {
     int n_levels = 0;
 
     std::shared_ptr<BiWork> bi_work;
+    std::shared_ptr<GmresWork> gm_work;
 
     Matrix(CtxPtr c, HostCsr h);
     void ensure_schedule();
@@ -47,6 +49,8 @@ public:
         do_apply(r, z);
     }
     int64_t applications() const { return applications_.load(std::memory_order_relaxed); }
+    // a captured graph that contains k applies was replayed
+    void add_applications(int64_t k) { applications_.fetch_add(k, std::memory_order_relaxed); }
     // setup-time applies (BlockPrecond interface split) that are not counted
     void apply_uncounted(const double* r, double* z) { do_apply(r, z); }
     virtual int64_t setup_memory_doubles() const { return 0; }
@@ -95,6 +99,8 @@ public:
                                                                                                     : nullptr;
     }
     cudaEvent_t post_mark = nullptr;
+    // the finest level's smoother runs the multi-SM wavefront (gs_wave.cu)
+    bool finest_wave() const { return !levels_.empty() && levels_[0].fast && num_levels() > 1 && levels_[0].gs.wave; }
 
 protected:
     void do_apply(const double* r, double* z) override;
@@ -158,6 +164,8 @@ public:
     int64_t work_per_apply() const override;
     const PrecondPtr& first() const { return first_; }
     const PrecondPtr& pm() const { return pm_; }
+    bool interface_split() const { return n_gamma_ > 0; }
+    bool early_correction() const { return early_ev_ != nullptr; }
 
 protected:
     void do_apply(const double* r, double* z) override;

@@ -145,6 +145,7 @@ def lib():
         p("sdg_precond_omega", _d, [_vp])
         p("sdg_precond_setup_seconds", _d, [_vp])
         p("sdg_precond_hierarchy", _i, [_vp, _i, P(_i), P(_i), P(_i64), _i])
+        p("sdg_precond_features", _i, [_vp, P(_i)])
         p("sdg_precond_set_graphs", _i, [_vp, _i])
         p("sdg_pd_gmres", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Restart), P(_Report)])
         p("sdg_pd_gmres_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Restart), P(_Report)])
@@ -219,7 +220,7 @@ class Context:
     def profile(self) -> dict:
         """Per kernel family: launches, total CUDA-event ms, total algorithmic bytes."""
         out = {}
-        for f in range(12):
+        for f in range(14):  # PF_COUNT (common.hpp)
             n, ms, by = _i64(), _d(), _d()
             _check(lib().sdg_context_profile(self.h, f, C.byref(n), C.byref(ms), C.byref(by)))
             if n.value:
@@ -476,6 +477,13 @@ class Preconditioner:
 
     def setup_seconds(self) -> float:
         return lib().sdg_precond_setup_seconds(self.h)
+
+    def features(self) -> set:
+        """Fast paths this handle runs: {"split", "early", "wave_v", "wave_d"}."""
+        f = _i()
+        _check(lib().sdg_precond_features(self.h, C.byref(f)))
+        names = {1: "split", 2: "early", 4: "wave_v", 8: "wave_d"}
+        return {nm for bit, nm in names.items() if f.value & bit}
 
     def hierarchy(self, which: int = 0):
         nl = _i()

@@ -115,10 +115,10 @@ def test_amg_on_system_blocks(ref):
                                   {"SDG_GS_BANDS": "4"}, {"SDG_GS_MERGE": "1"}, {"SDG_GS_MERGE": "2"},
                                   {"SDG_GS_MERGE": "4"}, {"SDG_GS_MERGE": "4", "SDG_GS_MERGE_CAP": "8"},
                                   {"SDG_TD_SPLIT": "0"}, {"SDG_SELL": "0"}, {"SDG_WALK_ROLES": "0"},
-                                  {"SDG_TD_EARLY": "0"}],
+                                  {"SDG_TD_EARLY": "0"}, {"SDG_GS_WAVE": "0"}],
                          ids=["label-block-walks", "2-cta-pipe", "cluster-kernel", "cluster-4-bands", "no-merge",
                               "merge-2", "merge-4", "merge-dynamic", "no-interface-split", "csr-spmv", "no-walk-roles",
-                              "late-interface-gemv"])
+                              "late-interface-gemv", "no-wave"])
 def test_smoother_paths_match_reference(ref, golden, monkeypatch, mode):
     """The other lower-solve plans (one walk per u/v block with a coupling
     step; the u/v blocks walked concurrently on a 2-CTA cluster; the banded
@@ -139,6 +139,44 @@ def test_smoother_paths_match_reference(ref, golden, monkeypatch, mode):
                                int(g["n_vel"]), int(g["n_pff"]), int(g["n_ppm"]))
     p = sdc.TdPreconditioner(system, "td_bgs", omega_override=float(g["omega"]))
     assert rel_l2(p.apply(g["apply_r"]), g["apply_z"]) < 1e-10
+
+
+@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3"])
+def test_wave_smoother_bitwise_vs_walks(monkeypatch, cfg_name):
+    """The multi-SM wavefront lower solve (gs_wave.cu, the default on the
+    structured finest levels) does every row's arithmetic in the order of the
+    level walks: the velocity AMG V-cycle equals the one with label-block
+    walks on its finest level (u block, coupling step, v block) bit for bit,
+    and the porous one equals the plain finest walk.  c1 runs 2 bands, c2 6,
+    c3 16 (one CTA each), so the cross-band flag hand-off is exercised; two
+    applies in a row check the epoch-tagged flags."""
+    from paper_2108_13229_b200 import scenarios
+    cfg = scenarios.CONFIGS[cfg_name]
+    s = scenarios.build_system(cfg)
+    V = sdc.submatrix(s.matrix, 0, s.n_vel, 0, s.n_vel)
+    comps = [0] * s.n_u + [1] * (s.n_vel - s.n_u)
+    D = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
+    rng = np.random.default_rng(3)
+    for mat, opts, knobs, feat in (
+            (V, sdc.AmgOptions(components=comps, max_levels=cfg.v_max_levels),
+             {"SDG_GS_WAVE": "0", "SDG_GS_SPLIT": "1"}, "wave_v"),
+            (D, sdc.AmgOptions(max_levels=cfg.d_max_levels), {"SDG_GS_WAVE": "0", "SDG_GS_MERGE": "1"}, "wave_v")):
+        r = [rng.standard_normal(mat.n_rows) for _ in range(2)]
+        monkeypatch.delenv("SDG_GS_KNOB_ROWS", raising=False)
+        wave = sdc.AmgPreconditioner(mat, opts)
+        assert feat in wave.features()
+        zw = [wave.apply(x) for x in r] + [wave.apply(r[0])]
+        del wave
+        monkeypatch.setenv("SDG_GS_KNOB_ROWS", str(mat.n_rows))  # the knobs act on the finest level only
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        walk = sdc.AmgPreconditioner(mat, opts)
+        assert feat not in walk.features()
+        zk = [walk.apply(x) for x in r]
+        for k in knobs:
+            monkeypatch.delenv(k)
+        assert np.array_equal(zw[0], zk[0]) and np.array_equal(zw[1], zk[1])
+        assert np.array_equal(zw[2], zw[0])
 
 
 def test_c2_merge_and_interface_split_agree(monkeypatch):
@@ -178,20 +216,23 @@ def test_c2_walk_roles_bitwise(monkeypatch):
     assert np.array_equal(z_roles, z_plain)
 
 
-@pytest.mark.parametrize("split", ["0", "1"], ids=["whole-v0-walk", "label-block-walks"])
+@pytest.mark.parametrize("split", ["0", "1"], ids=["v0-wave", "label-block-walks"])
 def test_c2_early_interface_correction_bitwise(monkeypatch, split):
     """td_bgs with the interface GEMV started on the side stream from the
     Uzawa post-smoother's mark (the default) against the GEMV after the join:
-    bitwise equal, for a whole V0 walk and for label-block walks."""
+    bitwise equal, for the V0 wavefront and for label-block walks."""
     from paper_2108_13229_b200 import scenarios
     monkeypatch.setenv("SDG_GS_SPLIT", split)
     cfg = scenarios.CONFIGS["c2"]
     s = scenarios.build_system(cfg)
     r = np.random.default_rng(5).standard_normal(s.n_total())
     early = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
+    assert {"split", "early"} <= early.features()
+    assert ("wave_v" in early.features()) == (split == "0")
     z_early = [early.apply(r), early.apply(2.0 * r)]
     monkeypatch.setenv("SDG_TD_EARLY", "0")
     late = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels, omega_override=early.omega())
+    assert "early" not in late.features() and "split" in late.features()
     z_late = [late.apply(r), late.apply(2.0 * r)]
     assert all(np.array_equal(a, b) for a, b in zip(z_early, z_late))
 

@@ -37,6 +37,12 @@ def test_gmres50_matches_reference(golden, name):
     assert res.report.converged
     assert within(res.report.iterations, int(g["gmres50_iters"]))
     assert rel_l2(res.x, g["gmres50_x"]) <= X_TOL
+    # applications = iterations + cycles (krylov.cpp:99,155), also when the
+    # Arnoldi steps replay captured graphs and one step ran speculatively
+    it = res.report.iterations
+    assert res.report.precond_applications == it + (it + 49) // 50
+    res2 = sdc.pd_gmres(sdc.LinearOperator.from_matrix(s.matrix), p, s.rhs, tol, 400, sdc.RestartController.fixed(50))
+    assert res2.report.iterations == it and np.array_equal(res2.x, res.x)  # cached workspace + graphs: deterministic
     r = s.rhs - sdc.spmv(s.matrix, res.x)
     assert np.linalg.norm(r) <= tol * (1 + 1e-9)
 
