@@ -3,8 +3,9 @@
 
 Metric (BASELINE.json): solve time to 1e-8 rel. residual; DoF*iter/s; SpMV
 GB/s vs B200 HBM peak.  `value` is DoF*iterations per second of whole solves
-(summed over ranks, each rank an independent replica = weak scaling), with the
-right-hand side already resident in HBM; `e2e` is the same metric through the
+with the right-hand side already resident in HBM; at N > 1 ranks the one
+system is split into horizontal strips over the GPUs (strong scaling, SURVEY.md
+§8(e); --replicas runs one independent copy per GPU instead); `e2e` is the same metric through the
 public host-pointer C-ABI call (sdg_bicgstab / sdg_pd_gmres: host->device copy
 of b and device->host copy of x inside the timed region).  One step = one full
 preconditioned solve of the workload's system.
@@ -18,6 +19,9 @@ minutes) and c5 (partitioned, 16 M DoF) run with --config; c1/c2 are parity
 cases.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--gpus N` without RANK/WORLD_SIZE in the environment re-launches itself
+through torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
@@ -55,8 +59,11 @@ def parse_args():
     ap.add_argument("--coupling-iterations", type=int, default=0,
                     help="config 5: cap the Dirichlet-Neumann loop (0 = run to convergence)")
     ap.add_argument("--sharded", action="store_true",
-                    help="strip-shard one system across the ranks (strong scaling, sdg_dist_*) instead of "
-                         "running one replica per rank")
+                    help="strip-shard one system across the ranks (strong scaling, sdg_dist_*); the default "
+                         "for N > 1 ranks")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1 ranks: one independent replica of the workload per GPU (weak scaling) instead "
+                         "of the strip-sharded solve")
     return ap.parse_args()
 
 
@@ -308,8 +315,9 @@ def run_reference(args):
     value = rs.n * sum(its) / sum(times)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_desc(cfg, rs.n), "dof": rs.n, "nnz": rs.a.nnz(),
+            "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": workload_desc(cfg, rs.n), "dof": rs.n, "nnz": int(len(rs.a.val)),
                        "iterations_per_step": its, "setup_s": st.setup_s, "system": st.assembly},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": f"each step = {threads} concurrent samples ({SAMPLE_DESC[cfg.solver]} of "
@@ -749,11 +757,25 @@ def run_sharded(args):
     return 0
 
 
+def launcher_cmd(args, port):
+    """`bench.py --gpus N` without a rank environment re-launches itself as N
+    ranks, the way the driver does (torch.distributed.run, one process per
+    GPU, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        return subprocess.call(launcher_cmd(args, port))
     if args.impl == "reference":
         return run_reference(args)
-    if args.sharded:
+    if args.sharded or (dist_env()[2] > 1 and not args.replicas):
         return run_sharded(args)
     from paper_2108_13229_b200 import scenarios
     if scenarios.CONFIGS[args.config].solver == "dn":

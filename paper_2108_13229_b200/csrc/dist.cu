@@ -144,6 +144,31 @@ void Transport::allreduce(Context& c, const double* partial, int k, double* host
 
 namespace {
 
+// out[j] = sum over ranks p in rank order of g[p * k + j] (the order the host
+// fold of Transport::allreduce uses, so both give the same bits)
+__global__ void k_fold_ranks(int k, int size, const double* __restrict__ g, double* __restrict__ out, int take_sqrt) {
+    pdl_begin();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    double s = 0.0;
+    for (int p = 0; p < size; ++p) s += g[static_cast<size_t>(p) * k + j];
+    out[j] = take_sqrt ? sqrt(s) : s;
+}
+
+}  // namespace
+
+void Transport::allreduce_device(Context& c, const double* partial, int k, double* out, bool take_sqrt) {
+    if (k <= 0) return;
+    const size_t need = static_cast<size_t>(size) * k;
+    if (gather_.size() < need) gather_.resize(need);
+    allgather(c, partial, k, gather_.get());
+    launch_k(c, k_fold_ranks, (k + 127) / 128, 128, 0, k, size, static_cast<const double*>(gather_.get()), out,
+             take_sqrt ? 1 : 0);
+    c.count();
+}
+
+namespace {
+
 struct HostTransport final : Transport {
     HostExchangeFn ex;
     HostAllgatherFn ag;
@@ -742,6 +767,7 @@ SolveOut dist_pd_gmres(DistSystem& S, DistTd* P, const double* b, double* x, dou
     double* sc = dd.get() + 128;
     double* yv = dd.get() + 192;
     double hh[64], up[64];
+    double* hcol = c.pinned->as<double>() + 2048;  // h1 | h2 | ||w|| read-back of one step
     auto precond = [&](const double* in, double* o) {
         if (P)
             P->apply(in, o);
@@ -791,25 +817,27 @@ SolveOut dist_pd_gmres(DistSystem& S, DistTd* P, const double* b, double* x, dou
         int used = 0;
         bool basis_exhausted = false;
         for (int i = 0; i < m; ++i) {
+            // the Arnoldi step runs on the device end to end: each CGS2 pass's
+            // partial dots are all-gathered and folded in rank order by a
+            // kernel (Transport::allreduce_device), and the host reads the
+            // Hessenberg column once per step
             const double* vi = basis.get() + ld * i;
             precond(vi, z.get());
             S.A.apply(c, t, z.get(), w.get());
             launch_multidot(c, ws, n, i + 1, basis.get(), ld, w.get(), h1);
-            t.allreduce(c, h1, i + 1, hh);
-            upload(h1, hh, i + 1);
-            for (int k = 0; k <= i; ++k) hij(k, i) += hh[k];
+            t.allreduce_device(c, h1, i + 1, h1);
             launch_multi_axpy(c, n, i + 1, basis.get(), ld, h1, w.get());
             launch_multidot(c, ws, n, i + 1, basis.get(), ld, w.get(), h2);
-            t.allreduce(c, h2, i + 1, hh);
-            upload(h2, hh, i + 1);
-            for (int k = 0; k <= i; ++k) hij(k, i) += hh[k];
+            t.allreduce_device(c, h2, i + 1, h2);
             launch_multi_axpy(c, n, i + 1, basis.get(), ld, h2, w.get());
             launch_norm2sq(c, ws, n, w.get(), sc);
-            t.allreduce(c, sc, 1, hh);
-            const double wn = std::sqrt(hh[0]);
-            up[0] = wn;
-            upload(sc, up, 1);
+            t.allreduce_device(c, sc, 1, sc, /*take_sqrt=*/true);
             launch_scale_by_inv(c, n, w.get(), sc, basis.get() + ld * (i + 1));
+            SDG_CUDA(cudaMemcpyAsync(hcol, dd.get(), sizeof(double) * 129, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            for (int k = 0; k <= i; ++k) hij(k, i) += hcol[k];
+            for (int k = 0; k <= i; ++k) hij(k, i) += hcol[64 + k];
+            const double wn = hcol[128];
             hij(i + 1, i) = wn;
             for (int k = 0; k < i; ++k) {
                 const double a0 = cs[k] * hij(k, i) + sn[k] * hij(k + 1, i);

@@ -50,6 +50,10 @@ struct Transport {
 
     // Sum of k per-rank partials (device), folded in rank order on the host.
     void allreduce(Context& c, const double* partial, int k, double* host_out);
+    // The same sum folded in rank order by a device kernel into out (device;
+    // may alias partial), stream-ordered: no host synchronisation.  take_sqrt:
+    // out = sqrt(sum) (a norm from squared partials).
+    void allreduce_device(Context& c, const double* partial, int k, double* out, bool take_sqrt = false);
 
 private:
     DevBuf<double> gather_;

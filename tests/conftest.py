@@ -60,3 +60,23 @@ def bitwise_equal(x, y):
     x, y = np.asarray(x, np.float64), np.asarray(y, np.float64)
     # -0.0 and +0.0 are the same value; everything else must match bit for bit
     return x.shape == y.shape and bool(np.all((x.view(np.uint64) == y.view(np.uint64)) | ((x == 0) & (y == 0))))
+
+
+def ref_spread(solve, rhs, seeds=8):
+    """The reference's own iteration-count spread under rounding-level input
+    changes (checker side): `solve(b)` runs the reference solver
+    and returns its iteration count; it is called on `rhs` and on `seeds`
+    copies of it multiplied element-wise by (1 + 2^-52 u), u ~ U(-1, 1).
+    BiCGSTAB counts are rounding-chaotic (the reference's own
+    -O2 and FMA builds take 211 and 75 iterations at 50^2), so a GPU count is
+    judged against this spread, not against one sample.  Returns (min, max)."""
+    counts = [solve(rhs)]
+    for sd in range(seeds):
+        u = np.random.default_rng(sd).uniform(-1.0, 1.0, rhs.size)
+        counts.append(solve(rhs * (1.0 + np.ldexp(u, -52))))
+    return min(counts), max(counts)
+
+
+def within_spread(it, lo, hi, slack=0.05):
+    """[0.95 min, 1.05 max] of the reference's spread."""
+    return (1.0 - slack) * lo <= it <= (1.0 + slack) * hi

@@ -36,6 +36,8 @@ def _worker(rank, world, port, out):
                 config = "c1"
                 steps = 1
                 warmup = 0
+                gpus = 2
+                ref_threads = 1
             out[world + rank] = bench.run_reference(A())
     finally:
         dist.destroy_process_group()
@@ -54,3 +56,32 @@ def test_job_totals_and_reference_ranks_gloo():
 def test_job_totals_single_process():
     import bench
     assert bench.job_totals(None, 3.0, 7.0) == (3.0, 7.0)
+
+
+def test_gpus_flag_relaunches_as_ranks():
+    """`bench.py --gpus 2` without a rank environment re-launches itself
+    through torch.distributed.run; the reference arm then runs on rank 0
+    only and prints exactly one JSON line (CPU only: c1, the reference's own
+    assembly and solver)."""
+    import json
+    import subprocess
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--config", "c1", "--steps", "1", "--warmup", "0", "--ref-threads", "2"],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+    assert line["config"]["system"].startswith("reference assemble_monolithic")
+
+
+def test_launcher_command():
+    import bench
+
+    class A:
+        gpus = 4
+    cmd = bench.launcher_cmd(A(), 12345)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=12345" in cmd
