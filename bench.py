@@ -303,8 +303,8 @@ def run_reference(args):
             reps = list(ex.map(lambda rm: ref_sample(R, rm, st.rtd, cfg, rs.rhs, tol)[1], rms))
         return sum(r.iterations for r in reps)
 
-    for _ in range(args.warmup):
-        batch()
+    for _ in range(args.warmup):  # untimed; one sample on one core warms the caches as well as a batch
+        ref_sample(R, rms[0], st.rtd, cfg, rs.rhs, tol)
     times, its = [], []
     for _ in range(args.steps):
         t0 = time.perf_counter()

@@ -129,8 +129,9 @@ int64_t sdg_context_launches(sdg_context* ctx);
  * family.  Enabling clears previous totals.  Families: 0 spmv, 1 gs,
  * 2 restrict, 3 prolong, 4 coarse, 5 uzawa, 6 ortho, 7 bicg, 8 vec, 9 setup,
  * 10 gsprep, 11 spmv_block, 12 gs_wave (the multi-SM wavefront smoother of
- * the structured finest levels), 13 iface (td_bgs interface GEMV). */
-#define SDG_PROF_FAMILIES 14
+ * the structured finest levels), 13 iface (td_bgs interface GEMV),
+ * 14 gs_lattice (the multi-SM lattice smoother of the aggregated coarse levels). */
+#define SDG_PROF_FAMILIES 15
 int sdg_context_set_profiling(sdg_context* ctx, int enable);
 int sdg_context_profile(sdg_context* ctx, int family, int64_t* launches, double* total_ms,
                         double* total_bytes);
@@ -221,6 +222,8 @@ int sdg_precond_set_graphs(sdg_precond* p, int enable);
 #define SDG_FEAT_EARLY 2
 #define SDG_FEAT_WAVE_V 4
 #define SDG_FEAT_WAVE_D 8
+#define SDG_FEAT_LATTICE_V 16 /* a coarse velocity (or AMG handle's) level on the multi-SM lattice smoother */
+#define SDG_FEAT_LATTICE_D 32
 int sdg_precond_features(const sdg_precond* p, int* features);
 
 /* ---- Krylov solvers (krylov.cpp) ----------------------------------------

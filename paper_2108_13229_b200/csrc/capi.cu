@@ -112,7 +112,7 @@ extern "C" int sdg_debug_wave_timeline(unsigned long long* out, int max_bands) {
 const char* sdg_profile_family_name(int family) {
     static const char* names[] = {"spmv", "gs", "restrict", "prolong", "coarse",
                                   "uzawa", "ortho", "bicg", "vec", "setup", "gsprep", "spmv_block",
-                                  "gs_wave", "iface"};
+                                  "gs_wave", "iface", "gs_lattice"};
     return (family >= 0 && family < sdg::PF_COUNT) ? names[family] : "?";
 }
 
@@ -346,10 +346,17 @@ int sdg_precond_features(const sdg_precond* p, int* features) {
         if (auto* blk = dynamic_cast<sdg::BlockPrecond*>(p->p.get())) {
             if (blk->interface_split()) f |= SDG_FEAT_SPLIT;
             if (blk->early_correction()) f |= SDG_FEAT_EARLY;
-            if (const sdg::AmgPrecond* a = amg_of(blk->first()); a && a->finest_wave()) f |= SDG_FEAT_WAVE_V;
-            if (const sdg::AmgPrecond* a = amg_of(blk->pm()); a && a->finest_wave()) f |= SDG_FEAT_WAVE_D;
-        } else if (const sdg::AmgPrecond* a = amg_of(p->p); a && a->finest_wave()) {
-            f |= SDG_FEAT_WAVE_V;
+            if (const sdg::AmgPrecond* a = amg_of(blk->first())) {
+                if (a->finest_wave()) f |= SDG_FEAT_WAVE_V;
+                if (a->coarse_lattice()) f |= SDG_FEAT_LATTICE_V;
+            }
+            if (const sdg::AmgPrecond* a = amg_of(blk->pm())) {
+                if (a->finest_wave()) f |= SDG_FEAT_WAVE_D;
+                if (a->coarse_lattice()) f |= SDG_FEAT_LATTICE_D;
+            }
+        } else if (const sdg::AmgPrecond* a = amg_of(p->p)) {
+            if (a->finest_wave()) f |= SDG_FEAT_WAVE_V;
+            if (a->coarse_lattice()) f |= SDG_FEAT_LATTICE_V;
         }
         *features = f;
     });

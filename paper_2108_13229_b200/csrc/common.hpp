@@ -111,6 +111,7 @@ enum ProfFamily {
     PF_SPMV_BLOCK,    // CSR SpMV of the blocks (C', Uzawa B / C) and small operators
     PF_GS_WAVE,       // Gauss-Seidel lower solve of the structured finest levels (multi-SM wavefront)
     PF_IFACE,         // td_bgs interface correction z_pm -= K w (column-major GEMV)
+    PF_GS_LATTICE,    // Gauss-Seidel lower solve of the aggregated coarse levels (multi-SM lattice)
     PF_COUNT
 };
 

@@ -653,6 +653,13 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     if (want_walk && !wave_off && !force_split && !try_pipe && !knob("SDG_GS_MERGE") &&
         build_wave(a, comps, dinv_h, s))
         return finish();
+    // 0a. the multi-SM lattice, when the level is an aggregated lattice
+    //     (gs_lattice.cu; SDG_GS_LATTICE=0 disables, here and in build_parts)
+    const char* lat_env = knob("SDG_GS_LATTICE");
+    lattice_off_ = lat_env && lat_env[0] == '0';
+    if (want_walk && !lattice_off_ && !force_split && !try_pipe && !knob("SDG_GS_MERGE") &&
+        build_lattice(a, dinv_h, s))
+        return finish();
     // 0b. one walk over merged levels: the first candidate, in the order
     //     (dynamic groups of <= 4 levels with <= 8 entries per row, fixed
     //     k = 4, 3, 2), whose modelled sweep (walk_model_cost, corrected form)
@@ -1026,7 +1033,8 @@ bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std
             max_k = std::max(max_k, nlow[i - lo]);
         }
         auto p = std::make_unique<GsPlan>();
-        if (!p->build_walk(sub, dsub, nlow, max_k, s)) return false;
+        if (!(!lattice_off_ && p->build_lattice(sub, dsub, s)) && !p->build_walk(sub, dsub, nlow, max_k, s))
+            return false;
         ps.push_back(std::move(p));
     }
     // one record buffer; the prep kernels write b through the global bidx
@@ -1330,6 +1338,12 @@ void launch_gs_lower(Context& c, const GsPlan& g, double* z_new, cudaEvent_t mar
             }
             launch_gs_lower(c, *g.parts[k], z_new + g.part_r0[k], k + 1 == g.parts.size() ? mark : nullptr);
         }
+        return;
+    }
+    if (g.lattice) {
+        ProfScope ps_(c, PF_GS_LATTICE, g.packed_bytes() + 8.0 * g.n);
+        launch_gs_lattice(c, g, z_new);
+        SDG_GS_CHECK();
         return;
     }
     if (g.wave) {

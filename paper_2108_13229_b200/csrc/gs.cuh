@@ -95,8 +95,16 @@ struct GsPlan {
     size_t wave_smem = 0;
     DevBuf<unsigned long long> wave_ticket;  // band tickets handed out (gs_wave.cu)
     DevBuf<double> wave_bnd;                 // band boundary rows, two parities, sentinel until written
+    // multi-SM lattice lower solve of an aggregated coarse level (gs_lattice.cu);
+    // records in `packed`
+    bool lattice = false;
+    int lat_bands = 0, lat_blocks = 0;
+    DevBuf<int> lat_win;                     // per (band, block): first window step of the previous band
+    DevBuf<unsigned long long> lat_ticket;   // band tickets handed out
+    DevBuf<double> lat_bnd;                  // last-chain values of every band, two parities, sentinel until written
     // per row: 1 when it has entries left of the diagonal (its lower solve reads other rows)
     std::vector<unsigned char> row_has_lower;
+    bool lattice_off_ = false;  // SDG_GS_LATTICE=0 (build_parts asks its parts too)
     // level merging (gs.cu, merge_levels): groups of k consecutive dependency
     // levels are walked as one; rows inside a group are substituted into each
     // other, so the walk reads only earlier groups and the prep computes the
@@ -146,6 +154,7 @@ struct GsPlan {
 private:
     bool build_wave(const HostCsr& a, const std::vector<int>& comps, const std::vector<double>& dinv_h,
                     cudaStream_t s);
+    bool build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, cudaStream_t s);
     bool build_parts(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
                      cudaStream_t s);
     bool build_pipe(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
@@ -178,6 +187,8 @@ void launch_gs_prep_post(Context& c, const GsPlan& g, const double* r, const dou
 void launch_gs_lower(Context& c, const GsPlan& g, double* z_new, cudaEvent_t mark = nullptr);
 // multi-SM wavefront variant (plans with wave == true; gs_wave.cu)
 void launch_gs_wave(Context& c, const GsPlan& g, double* z_new);
+// multi-SM lattice variant (plans with lattice == true; gs_lattice.cu)
+void launch_gs_lattice(Context& c, const GsPlan& g, double* z_new);
 // dev aid (SDG_WAVE_TL=1): per band {start, first block, end, waiting ns} of the last wave launch
 int wave_timeline_copy(unsigned long long* out, int max_bands);
 // single-CTA variant (plans with walk == true; gs_walk.cu)

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
         tma_block_if(ring + d * BLK, src + static_cast<size_t>(d) * BLK, BLK * 8, bars + d, lane == 0);
     const int j = band * 32 + lane;
     const bool has_src = band > 0, has_dst = band + 1 < a.nbands;
-    unsigned long long wait_ns = 0, t_start = a.tl ? gtimer() : 0, t_first = 0;
+    unsigned long long wait_ns = 0, t_start = a.tl ? gtimer() : 0, t_first = 0, tma_cyc = 0, comp_cyc = 0;
     const size_t bstride = static_cast<size_t>(NBF) * a.bcols;                 // one band boundary
     const size_t pstride = static_cast<size_t>(a.nbands - 1) * bstride;         // one parity
     const double* sb_in = has_src ? a.bnd + par * pstride + (band - 1) * bstride : a.bnd;   // read (lane 0)
@@ -289,7 +289,9 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
         for (int q = 0; q < a.nblocks; ++q) {
             load_bnd(q + 1, nbu, nbv);  // in flight during this block
             const int slot = q % kWaveDepth;
+            const long long c0 = a.tl ? clock64() : 0;
             ptx::mbar_wait(bars + slot, (q / kWaveDepth) & 1);
+            const long long c1 = a.tl ? clock64() : 0;
             const double2* B = reinterpret_cast<const double2*>(ring + slot * BLK) + lane;
             // every lane inside its u and v rows for the whole block: no
             // per-step column tests (the interior blocks, most of the sweep)
@@ -337,6 +339,11 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
                 run_block(std::true_type{});
             else
                 run_block(std::false_type{});
+            if (a.tl) {
+                const long long c2 = clock64();
+                tma_cyc += c1 - c0;
+                comp_cyc += c2 - c1;
+            }
             __syncwarp();  // every lane has read the slot
             tma_block_if(ring + slot * BLK, src + static_cast<size_t>(q + kWaveDepth) * BLK, BLK * 8, bars + slot,
                          lane == 0 && q + kWaveDepth < a.nblocks);
@@ -348,7 +355,9 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
         }
     }
     if (a.tl && lane == 0) {
-        unsigned long long* o = a.tl + 4 * band;
+        unsigned long long* o = a.tl + 8 * band;
+        o[4] = tma_cyc;
+        o[5] = comp_cyc;
         o[0] = t_start;
         o[1] = t_first;
         o[2] = gtimer();
@@ -498,7 +507,7 @@ unsigned long long* wave_timeline(int bands) {
         return e && e[0] == '1';
     }();
     if (!on) return nullptr;
-    if (!g_wave_tl) SDG_CUDA(cudaMalloc(&g_wave_tl, 4 * 1024 * sizeof(unsigned long long)));
+    if (!g_wave_tl) SDG_CUDA(cudaMalloc(&g_wave_tl, 8 * 1024 * sizeof(unsigned long long)));
     g_wave_tl_bands = std::min(bands, 1024);
     return g_wave_tl;
 }
@@ -508,7 +517,7 @@ int wave_timeline_copy(unsigned long long* out, int max_bands) {
     if (!g_wave_tl) return 0;
     const int nb = std::min(max_bands, g_wave_tl_bands);
     SDG_CUDA(cudaDeviceSynchronize());
-    SDG_CUDA(cudaMemcpy(out, g_wave_tl, 4 * nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    SDG_CUDA(cudaMemcpy(out, g_wave_tl, 8 * nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     return nb;
 }
 

@@ -101,6 +101,17 @@ public:
     cudaEvent_t post_mark = nullptr;
     // the finest level's smoother runs the multi-SM wavefront (gs_wave.cu)
     bool finest_wave() const { return !levels_.empty() && levels_[0].fast && num_levels() > 1 && levels_[0].gs.wave; }
+    // some coarse level's smoother runs the multi-SM lattice (gs_lattice.cu), itself or in a label block
+    bool coarse_lattice() const {
+        for (size_t l = 1; l + 1 < levels_.size(); ++l) {
+            const GsPlan& g = levels_[l].gs;
+            if (!levels_[l].fast) continue;
+            if (g.lattice) return true;
+            for (const auto& p : g.parts)
+                if (p->lattice) return true;
+        }
+        return false;
+    }
 
 protected:
     void do_apply(const double* r, double* z) override;

@@ -220,7 +220,7 @@ class Context:
     def profile(self) -> dict:
         """Per kernel family: launches, total CUDA-event ms, total algorithmic bytes."""
         out = {}
-        for f in range(14):  # PF_COUNT (common.hpp)
+        for f in range(15):  # PF_COUNT (common.hpp)
             n, ms, by = _i64(), _d(), _d()
             _check(lib().sdg_context_profile(self.h, f, C.byref(n), C.byref(ms), C.byref(by)))
             if n.value:
@@ -479,10 +479,10 @@ class Preconditioner:
         return lib().sdg_precond_setup_seconds(self.h)
 
     def features(self) -> set:
-        """Fast paths this handle runs: {"split", "early", "wave_v", "wave_d"}."""
+        """Fast paths this handle runs: {"split", "early", "wave_v", "wave_d", "lattice_v", "lattice_d"}."""
         f = _i()
         _check(lib().sdg_precond_features(self.h, C.byref(f)))
-        names = {1: "split", 2: "early", 4: "wave_v", 8: "wave_d"}
+        names = {1: "split", 2: "early", 4: "wave_v", 8: "wave_d", 16: "lattice_v", 32: "lattice_d"}
         return {nm for bit, nm in names.items() if f.value & bit}
 
     def hierarchy(self, which: int = 0):

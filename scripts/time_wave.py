@@ -1,7 +1,8 @@
 """Dev helper: device time of N AMG V-cycle applies of the velocity block
-(MAC, finest level on the wavefront smoother) and of the porous block (5-point)
-of one config, each alone on the stream, wave on vs off (SDG_GS_WAVE=0 with
-the knob restricted to the finest level).  python scripts/time_wave.py c3 [N]"""
+(MAC) and of the porous block (5-point) of one config, each alone on the
+stream, for the default plans and with the multi-SM smoothers switched off
+level by level (SDG_GS_WAVE=0 on the finest level, SDG_GS_LATTICE=0 on level 1).
+python scripts/time_wave.py c3 [N]"""
 import os, sys, time
 import ctypes as C
 sys.path.insert(0, os.getcwd())
@@ -18,9 +19,15 @@ comps = [0] * s.n_u + [1] * (s.n_vel - s.n_u)
 D = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
 for name, mat, opts in (("V", V, sdc.AmgOptions(components=comps, max_levels=cfg.v_max_levels)),
                         ("D", D, sdc.AmgOptions(max_levels=cfg.d_max_levels))):
-    for wave in ("1", "0"):
-        os.environ["SDG_GS_KNOB_ROWS"] = str(mat.n_rows)
-        os.environ["SDG_GS_WAVE"] = wave
+    base = sdc.AmgPreconditioner(mat, opts, ctx=ctx)
+    rows = [r for r, _ in base.hierarchy()]
+    del base
+    variants = [("default", {}), ("no-wave", {"SDG_GS_KNOB_ROWS": str(rows[0]), "SDG_GS_WAVE": "0"}),
+                ("no-lattice", {"SDG_GS_KNOB_ROWS": str(rows[1]), "SDG_GS_LATTICE": "0"})]
+    for vname, env in variants:
+        for k in ("SDG_GS_KNOB_ROWS", "SDG_GS_WAVE", "SDG_GS_LATTICE"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
         amg = sdc.AmgPreconditioner(mat, opts, ctx=ctx)
         r = torch.randn(mat.n_rows, dtype=torch.float64, device="cuda")
         z = torch.zeros_like(r)
@@ -33,6 +40,6 @@ for name, mat, opts in (("V", V, sdc.AmgOptions(components=comps, max_levels=cfg
         run(n_app)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / n_app
-        print(f"{cfg.name} {name} n={mat.n_rows} wave={wave} features={sorted(amg.features())} "
-              f"{dt * 1e6:.1f} us/apply |z|={z.norm().item():.15e}", flush=True)
+        print(f"{cfg.name} {name} n={mat.n_rows} {vname:10s} features={sorted(amg.features())} "
+              f"{dt * 1e6:.1f} us/apply", flush=True)
         del amg

@@ -21,12 +21,12 @@ r = np.random.default_rng(1).standard_normal(mat.n_rows)
 for _ in range(3):
     amg.apply(r)
 L = sdc.lib()
-buf = (C.c_ulonglong * 4096)()
+buf = (C.c_ulonglong * 8192)()
 nb = L.sdg_debug_wave_timeline(buf, 1024)
-t = np.array(buf[: 4 * nb], dtype=np.float64).reshape(nb, 4)
+t = np.array(buf[: 8 * nb], dtype=np.float64).reshape(nb, 8)
 t0 = t[:, 0].min()
 print(f"{cfg.name} {which}: {nb} bands, last wave launch (the post-smoother), ns from the first band start")
 for b in range(nb):
     print(f"band {b:3d}: start {t[b,0]-t0:9.0f} first {t[b,1]-t0:9.0f} end {t[b,2]-t0:9.0f} "
-          f"run {t[b,2]-t[b,1]:9.0f} wait {t[b,3]:9.0f}")
+          f"run {t[b,2]-t[b,1]:9.0f} wait {t[b,3]:9.0f} tma-wait cyc {t[b,4]:9.0f} compute cyc {t[b,5]:9.0f}")
 print(f"total {t[:,2].max()-t0:.0f} ns")

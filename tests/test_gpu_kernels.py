@@ -179,6 +179,43 @@ def test_wave_smoother_bitwise_vs_walks(monkeypatch, cfg_name):
         assert np.array_equal(zw[2], zw[0])
 
 
+@pytest.mark.parametrize("cfg_name", ["c2", "c3"])
+def test_lattice_smoother_bitwise_vs_walks(monkeypatch, cfg_name):
+    """The multi-SM lattice lower solve (gs_lattice.cu) on the first coarse
+    level does every row's arithmetic in the order of the level walk: the
+    velocity AMG V-cycle (lattice on both label blocks of level 1) equals the
+    one with plain level-1 walks bit for bit, and so does the porous one where
+    its level 1 is a lattice (c3; at c2 the porous aggregates are not)."""
+    from paper_2108_13229_b200 import scenarios
+    cfg = scenarios.CONFIGS[cfg_name]
+    s = scenarios.build_system(cfg)
+    V = sdc.submatrix(s.matrix, 0, s.n_vel, 0, s.n_vel)
+    comps = [0] * s.n_u + [1] * (s.n_vel - s.n_u)
+    D = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
+    rng = np.random.default_rng(4)
+    for mat, opts, knobs, expect in (
+            (V, sdc.AmgOptions(components=comps, max_levels=cfg.v_max_levels), {"SDG_GS_LATTICE": "0"}, True),
+            (D, sdc.AmgOptions(max_levels=cfg.d_max_levels), {"SDG_GS_LATTICE": "0", "SDG_GS_MERGE": "1"},
+             cfg_name == "c3")):
+        r = [rng.standard_normal(mat.n_rows) for _ in range(2)]
+        monkeypatch.delenv("SDG_GS_KNOB_ROWS", raising=False)
+        lat = sdc.AmgPreconditioner(mat, opts)
+        assert ("lattice_v" in lat.features()) == expect
+        zl = [lat.apply(x) for x in r] + [lat.apply(r[0])]
+        n1 = lat.hierarchy()[1][0]
+        del lat
+        monkeypatch.setenv("SDG_GS_KNOB_ROWS", str(n1))  # the knobs act on level 1 only
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        walk = sdc.AmgPreconditioner(mat, opts)
+        assert "lattice_v" not in walk.features()
+        zk = [walk.apply(x) for x in r]
+        for k in knobs:
+            monkeypatch.delenv(k)
+        assert np.array_equal(zl[0], zk[0]) and np.array_equal(zl[1], zk[1])
+        assert np.array_equal(zl[2], zl[0])
+
+
 def test_c2_merge_and_interface_split_agree(monkeypatch):
     """The c2 bench system: the td_bgs apply with the interface split and the
     merged walks (defaults) against the plain sequential apply with unmerged
