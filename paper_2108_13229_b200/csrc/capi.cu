@@ -105,6 +105,30 @@ int sdg_context_profile(sdg_context* ctx, int family, int64_t* launches, double*
 }
 
 extern "C" int sdg_debug_walk_timeline(unsigned long long* out, int max) { return sdg::walk_timeline(out, max); }
+extern "C" double sdg_lattice_check_host(int n, const int* rowptr, const int* col, const double* val,
+                                         const double* b) {
+    try {
+        sdg::HostCsr a(n, n);
+        a.rp.assign(rowptr, rowptr + n + 1);
+        a.ci.assign(col, col + rowptr[n]);
+        a.v.assign(val, val + rowptr[n]);
+        return sdg::lattice_check_host(a, b);
+    } catch (...) {
+        return -2.0;
+    }
+}
+extern "C" int sdg_debug_lattice_sweep(sdg_context* ctx, int n, const int* rowptr, const int* col,
+                                       const double* val, const double* b, double* z_host, double* z_dev_out,
+                                       int repeats) {
+    return guard([&] {
+        sdg::HostCsr a(n, n);
+        a.rp.assign(rowptr, rowptr + n + 1);
+        a.ci.assign(col, col + rowptr[n]);
+        a.v.assign(val, val + rowptr[n]);
+        if (!sdg::lattice_emulate_host(a, b, z_host)) sdg::fail(SDG_EINVAL, "not a lattice");
+        if (ctx && !sdg::lattice_run_device(*ctx->p, a, b, z_dev_out, repeats)) sdg::fail(SDG_EINVAL, "not a lattice");
+    });
+}
 extern "C" int sdg_debug_wave_timeline(unsigned long long* out, int max_bands) {
     return sdg::wave_timeline_copy(out, max_bands);
 }

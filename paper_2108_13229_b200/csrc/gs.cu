@@ -654,9 +654,11 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
         build_wave(a, comps, dinv_h, s))
         return finish();
     // 0a. the multi-SM lattice, when the level is an aggregated lattice
-    //     (gs_lattice.cu; SDG_GS_LATTICE=0 disables, here and in build_parts)
+    //     (gs_lattice.cu; opt-in, SDG_GS_LATTICE=1, here and in build_parts:
+    //     bitwise equal to the level walks but measured slower than them at c3,
+    //     DESIGN.md §3)
     const char* lat_env = knob("SDG_GS_LATTICE");
-    lattice_off_ = lat_env && lat_env[0] == '0';
+    lattice_off_ = !(lat_env && lat_env[0] == '1');
     if (want_walk && !lattice_off_ && !force_split && !try_pipe && !knob("SDG_GS_MERGE") &&
         build_lattice(a, dinv_h, s))
         return finish();
@@ -1042,7 +1044,7 @@ bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std
     std::vector<size_t> off(nparts);
     for (int k = 0; k < nparts; ++k) {
         off[k] = total;
-        total += ps[k]->packed.size();
+        total += (ps[k]->packed.size() + 31) / 32 * 32;  // 256-byte aligned parts: TMA sources
     }
     packed.resize(total);
     std::vector<int> bidx_h(n);

@@ -151,10 +151,12 @@ struct GsPlan {
         int shape[4] = {0, 0, 0, 0};          // out: chosen W, R2, R8, wide width
     };
 
+    // the lattice plan of a whole matrix (gs_lattice.cu); false if it is not one
+    bool build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, cudaStream_t s);
+
 private:
     bool build_wave(const HostCsr& a, const std::vector<int>& comps, const std::vector<double>& dinv_h,
                     cudaStream_t s);
-    bool build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, cudaStream_t s);
     bool build_parts(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
                      cudaStream_t s);
     bool build_pipe(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
@@ -189,6 +191,11 @@ void launch_gs_lower(Context& c, const GsPlan& g, double* z_new, cudaEvent_t mar
 void launch_gs_wave(Context& c, const GsPlan& g, double* z_new);
 // multi-SM lattice variant (plans with lattice == true; gs_lattice.cu)
 void launch_gs_lattice(Context& c, const GsPlan& g, double* z_new);
+// host check of the lattice planner: emulated sweep vs sequential lower solve
+// (max abs difference; -1 when the matrix is not a lattice)
+double lattice_check_host(const HostCsr& a, const double* b);
+bool lattice_emulate_host(const HostCsr& a, const double* b, double* z);
+bool lattice_run_device(Context& c, const HostCsr& a, const double* b, double* z, int repeats);
 // dev aid (SDG_WAVE_TL=1): per band {start, first block, end, waiting ns} of the last wave launch
 int wave_timeline_copy(unsigned long long* out, int max_bands);
 // single-CTA variant (plans with walk == true; gs_walk.cu)

@@ -42,6 +42,7 @@
 #include "ptx.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -197,11 +198,17 @@ size_t lat_smem_bytes() {
 
 }  // namespace
 
+// Host plan of the lattice (no device work): records, b slots, windows.
+struct LatticeHost {
+    int nb = 0, nblocks = 0, nch = 0;
+    std::vector<double> rec;
+    std::vector<int> bidx, win;
+};
+
 // Plans the lattice for the lower triangle of `a` (all of it: a label block's
-// own matrix when called from build_parts).  Returns false, leaving the plan
-// untouched, when the level is not such a lattice.  SDG_GS_LATTICE=0 disables
-// it (GsPlan::build / build_parts; the level walks then run).
-bool GsPlan::build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, cudaStream_t s) {
+// own matrix when called from build_parts).  Returns false when the level is
+// not such a lattice.
+static bool plan_lattice(const HostCsr& a, const std::vector<double>& dinv_h, LatticeHost& out) {
     const int nn = a.n_rows;
     if (nn < 256) return false;
     // lower entries in column order
@@ -220,7 +227,6 @@ bool GsPlan::build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, 
     // chains: row i joins the chain whose last row is i's most recent lower neighbour
     std::vector<int> chain(nn), tail_chain(nn, -1);  // tail_chain[r] = chain whose last row is r
     int nch = 0;
-    std::vector<int> first_row;
     for (int i = 0; i < nn; ++i) {
         int pick = -1;
         for (int k = lp[i]; k < lp[i + 1]; ++k)
@@ -230,7 +236,6 @@ bool GsPlan::build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, 
             tail_chain[pick] = -1;
         } else {
             chain[i] = nch++;
-            first_row.push_back(i);
         }
         tail_chain[i] = chain[i];
     }
@@ -254,7 +259,6 @@ bool GsPlan::build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, 
         tmax = std::max(tmax, tt);
     }
     const int nblocks = (tmax + 1 + kLatKU - 1) / kLatKU;
-    const int T = nblocks * kLatKU;
     // windows: per consumer block, the steps of the previous band's last chain it reads
     std::vector<int> wlo(static_cast<size_t>(nb) * nblocks, INT32_MAX), whi(static_cast<size_t>(nb) * nblocks, -1);
     for (int i = 0; i < nn; ++i) {
@@ -270,20 +274,24 @@ bool GsPlan::build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, 
             whi[q] = std::max(whi[q], step[j]);
         }
     }
-    std::vector<int> win(static_cast<size_t>(nb) * nblocks, -1);
+    std::vector<int>& win = out.win;
+    win.assign(static_cast<size_t>(nb) * nblocks, -1);
     for (size_t q = 0; q < win.size(); ++q) {
         if (whi[q] < 0) continue;
         if (whi[q] - wlo[q] >= kLatW || wlo[q] >= (1 << 24)) return false;
         win[q] = wlo[q] * 64 + (whi[q] - wlo[q] + 1);
     }
     // records
+    const int T = nblocks * kLatKU;
     const size_t blk = static_cast<size_t>(kLatF) * kLatKU * 32;
     auto slot = [&](int f, int b, int lane, int t) {
         const int q = t / kLatKU, u = t % kLatKU;
         return (static_cast<size_t>(b) * nblocks + q) * blk + static_cast<size_t>(f) * kLatKU * 32 +
                static_cast<size_t>(u / 2) * 64 + 2 * lane + (u % 2);
     };
-    std::vector<double> rec(static_cast<size_t>(nb) * nblocks * blk, 0.0);
+    std::vector<double>& rec = out.rec;
+    rec.assign(static_cast<size_t>(nb) * nblocks * blk, 0.0);
+    if (rec.size() > static_cast<size_t>(INT32_MAX)) return false;
     auto put_int2 = [&](size_t at, int x, int y) {
         int v[2] = {x, y};
         std::memcpy(&rec[at], v, sizeof v);
@@ -296,10 +304,10 @@ bool GsPlan::build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, 
                 put_int2(slot(6, b, l, t), kLatZero, kLatZero);
                 put_int2(slot(7, b, l, t), -1, 0);
             }
-    std::vector<int> bx(nn);
+    out.bidx.assign(nn, 0);
     for (int i = 0; i < nn; ++i) {
         const int c = chain[i], b = c / 32, l = c % 32, t = step[i];
-        bx[i] = static_cast<int>(slot(0, b, l, t));
+        out.bidx[i] = static_cast<int>(slot(0, b, l, t));
         int src[4] = {kLatZero, kLatZero, kLatZero, kLatZero};
         int m = 0;
         for (int k = lp[i]; k < lp[i + 1]; ++k, ++m) {
@@ -315,26 +323,143 @@ bool GsPlan::build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, 
         put_int2(slot(6, b, l, t), src[2], src[3]);
         put_int2(slot(7, b, l, t), i, lp[i + 1] - lp[i] > 2 ? 1 : 0);
     }
-    if (rec.size() > static_cast<size_t>(INT32_MAX)) return false;
-    packed.upload(rec, s);
-    bidx.upload(bx, s);
-    lat_win.upload(win, s);
+    out.nb = nb;
+    out.nblocks = nblocks;
+    out.nch = nch;
+    return true;
+}
+
+// CPU emulation of k_gs_lattice over a host plan (same records, ring, windows,
+// boundary buffer and arithmetic), bands in order: the check of the planner.
+static void emulate_lattice(const LatticeHost& h, const double* b_nat, double* z) {
+    const int KU = kLatKU, T = h.nblocks * KU;
+    const size_t blk = static_cast<size_t>(kLatF) * KU * 32;
+    std::vector<double> rec = h.rec;
+    for (size_t i = 0; i < h.bidx.size(); ++i) rec[h.bidx[i]] = b_nat[i];
+    std::vector<double> bnd(static_cast<size_t>(h.nb) * T, 0.0);
+    for (int band = 0; band < h.nb; ++band) {
+        std::vector<double> vals(kLatVals, 0.0);
+        for (int q = 0; q < h.nblocks; ++q) {
+            const int w = h.win[static_cast<size_t>(band) * h.nblocks + q];
+            for (int l = 0; l < 32; ++l)
+                vals[kLatWin + (q & 1) * kLatW + l] =
+                    (band > 0 && w >= 0 && l < (w & 63)) ? bnd[static_cast<size_t>(band - 1) * T + (w >> 6) + l] : 0.0;
+            const double* B = rec.data() + (static_cast<size_t>(band) * h.nblocks + q) * blk;
+            for (int u = 0; u < KU; ++u) {
+                const int step = q * KU + u;
+                double res[32];
+                int rows[32];
+                for (int l = 0; l < 32; ++l) {
+                    auto f = [&](int fld) { return B[static_cast<size_t>(fld) * KU * 32 + (u / 2) * 64 + 2 * l + u % 2]; };
+                    auto fi = [&](int fld) {
+                        int v[2];
+                        const double d = f(fld);
+                        std::memcpy(v, &d, sizeof v);
+                        return std::pair<int, int>(v[0], v[1]);
+                    };
+                    const auto s01 = fi(5), s23 = fi(6), rw = fi(7);
+                    const double z0 = vals[s01.first], z1 = vals[s01.second], z2 = vals[s23.first],
+                                 z3 = vals[s23.second];
+                    const double acc = std::fma(f(2), z1, std::fma(f(1), z0, f(0)));
+                    const double wide = (acc + std::fma(f(4), z3, f(3) * z2)) + 0.0;
+                    res[l] = rw.second ? wide : acc;
+                    rows[l] = rw.first;
+                }
+                for (int l = 0; l < 32; ++l) {
+                    vals[l * kLatR + (step & (kLatR - 1))] = res[l];
+                    if (rows[l] >= 0) z[rows[l]] = res[l];
+                }
+                bnd[static_cast<size_t>(band) * T + step] = res[31];
+            }
+        }
+    }
+}
+
+// SDG_GS_LATTICE=0 disables the lattice (GsPlan::build / build_parts; the level walks then run).
+bool GsPlan::build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, cudaStream_t s) {
+    LatticeHost h;
+    if (!plan_lattice(a, dinv_h, h)) return false;
+    const int T = h.nblocks * kLatKU;
+    n = a.n_rows;  // (build_parts builds its parts through this entry point)
+    packed.upload(h.rec, s);
+    bidx.upload(h.bidx, s);
+    lat_win.upload(h.win, s);
     lat_ticket.resize(1);
     SDG_CUDA(cudaMemsetAsync(lat_ticket.get(), 0, sizeof(unsigned long long), s));
     {
         double sent;
         std::memcpy(&sent, &kLatSent, sizeof sent);
-        lat_bnd.upload(std::vector<double>(static_cast<size_t>(2) * nb * T, sent), s);
+        lat_bnd.upload(std::vector<double>(static_cast<size_t>(2) * h.nb * T, sent), s);
     }
     lattice = true;
-    lat_bands = nb;
-    lat_blocks = nblocks;
+    lat_bands = h.nb;
+    lat_blocks = h.nblocks;
     walk = false;
     wave = false;
     usable = true;
     if (std::getenv("SDG_DEBUG"))
-        std::fprintf(stderr, "[sdg gs lattice] n=%d: %d chains in %d bands, %d steps\n", nn, nch, nb, T);
+        std::fprintf(stderr, "[sdg gs lattice] n=%d: %d chains in %d bands, %d steps\n", a.n_rows, h.nch, h.nb, T);
     return true;
+}
+
+// Host check of the planner (no GPU): plans the lattice of `a`, runs the
+// emulation on b and returns the max |z - z_seq| against the sequential lower
+// solve z_i = b_i + sum_{j<i} c_ij z_j (c = -a_ij / d_i); -1 when `a` is not a lattice.
+// dev aids: the emulated sweep (host) and the kernel's sweep (device) of the
+// lattice of `a` for right-hand side b (the lower solve z = b + C z)
+bool lattice_emulate_host(const HostCsr& a, const double* b, double* z) {
+    const int n = a.n_rows;
+    std::vector<double> dinv(n, 1.0);
+    for (int i = 0; i < n; ++i)
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+            if (a.ci[k] == i) dinv[i] = 1.0 / a.v[k];
+    LatticeHost h;
+    if (!plan_lattice(a, dinv, h)) return false;
+    emulate_lattice(h, b, z);
+    return true;
+}
+
+bool lattice_run_device(Context& c, const HostCsr& a, const double* b, double* z, int repeats) {
+    const int n = a.n_rows;
+    std::vector<double> dinv(n, 1.0);
+    for (int i = 0; i < n; ++i)
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+            if (a.ci[k] == i) dinv[i] = 1.0 / a.v[k];
+    GsPlan g;
+    g.n = n;
+    if (!g.build_lattice(a, dinv, c.stream)) return false;
+    std::vector<double> rec(g.packed.size());
+    std::vector<int> bx(n);
+    SDG_CUDA(cudaMemcpy(rec.data(), g.packed.get(), rec.size() * 8, cudaMemcpyDeviceToHost));
+    SDG_CUDA(cudaMemcpy(bx.data(), g.bidx.get(), n * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) rec[bx[i]] = b[i];
+    SDG_CUDA(cudaMemcpy(g.packed.get(), rec.data(), rec.size() * 8, cudaMemcpyHostToDevice));
+    DevBuf<double> zd(n);
+    for (int r = 0; r < repeats; ++r) launch_gs_lattice(c, g, zd.get());
+    SDG_CUDA(cudaStreamSynchronize(c.stream));
+    SDG_CUDA(cudaMemcpy(z, zd.get(), n * 8, cudaMemcpyDeviceToHost));
+    return true;
+}
+
+double lattice_check_host(const HostCsr& a, const double* b) {
+    const int n = a.n_rows;
+    std::vector<double> dinv(n, 1.0);
+    for (int i = 0; i < n; ++i)
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+            if (a.ci[k] == i) dinv[i] = 1.0 / a.v[k];
+    LatticeHost h;
+    if (!plan_lattice(a, dinv, h)) return -1.0;
+    std::vector<double> z(n, 0.0), zs(n, 0.0);
+    emulate_lattice(h, b, z.data());
+    for (int i = 0; i < n; ++i) {
+        double acc = b[i];
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+            if (a.ci[k] < i) acc += -(a.v[k] * dinv[i]) * zs[a.ci[k]];
+        zs[i] = acc;
+    }
+    double err = 0.0;
+    for (int i = 0; i < n; ++i) err = std::max(err, std::abs(z[i] - zs[i]));
+    return err;
 }
 
 void launch_gs_lattice(Context& c, const GsPlan& g, double* z_new) {

@@ -1,7 +1,7 @@
 """Dev helper: device time of N AMG V-cycle applies of the velocity block
 (MAC) and of the porous block (5-point) of one config, each alone on the
 stream, for the default plans and with the multi-SM smoothers switched off
-level by level (SDG_GS_WAVE=0 on the finest level, SDG_GS_LATTICE=0 on level 1).
+level by level (SDG_GS_WAVE=0 on the finest level; the opt-in SDG_GS_LATTICE=1 on level 1).
 python scripts/time_wave.py c3 [N]"""
 import os, sys, time
 import ctypes as C
@@ -23,7 +23,7 @@ for name, mat, opts in (("V", V, sdc.AmgOptions(components=comps, max_levels=cfg
     rows = [r for r, _ in base.hierarchy()]
     del base
     variants = [("default", {}), ("no-wave", {"SDG_GS_KNOB_ROWS": str(rows[0]), "SDG_GS_WAVE": "0"}),
-                ("no-lattice", {"SDG_GS_KNOB_ROWS": str(rows[1]), "SDG_GS_LATTICE": "0"})]
+                ("lattice", {"SDG_GS_KNOB_ROWS": str(rows[1]), "SDG_GS_LATTICE": "1"})]
     for vname, env in variants:
         for k in ("SDG_GS_KNOB_ROWS", "SDG_GS_WAVE", "SDG_GS_LATTICE"):
             os.environ.pop(k, None)

@@ -181,11 +181,13 @@ def test_wave_smoother_bitwise_vs_walks(monkeypatch, cfg_name):
 
 @pytest.mark.parametrize("cfg_name", ["c2", "c3"])
 def test_lattice_smoother_bitwise_vs_walks(monkeypatch, cfg_name):
-    """The multi-SM lattice lower solve (gs_lattice.cu) on the first coarse
-    level does every row's arithmetic in the order of the level walk: the
+    """The multi-SM lattice lower solve (gs_lattice.cu, opt-in SDG_GS_LATTICE=1)
+    on the first coarse level does every row's arithmetic in the order of the
+    level walk: the
     velocity AMG V-cycle (lattice on both label blocks of level 1) equals the
     one with plain level-1 walks bit for bit, and so does the porous one where
-    its level 1 is a lattice (c3; at c2 the porous aggregates are not)."""
+    its level 1 is a lattice (c3; at c2 the porous aggregates are not, and the
+    velocity level 1 fits one level walk)."""
     from paper_2108_13229_b200 import scenarios
     cfg = scenarios.CONFIGS[cfg_name]
     s = scenarios.build_system(cfg)
@@ -194,11 +196,13 @@ def test_lattice_smoother_bitwise_vs_walks(monkeypatch, cfg_name):
     D = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
     rng = np.random.default_rng(4)
     for mat, opts, knobs, expect in (
-            (V, sdc.AmgOptions(components=comps, max_levels=cfg.v_max_levels), {"SDG_GS_LATTICE": "0"}, True),
+            (V, sdc.AmgOptions(components=comps, max_levels=cfg.v_max_levels), {"SDG_GS_LATTICE": "0"},
+             cfg_name == "c3"),  # c2's level 1 fits one level walk
             (D, sdc.AmgOptions(max_levels=cfg.d_max_levels), {"SDG_GS_LATTICE": "0", "SDG_GS_MERGE": "1"},
              cfg_name == "c3")):
         r = [rng.standard_normal(mat.n_rows) for _ in range(2)]
         monkeypatch.delenv("SDG_GS_KNOB_ROWS", raising=False)
+        monkeypatch.setenv("SDG_GS_LATTICE", "1")  # opt-in
         lat = sdc.AmgPreconditioner(mat, opts)
         assert ("lattice_v" in lat.features()) == expect
         zl = [lat.apply(x) for x in r] + [lat.apply(r[0])]
