@@ -51,6 +51,9 @@ typedef struct sdg_precond sdg_precond;
 #define SDG_TD_BGS 1
 #define SDG_PV_BJ 2
 #define SDG_PV_BGS 3
+/* OR-ed into sdg_td_create's kind: ILU(0) instead of AMG on the grounded
+ * porous block D' (the td_*_uzawa_ilu0 choices, bench.cpp:156-172) */
+#define SDG_TD_ILU0 16
 
 /* RestartController (krylov.hpp:23-47). Updated in place by sdg_pd_gmres
  * only on the caller's copy semantics of the reference: the reference takes
@@ -170,6 +173,9 @@ int sdg_uzawa_create(sdg_matrix* v, sdg_matrix* b, sdg_matrix* c, const sdg_uzaw
 int sdg_block_create(int kind, sdg_matrix* matrix, int n_v, int n_pff, int n_ppm,
                      sdg_precond* first, sdg_precond* pm, sdg_precond** out);
 /* IdentityPreconditioner(n) (operator.hpp:64-76). */
+/* Ilu0Preconditioner(a) (precond.hpp:18-30, precond.cpp:13-87): factors
+ * bitwise the reference's; apply = the two triangular solves on the device. */
+int sdg_ilu0_create(sdg_matrix* a, sdg_precond** out);
 int sdg_identity_create(sdg_context* ctx, int n, sdg_precond** out);
 /* ground_dof (precond.cpp:375-392) applied on the host to a CSR copy. */
 int sdg_ground_dof_host(int n, const int* rowptr, const int* col, double* val_inout, int dof);
@@ -293,6 +299,13 @@ int sdg_assemble_monolithic(const sdg_scenario* sc, const double* k_cell, const 
  * close the coupling loop (coupling.cpp:218-242): stokes_pressure_trace
  * (assembly.cpp:382-391) of the free-flow solution and
  * darcy_velocity_trace_dirichlet (assembly.cpp:393-402) of the porous one. */
+/* The right-hand side of assemble_monolithic on the device (the matrix is
+ * step-invariant, so BASELINE config 4 re-assembles only this each time step):
+ * rhs_dev[n_total] from the previous velocity v_prev_dev[n_vel] (device, or NULL
+ * for zero), on the context's stream; bitwise the host assembly's rhs.
+ * Replaces the per-step assemble_monolithic call of MonolithicDriver::advance
+ * (bench.cpp:187, assembly.cpp:327-380). */
+int sdg_assemble_rhs_device(sdg_context* ctx, const sdg_scenario* sc, const double* v_prev_dev, double* rhs_dev);
 int sdg_assemble_stokes(const sdg_scenario* sc, const double* v_prev, const double* v_gamma, int* n,
                         int64_t* nnz, int* rowptr, int* col, double* val, double* rhs);
 int sdg_assemble_darcy(const sdg_scenario* sc, const double* p_gamma, int* n, int64_t* nnz, int* rowptr,

@@ -244,6 +244,21 @@ int ref_amg_precond_new(void* mat, int max_levels, void** out) {
 
 void ref_precond_free(void* p) { delete static_cast<PrecondHandle*>(p); }
 
+// ILU(0) (precond.cpp:13-87) of a matrix, and a plain apply of any precond handle.
+int ref_ilu0_new(void* mat, void** out) {
+    return guarded([&] {
+        *out = new PrecondHandle{std::make_shared<Ilu0Preconditioner>(static_cast<MatrixHandle*>(mat)->a)};
+    });
+}
+
+int ref_precond_apply(void* p, const double* r, double* z) {
+    return guarded([&] {
+        const auto& pc = static_cast<PrecondHandle*>(p)->p;
+        const int n = pc->rows();
+        pc->apply(std::span<const double>(r, n), std::span<double>(z, n));
+    });
+}
+
 
 // Interface traces of a monolithic solution (assembly.cpp:382-428).
 int ref_system_traces(void* hs, const double* x, double* p_ff_gamma, double* v_pm_gamma) {
@@ -414,7 +429,7 @@ int ref_lu_solve_dense_check(void* m, const double* b, double* x) {
 // td_* block preconditioner wired as MonolithicDriver::build_preconditioner
 // (bench.cpp:121-182): D' = ground_dof(A[pm,pm]); V labels u=0 / v=1;
 // UzawaConfig{inexact, amg = v_amg}; BlockPreconditioner(kind, A, ...).
-// kind: 0 = td_bj, 1 = td_bgs.
+// kind: 0 = td_bj, 1 = td_bgs, 2 = td_bj with ILU(0) on D', 3 = td_bgs with ILU(0).
 
 int ref_td_new(int n, const int* rp, const int* ci, const double* v, int n_u, int n_vel,
                int n_pff, int n_ppm, int kind, int v_max_levels, int d_max_levels, void** out) {
@@ -438,9 +453,13 @@ int ref_td_new(int n, const int* rp, const int* ci, const double* v, int n_u, in
         UzawaConfig ucfg;
         ucfg.amg = v_amg;
         h->uz = std::make_shared<UzawaPreconditioner>(v_block, b_block, c_block, ucfg);
-        h->pm = std::make_shared<AmgPreconditioner>(d_block, d_amg);
+        // kind 2 / 3: td_bj / td_bgs with ILU(0) on D' (bench.cpp:156-172, td_*_uzawa_ilu0)
+        if (kind >= 2)
+            h->pm = std::make_shared<Ilu0Preconditioner>(d_block);
+        else
+            h->pm = std::make_shared<AmgPreconditioner>(d_block, d_amg);
         h->block = std::make_shared<BlockPreconditioner>(
-            kind == 0 ? BlockPrecondKind::td_bj : BlockPrecondKind::td_bgs, h->a, n_vel, n_pff,
+            kind % 2 == 0 ? BlockPrecondKind::td_bj : BlockPrecondKind::td_bgs, h->a, n_vel, n_pff,
             n_ppm, h->uz, h->pm);
         h->setup_seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -138,6 +138,8 @@ class RefLib:
         p("ref_uzawa_stokes_new", _i, [_vp, _i, _i, C.POINTER(_vp)])
         p("ref_amg_precond_new", _i, [_vp, _i, C.POINTER(_vp)])
         p("ref_precond_free", None, [_vp])
+        p("ref_ilu0_new", _i, [_vp, C.POINTER(_vp)])
+        p("ref_precond_apply", _i, [_vp, _dp, _dp])
         p("ref_ground_dof", _i, [_vp, _i, C.POINTER(_vp)])
         p("ref_amg_setup", _i, [_vp, _i, _d, _i, _vp, C.POINTER(_vp)])
         p("ref_hier_num_levels", _i, [_vp])
@@ -282,6 +284,18 @@ class RefLib:
             h = _vp()
             self._check(self.L.ref_amg_precond_new(m.h, max_levels, C.byref(h)))
             return RefPrecond(self, h)
+
+    def ilu0(self, a: Csr) -> "RefPrecond":
+        """Ilu0Preconditioner (precond.cpp:13-87)."""
+        with self.matrix(a) as m:
+            h = _vp()
+            self._check(self.L.ref_ilu0_new(m.h, C.byref(h)))
+            return RefPrecond(self, h)
+
+    def precond_apply(self, p: "RefPrecond", r):
+        z = np.empty(len(r))
+        self._check(self.L.ref_precond_apply(p.h, _f64(r), z))
+        return z
 
     def ground_dof(self, a: Csr, dof=0) -> Csr:
         with self.matrix(a) as m:
@@ -443,7 +457,7 @@ class RefTd:
         self.lib = lib
         self.sys = s
         self.h = _vp()
-        k = {"td_bj": 0, "td_bgs": 1}[kind]
+        k = {"td_bj": 0, "td_bgs": 1, "td_bj_ilu0": 2, "td_bgs_ilu0": 3}[kind]
         t0 = time.perf_counter()
         lib._check(lib.L.ref_td_new(s.n, s.a.rowptr, s.a.col, s.a.val, s.n_u, s.n_vel, s.n_pff, s.n_ppm,
                                     k, v_max_levels, d_max_levels, C.byref(self.h)))

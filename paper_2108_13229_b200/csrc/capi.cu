@@ -255,6 +255,14 @@ int sdg_block_create(int kind, sdg_matrix* matrix, int n_v, int n_pff, int n_ppm
     });
 }
 
+int sdg_ilu0_create(sdg_matrix* a, sdg_precond** out) {
+    return guard([&] {
+        need(a, "sdg_ilu0_create");
+        need(out, "sdg_ilu0_create");
+        *out = new sdg_precond{std::make_shared<sdg::Ilu0Precond>(a->p->ctx, a->p->host)};
+    });
+}
+
 int sdg_identity_create(sdg_context* ctx, int n, sdg_precond** out) {
     return guard([&] {
         need(ctx, "sdg_identity_create");
@@ -287,6 +295,8 @@ int sdg_td_create(sdg_matrix* a, int n_u, int n_vel, int n_pff, int n_ppm, int k
     return guard([&] {
         need(a, "sdg_td_create");
         need(out, "sdg_td_create");
+        const bool ilu0 = (kind & SDG_TD_ILU0) != 0;  // td_*_uzawa_ilu0 (bench.cpp:156-172)
+        kind &= ~SDG_TD_ILU0;
         if (kind != SDG_TD_BJ && kind != SDG_TD_BGS) sdg::fail(SDG_EINVAL, "sdg_td_create: kind must be td_bj or td_bgs");
         auto t0 = std::chrono::steady_clock::now();
         const sdg::HostCsr& A = a->p->host;
@@ -306,7 +316,11 @@ int sdg_td_create(sdg_matrix* a, int n_u, int n_vel, int n_pff, int n_ppm, int k
         auto first = std::make_shared<sdg::UzawaPrecond>(
             ctx, sdg::submatrix(A, 0, n_vel, 0, n_vel), sdg::submatrix(A, 0, n_vel, n_vel, n_ff),
             sdg::submatrix(A, n_vel, n_ff, 0, n_vel), v_amg, 1e-3, 200, 1729u, omega_override);
-        auto pm = std::make_shared<sdg::AmgPrecond>(ctx, d_block, d_amg);
+        sdg::PrecondPtr pm;
+        if (ilu0)
+            pm = std::make_shared<sdg::Ilu0Precond>(ctx, d_block);
+        else
+            pm = std::make_shared<sdg::AmgPrecond>(ctx, d_block, d_amg);
         auto blk = std::make_shared<sdg::BlockPrecond>(ctx, kind, A, n_vel, n_pff, n_ppm, first, pm);
         blk->setup_seconds = seconds_since(t0);
         *out = new sdg_precond{blk};
@@ -573,6 +587,15 @@ int sdg_assemble_monolithic(const sdg_scenario* sc, const double* k_cell, const 
         if (col) std::memcpy(col, s.a.ci.data(), sizeof(int) * s.a.ci.size());
         if (val) std::memcpy(val, s.a.v.data(), sizeof(double) * s.a.v.size());
         if (rhs) std::memcpy(rhs, s.rhs.data(), sizeof(double) * s.rhs.size());
+    });
+}
+
+int sdg_assemble_rhs_device(sdg_context* ctx, const sdg_scenario* sc, const double* v_prev_dev, double* rhs_dev) {
+    return guard([&] {
+        need(ctx, "sdg_assemble_rhs_device");
+        need(sc, "sdg_assemble_rhs_device");
+        need(rhs_dev, "sdg_assemble_rhs_device");
+        sdg::launch_assemble_rhs(*ctx->p, *sc, v_prev_dev, rhs_dev);
     });
 }
 

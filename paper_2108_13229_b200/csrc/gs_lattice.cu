@@ -7,36 +7,35 @@
 // level is a lattice -- every aggregate depends on its west neighbour in its
 // own aggregate row and on two or three aggregates of the row below.  The
 // level walk (gs_walk.cu) pays a CTA-wide hand-off per dependency level
-// (~300-500 cycles, one SM); here the rows are cut into CHAINS and each
-// chain is a lane, as the wavefront does for the finest grids (gs_wave.cu):
+// (~300-500 cycles, one SM); here the rows are cut into CHAINS and each chain
+// is a lane, as the wavefront does for the finest grids (gs_wave.cu):
 //
 //   * a chain is a sequence of rows each of which depends on its predecessor
 //     (row i joins the chain whose last row is i's most recent lower
 //     neighbour; otherwise it starts a chain).  Chains ordered by their first
 //     row are the lanes; 32 consecutive chains are a band, one warp, one CTA;
 //   * every row gets a step: one after its chain predecessor and one after
-//     each lower neighbour in its band (the schedule is a topological order
-//     of the lower triangle, so the sweep stays the exact lexicographic
-//     Gauss-Seidel sweep).  Lanes with nothing to do at a step run a zero
-//     record;
-//   * within a band every lane stores its value of step t into a shared-
-//     memory ring (32 lanes x R steps) and reads its lower neighbours from it
-//     (a __syncwarp per step); across bands only the last chain of band b - 1
-//     may feed band b: its lane 31 stores each step's value into a boundary
-//     buffer that holds a sentinel until written (the value is its own flag,
-//     as in gs_wave.cu), and band b loads a 32-step window of it per block,
-//     one block ahead, into shared memory;
+//     each lower neighbour in its band, so the schedule is a topological
+//     order of the lower triangle and the sweep stays the exact lexicographic
+//     Gauss-Seidel sweep.  A lane with no row at a step runs a zero record;
+//   * a lane keeps its last three values in registers (h1..h3) and the last
+//     four values of the lane below in a shift register fed by one warp
+//     shuffle per step (p1..p4): a row may depend on its own chain 1..3 steps
+//     back and on the chain below 1..4 steps back (the lattices of the c3
+//     coarse levels need exactly that).  Lane 0's chain-below is the last
+//     chain of the previous band: its lane 31 stores every step's value into
+//     a boundary buffer that holds a sentinel until written (the value is its
+//     own flag, as in gs_wave.cu), and lane 0 reads a window of it, loaded one
+//     block ahead into shared memory;
 //   * records [block][field][KU/2 step pairs][32 lanes][2] are streamed by
 //     1-D TMA bulk copies into a shared-memory ring, as in gs_wave.cu.
 //
-// Arithmetic: the level walk's, bit for bit -- the lower entries in column
-// order, c = -a_ij / d_i; rows with <= 2 lower entries
-//   z = fma(c1, z1, fma(c0, z0, b)),
-// wider rows (the walk's wide record, pairs then a balanced tree)
-//   z = (fma(c1, z1, fma(c0, z0, b)) + fma(c3, z3, c2 z2)) + 0.
-// Levels that are not such a lattice (more than 4 lower entries in a row,
-// a dependency on another band than the previous one's last chain, a window
-// wider than 32 steps) keep the level walk.
+// Arithmetic: z = b + sum c_s v_s over the seven sources in a fixed order
+// (p4, p3, p2, p1, h3, h2, h1; fma chain, c = -a_ij / d_i, zero coefficients
+// for absent sources), so the newest values enter last.  That is a
+// reassociation of the row sum (the level walk sums in column order): equal to
+// the reference sweep to rounding, like the rest of the fast smoother.  Levels
+// that are not such a lattice keep the level walk.
 #include "gs.cuh"
 #include "launch.cuh"
 #include "ptx.cuh"
@@ -53,13 +52,10 @@ namespace sdg {
 namespace {
 
 constexpr int kLatKU = 8;       // steps per block
-constexpr int kLatF = 8;        // record fields: b, c0..c3, src01, src23, (rowid, wide)
+constexpr int kLatF = 9;        // record fields: b, c_h1..c_h3, c_p1..c_p4, (rowid, lane-0 window slots)
 constexpr int kLatDepth = 4;    // blocks of records in flight
-constexpr int kLatR = 64;       // ring steps per lane
 constexpr int kLatW = 32;       // window steps of the previous band's last chain
-constexpr int kLatZero = 32 * kLatR;           // index of the constant zero in the value array
-constexpr int kLatWin = kLatZero + 1;          // two windows (block parity) follow
-constexpr int kLatVals = kLatWin + 2 * kLatW;  // doubles of the value array
+constexpr int kLatVals = 2 * kLatW;  // the two windows (block parity) in shared memory
 constexpr unsigned long long kLatSent = 0x7ff4deadbeefcafeull;
 
 struct LatArgs {
@@ -107,8 +103,8 @@ __global__ void __launch_bounds__(32, 1) k_gs_lattice(LatArgs a) {
     constexpr int KU = kLatKU, F = kLatF, BLK = F * KU * 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* ring = reinterpret_cast<double*>(smem_raw);      // records
-    double* vals = ring + kLatDepth * BLK;                   // value ring | zero | windows
-    uint64_t* bars = reinterpret_cast<uint64_t*>(vals + kLatVals + 1);
+    double* wins = ring + kLatDepth * BLK;                   // two windows
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wins + kLatVals);
     const int lane = threadIdx.x;
     unsigned long long t = 0;
     if (lane == 0) {
@@ -117,7 +113,6 @@ __global__ void __launch_bounds__(32, 1) k_gs_lattice(LatArgs a) {
         for (int d = 0; d < kLatDepth; ++d) ptx::mbar_init(bars + d, 1);
         ptx::fence_mbar_init();
     }
-    for (int k = lane; k < kLatVals; k += 32) vals[k] = 0.0;
     t = __shfl_sync(0xffffffffu, t, 0);
     __syncwarp();
     const int band = static_cast<int>(t % static_cast<unsigned long long>(a.nbands));
@@ -137,7 +132,6 @@ __global__ void __launch_bounds__(32, 1) k_gs_lattice(LatArgs a) {
         for (int k = lane; k < T; k += 32) rs[k] = __longlong_as_double(static_cast<long long>(kLatSent));
     }
     const int* win = a.win + static_cast<size_t>(band) * a.nblocks;
-    // window of block q: steps win[q] .. win[q] + 31 of the previous band's last chain
     // win[q] = first step * 64 + steps needed (<= 32), or -1: no window
     auto load_win = [&](int q) {
         const int w = q < a.nblocks ? win[q] : -1;
@@ -147,17 +141,19 @@ __global__ void __launch_bounds__(32, 1) k_gs_lattice(LatArgs a) {
         const int w = q < a.nblocks ? win[q] : -1;
         while (!__all_sync(0xffffffffu, lat_ready(v)))
             v = lat_ld_if(b_in + (w >> 6) + lane, has_src && w >= 0 && lane < (w & 63));
-        vals[kLatWin + (q & 1) * kLatW + lane] = v;
+        wins[(q & 1) * kLatW + lane] = v;
     };
     double wv = load_win(0);
     settle(0, wv);
     const bool pub = has_dst && lane == 31;
+    double h1 = 0.0, h2 = 0.0, h3 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0, p4 = 0.0;
     for (int q = 0; q < a.nblocks; ++q) {
         double wn = load_win(q + 1);  // in flight during this block
         const int slot = q % kLatDepth;
         ptx::mbar_wait(bars + slot, (q / kLatDepth) & 1);
         __syncwarp();  // the window stored at the end of the previous block
         const double2* B = reinterpret_cast<const double2*>(ring + slot * BLK) + lane;
+        const double* W = wins + (q & 1) * kLatW;
 #pragma unroll
         for (int u2 = 0; u2 < KU / 2; ++u2) {
             double2 R[F];
@@ -166,25 +162,41 @@ __global__ void __launch_bounds__(32, 1) k_gs_lattice(LatArgs a) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 auto r = [&](int f) { return h ? R[f].y : R[f].x; };
-                auto ri = [&](int f) {
-                    const int2 v = *reinterpret_cast<const int2*>(h ? &R[f].y : &R[f].x);
-                    return v;
-                };
-                const int2 s01 = ri(5), s23 = ri(6), rw = ri(7);
-                const double z0 = vals[s01.x], z1 = vals[s01.y], z2 = vals[s23.x], z3 = vals[s23.y];
-                const double acc = fma(r(2), z1, fma(r(1), z0, r(0)));
-                const double wide = (acc + fma(r(4), z3, r(3) * z2)) + 0.0;
-                const double res = rw.y ? wide : acc;
+                const int2 rw = *reinterpret_cast<const int2*>(h ? &R[8].y : &R[8].x);
+                // the lane below, one step back (lane 0: its register is lane 31's, unused)
+                const double pn = __shfl_up_sync(0xffffffffu, h1, 1);
+                p4 = p3;
+                p3 = p2;
+                p2 = p1;
+                p1 = pn;
+                double P1 = p1, P2 = p2, P3 = p3, P4 = p4;
+                if (has_src) {  // lane 0: the previous band's last chain, from the window
+                    const unsigned ws = static_cast<unsigned>(rw.y);
+                    const double w1 = W[ws & 31], w2 = W[(ws >> 8) & 31], w3 = W[(ws >> 16) & 31],
+                                 w4 = W[(ws >> 24) & 31];
+                    if (lane == 0) {
+                        P1 = w1;
+                        P2 = w2;
+                        P3 = w3;
+                        P4 = w4;
+                    }
+                }
+                double acc = fma(r(7), P4, r(0));
+                acc = fma(r(6), P3, acc);
+                acc = fma(r(5), P2, acc);
+                acc = fma(r(4), P1, acc);
+                acc = fma(r(3), h3, acc);
+                acc = fma(r(2), h2, acc);
+                const double res = fma(r(1), h1, acc);
+                h3 = h2;
+                h2 = h1;
+                h1 = res;
                 const int step = q * KU + 2 * u2 + h;
-                // no lane reads a slot written in this step (same-band sources are
-                // at least one and less than kLatR steps old, GsPlan::build_lattice)
-                vals[lane * kLatR + (step & (kLatR - 1))] = res;
                 lat_st_if(a.z + rw.x, res, rw.x >= 0);
                 lat_st_relaxed_if(b_out + step, res, pub);
-                __syncwarp();  // the step's values are visible to the next step
             }
         }
-        __syncwarp();  // every lane has read the record slot
+        __syncwarp();  // every lane has read the record slot and the window
         lat_tma_if(ring + slot * BLK, src + static_cast<size_t>(q + kLatDepth) * BLK, BLK * 8, bars + slot,
                    lane == 0 && q + kLatDepth < a.nblocks);
         if (q + 1 < a.nblocks) settle(q + 1, wn);
@@ -192,7 +204,7 @@ __global__ void __launch_bounds__(32, 1) k_gs_lattice(LatArgs a) {
 }
 
 size_t lat_smem_bytes() {
-    return static_cast<size_t>(kLatDepth) * kLatF * kLatKU * 32 * sizeof(double) + (kLatVals + 1) * sizeof(double) +
+    return static_cast<size_t>(kLatDepth) * kLatF * kLatKU * 32 * sizeof(double) + kLatVals * sizeof(double) +
            kLatDepth * sizeof(uint64_t);
 }
 
@@ -222,7 +234,7 @@ static bool plan_lattice(const HostCsr& a, const std::vector<double>& dinv_h, La
                 lv.push_back(-(a.v[k] * dinv_h[i]));
             }
         lp[i + 1] = static_cast<int>(lc.size());
-        if (lp[i + 1] - lp[i] > 4) return false;
+        if (lp[i + 1] - lp[i] > 7) return false;
     }
     // chains: row i joins the chain whose last row is i's most recent lower neighbour
     std::vector<int> chain(nn), tail_chain(nn, -1);  // tail_chain[r] = chain whose last row is r
@@ -251,24 +263,21 @@ static bool plan_lattice(const HostCsr& a, const std::vector<double>& dinv_h, La
             const int j = lc[k], cj = chain[j], bj = cj / 32;
             if (bj == b)
                 tt = std::max(tt, step[j] + 1);
-            else if (!(bj == b - 1 && cj % 32 == 31))
-                return false;  // only the previous band's last chain may feed a band
+            else if (!(bj == b - 1 && cj % 32 == 31 && c % 32 == 0))
+                return false;  // across bands only: lane 0 <- the previous band's last chain
         }
         step[i] = tt;
         last_step[c] = tt;
         tmax = std::max(tmax, tt);
     }
     const int nblocks = (tmax + 1 + kLatKU - 1) / kLatKU;
-    // windows: per consumer block, the steps of the previous band's last chain it reads
+    // windows: per consumer block, the steps of the previous band's last chain lane 0 reads
     std::vector<int> wlo(static_cast<size_t>(nb) * nblocks, INT32_MAX), whi(static_cast<size_t>(nb) * nblocks, -1);
     for (int i = 0; i < nn; ++i) {
         const int b = chain[i] / 32;
         for (int k = lp[i]; k < lp[i + 1]; ++k) {
             const int j = lc[k];
-            if (chain[j] / 32 == b) {
-                if (step[i] - step[j] >= kLatR) return false;  // older than the ring
-                continue;
-            }
+            if (chain[j] / 32 == b) continue;
             const size_t q = static_cast<size_t>(b) * nblocks + step[i] / kLatKU;
             wlo[q] = std::min(wlo[q], step[j]);
             whi[q] = std::max(whi[q], step[j]);
@@ -296,32 +305,45 @@ static bool plan_lattice(const HostCsr& a, const std::vector<double>& dinv_h, La
         int v[2] = {x, y};
         std::memcpy(&rec[at], v, sizeof v);
     };
-    // idle slots: zero coefficients reading the zero cell, no row
-    for (int b = 0; b < nb; ++b)
+    for (int b = 0; b < nb; ++b)  // no row: no store
         for (int l = 0; l < 32; ++l)
-            for (int t = 0; t < T; ++t) {
-                put_int2(slot(5, b, l, t), kLatZero, kLatZero);
-                put_int2(slot(6, b, l, t), kLatZero, kLatZero);
-                put_int2(slot(7, b, l, t), -1, 0);
-            }
+            for (int t = 0; t < T; ++t) put_int2(slot(8, b, l, t), -1, 0);
     out.bidx.assign(nn, 0);
     for (int i = 0; i < nn; ++i) {
         const int c = chain[i], b = c / 32, l = c % 32, t = step[i];
         out.bidx[i] = static_cast<int>(slot(0, b, l, t));
-        int src[4] = {kLatZero, kLatZero, kLatZero, kLatZero};
-        int m = 0;
-        for (int k = lp[i]; k < lp[i + 1]; ++k, ++m) {
+        // window deps of lane 0, newest first -> P1, P2, ...
+        std::vector<std::pair<int, double>> wdeps;
+        for (int k = lp[i]; k < lp[i + 1]; ++k) {
             const int j = lc[k], cj = chain[j];
-            rec[slot(1 + m, b, l, t)] = lv[k];
-            if (cj / 32 == b)
-                src[m] = (cj % 32) * kLatR + (step[j] & (kLatR - 1));
-            else
-                src[m] = kLatWin + ((t / kLatKU) & 1) * kLatW +
-                         (step[j] - (win[static_cast<size_t>(b) * nblocks + t / kLatKU] >> 6));
+            if (cj / 32 != b) {
+                wdeps.push_back({step[j], lv[k]});
+                continue;
+            }
+            const int age = t - step[j];
+            int field;
+            if (cj == c) {  // own chain, age 1..3 -> h1..h3
+                if (age < 1 || age > 3) return false;
+                field = age;
+            } else if (cj % 32 == l - 1) {  // the chain below, age 1..4 -> p1..p4
+                if (age < 1 || age > 4) return false;
+                field = 3 + age;
+            } else {
+                return false;
+            }
+            rec[slot(field, b, l, t)] = lv[k];
         }
-        put_int2(slot(5, b, l, t), src[0], src[1]);
-        put_int2(slot(6, b, l, t), src[2], src[3]);
-        put_int2(slot(7, b, l, t), i, lp[i + 1] - lp[i] > 2 ? 1 : 0);
+        unsigned ws = 0;
+        if (!wdeps.empty()) {
+            if (wdeps.size() > 4) return false;
+            std::sort(wdeps.begin(), wdeps.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+            const int w0 = win[static_cast<size_t>(b) * nblocks + t / kLatKU] >> 6;
+            for (size_t k = 0; k < wdeps.size(); ++k) {
+                rec[slot(4 + static_cast<int>(k), b, l, t)] = wdeps[k].second;
+                ws |= static_cast<unsigned>(wdeps[k].first - w0) << (8 * k);
+            }
+        }
+        put_int2(slot(8, b, l, t), i, static_cast<int>(ws));
     }
     out.nb = nb;
     out.nblocks = nblocks;
@@ -329,8 +351,9 @@ static bool plan_lattice(const HostCsr& a, const std::vector<double>& dinv_h, La
     return true;
 }
 
-// CPU emulation of k_gs_lattice over a host plan (same records, ring, windows,
-// boundary buffer and arithmetic), bands in order: the check of the planner.
+// CPU emulation of k_gs_lattice over a host plan (same records, registers,
+// windows, boundary buffer and arithmetic), bands in order: the check of the
+// planner.
 static void emulate_lattice(const LatticeHost& h, const double* b_nat, double* z) {
     const int KU = kLatKU, T = h.nblocks * KU;
     const size_t blk = static_cast<size_t>(kLatF) * KU * 32;
@@ -338,36 +361,47 @@ static void emulate_lattice(const LatticeHost& h, const double* b_nat, double* z
     for (size_t i = 0; i < h.bidx.size(); ++i) rec[h.bidx[i]] = b_nat[i];
     std::vector<double> bnd(static_cast<size_t>(h.nb) * T, 0.0);
     for (int band = 0; band < h.nb; ++band) {
-        std::vector<double> vals(kLatVals, 0.0);
+        double H[32][3] = {}, Pp[32][4] = {};
+        double Wn[kLatW];
         for (int q = 0; q < h.nblocks; ++q) {
             const int w = h.win[static_cast<size_t>(band) * h.nblocks + q];
-            for (int l = 0; l < 32; ++l)
-                vals[kLatWin + (q & 1) * kLatW + l] =
-                    (band > 0 && w >= 0 && l < (w & 63)) ? bnd[static_cast<size_t>(band - 1) * T + (w >> 6) + l] : 0.0;
+            for (int l = 0; l < kLatW; ++l)
+                Wn[l] = (band > 0 && w >= 0 && l < (w & 63)) ? bnd[static_cast<size_t>(band - 1) * T + (w >> 6) + l]
+                                                             : 0.0;
             const double* B = rec.data() + (static_cast<size_t>(band) * h.nblocks + q) * blk;
             for (int u = 0; u < KU; ++u) {
                 const int step = q * KU + u;
+                double pn[32];
+                for (int l = 0; l < 32; ++l) pn[l] = l > 0 ? H[l - 1][0] : H[31][0];
                 double res[32];
-                int rows[32];
                 for (int l = 0; l < 32; ++l) {
                     auto f = [&](int fld) { return B[static_cast<size_t>(fld) * KU * 32 + (u / 2) * 64 + 2 * l + u % 2]; };
-                    auto fi = [&](int fld) {
-                        int v[2];
-                        const double d = f(fld);
-                        std::memcpy(v, &d, sizeof v);
-                        return std::pair<int, int>(v[0], v[1]);
-                    };
-                    const auto s01 = fi(5), s23 = fi(6), rw = fi(7);
-                    const double z0 = vals[s01.first], z1 = vals[s01.second], z2 = vals[s23.first],
-                                 z3 = vals[s23.second];
-                    const double acc = std::fma(f(2), z1, std::fma(f(1), z0, f(0)));
-                    const double wide = (acc + std::fma(f(4), z3, f(3) * z2)) + 0.0;
-                    res[l] = rw.second ? wide : acc;
-                    rows[l] = rw.first;
+                    int rw[2];
+                    const double d8 = f(8);
+                    std::memcpy(rw, &d8, sizeof rw);
+                    double* P = Pp[l];
+                    P[3] = P[2];
+                    P[2] = P[1];
+                    P[1] = P[0];
+                    P[0] = pn[l];
+                    double v[4] = {P[0], P[1], P[2], P[3]};
+                    if (band > 0 && l == 0) {
+                        const unsigned ws = static_cast<unsigned>(rw[1]);
+                        for (int k = 0; k < 4; ++k) v[k] = Wn[(ws >> (8 * k)) & 31];
+                    }
+                    double acc = std::fma(f(7), v[3], f(0));
+                    acc = std::fma(f(6), v[2], acc);
+                    acc = std::fma(f(5), v[1], acc);
+                    acc = std::fma(f(4), v[0], acc);
+                    acc = std::fma(f(3), H[l][2], acc);
+                    acc = std::fma(f(2), H[l][1], acc);
+                    res[l] = std::fma(f(1), H[l][0], acc);
+                    if (rw[0] >= 0) z[rw[0]] = res[l];
                 }
                 for (int l = 0; l < 32; ++l) {
-                    vals[l * kLatR + (step & (kLatR - 1))] = res[l];
-                    if (rows[l] >= 0) z[rows[l]] = res[l];
+                    H[l][2] = H[l][1];
+                    H[l][1] = H[l][0];
+                    H[l][0] = res[l];
                 }
                 bnd[static_cast<size_t>(band) * T + step] = res[31];
             }

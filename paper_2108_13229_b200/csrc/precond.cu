@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <string>
 
+#include "launch.cuh"
 #include "power.cuh"
 #include "solver.hpp"
 
@@ -122,6 +123,71 @@ void Matrix::ensure_schedule() {
 }
 
 void IdentityPrecond::do_apply(const double* r, double* z) { launch_copy(*ctx_, z, r, n_); }
+
+// ---------------------------------------------------------------------------
+// ILU(0)
+
+namespace {
+__global__ void k_reverse(int n, const double* __restrict__ x, double* __restrict__ y) {
+    pdl_begin();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = x[n - 1 - i];
+}
+void launch_reverse(Context& c, int n, const double* x, double* y) {
+    ProfScope ps_(c, PF_VEC, 16.0 * n);
+    if (n == 0) return;
+    launch_k(c, k_reverse, (n + 255) / 256, 256, 0, n, x, y);
+    c.count();
+}
+}  // namespace
+
+Ilu0Precond::Ilu0Precond(CtxPtr c, const HostCsr& a) : Precond(std::move(c)), n_(a.n_rows) {
+    auto t0 = std::chrono::steady_clock::now();
+    Context& cx = *ctx_;
+    HostCsr lo, up;
+    ilu0_factor(a, lo, up);
+    nnz_ = lo.nnz() + up.nnz();
+    const int n = n_;
+    // L + I (unit diagonal: the lower solve's 1/d is 1)
+    HostCsr ml(n, n);
+    for (int i = 0; i < n; ++i) {
+        for (int k = lo.rp[i]; k < lo.rp[i + 1]; ++k) {
+            ml.ci.push_back(lo.ci[k]);
+            ml.v.push_back(lo.v[k]);
+        }
+        ml.ci.push_back(i);
+        ml.v.push_back(1.0);
+        ml.rp[i + 1] = static_cast<int>(ml.ci.size());
+    }
+    // U reversed: row i' = n-1-i holds U's row i with columns n-1-j, sorted ascending
+    HostCsr mu(n, n);
+    for (int ip = 0; ip < n; ++ip) {
+        const int i = n - 1 - ip;
+        for (int k = up.rp[i + 1] - 1; k >= up.rp[i]; --k) {  // descending j = ascending n-1-j
+            mu.ci.push_back(n - 1 - up.ci[k]);
+            mu.v.push_back(up.v[k]);
+        }
+        mu.rp[ip + 1] = static_cast<int>(mu.ci.size());
+    }
+    lower_.build(ml, {}, cx.stream, 0, false);
+    upper_rev_.build(mu, {}, cx.stream, 0, false);
+    y_.resize(std::max(n, 1));
+    t_.resize(std::max(n, 1));
+    cx.sync();
+    setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// precond.cpp:73-87: y = L^{-1} r (unit lower), z = U^{-1} y, the backward
+// solve as a forward one on the reversed U
+void Ilu0Precond::do_apply(const double* r, double* z) {
+    Context& cx = *ctx_;
+    launch_gs_prep_pre(cx, lower_, r);
+    launch_gs_lower(cx, lower_, y_.get());
+    launch_reverse(cx, n_, y_.get(), t_.get());
+    launch_gs_prep_pre(cx, upper_rev_, t_.get());
+    launch_gs_lower(cx, upper_rev_, y_.get());
+    launch_reverse(cx, n_, y_.get(), z);
+}
 
 // ---------------------------------------------------------------------------
 // AMG

@@ -57,6 +57,56 @@ HostCsr ground_dof(const HostCsr& a, int dof) {
 }
 
 // ---------------------------------------------------------------------------
+// ILU(0) factorization (precond.cpp:13-87): in place on the pattern of a, row
+// by row, l_ik = a_ik / u_kk for k < i in column order, then row k's upper part
+// merged into the rest of row i (fill outside the pattern dropped); the same
+// operation sequence, so the factors are the reference's bit for bit.
+void ilu0_factor(const HostCsr& a, HostCsr& lower, HostCsr& upper) {
+    if (a.n_rows != a.n_cols) fail(SDG_EDIM, "ilu0: matrix must be square");
+    const int n = a.n_rows;
+    std::vector<double> f = a.v;
+    std::vector<int> diag(n, -1);
+    for (int i = 0; i < n; ++i)
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+            if (a.ci[k] == i) diag[i] = k;
+    for (int i = 0; i < n; ++i) {
+        const int row_end = a.rp[i + 1];
+        for (int kk = a.rp[i]; kk < row_end; ++kk) {
+            const int k = a.ci[kk];
+            if (k >= i) break;
+            if (diag[k] < 0 || f[diag[k]] == 0.0) fail(SDG_ESINGULAR, "ilu0: zero pivot in row " + std::to_string(k));
+            const double lik = f[kk] / f[diag[k]];
+            f[kk] = lik;
+            int p = diag[k] + 1, q = kk + 1;
+            const int k_end = a.rp[k + 1];
+            while (p < k_end && q < row_end) {
+                if (a.ci[p] == a.ci[q]) {
+                    f[q] -= lik * f[p];
+                    ++p;
+                    ++q;
+                } else if (a.ci[p] < a.ci[q]) {
+                    ++p;
+                } else {
+                    ++q;
+                }
+            }
+        }
+        if (diag[i] < 0 || f[diag[i]] == 0.0) fail(SDG_ESINGULAR, "ilu0: zero pivot in row " + std::to_string(i));
+    }
+    lower = HostCsr(n, n);
+    upper = HostCsr(n, n);
+    for (int i = 0; i < n; ++i) {
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k) {
+            HostCsr& t = a.ci[k] < i ? lower : upper;
+            t.ci.push_back(a.ci[k]);
+            t.v.push_back(f[k]);
+        }
+        lower.rp[i + 1] = static_cast<int>(lower.ci.size());
+        upper.rp[i + 1] = static_cast<int>(upper.ci.size());
+    }
+}
+
+// ---------------------------------------------------------------------------
 // aggregation
 
 namespace {

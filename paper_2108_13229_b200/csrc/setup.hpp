@@ -14,6 +14,8 @@ namespace sdg {
 HostCsr submatrix(const HostCsr& a, int row_begin, int row_end, int col_begin, int col_end);
 // precond.cpp:375-392
 HostCsr ground_dof(const HostCsr& a, int dof);
+// ILU(0) factors (precond.cpp:13-87, bitwise): strict lower L, upper U with the diagonal first in each row
+void ilu0_factor(const HostCsr& a, HostCsr& lower, HostCsr& upper);
 
 struct AmgOpts {
     int max_levels = 3;

@@ -15,6 +15,9 @@
 
 namespace sdg {
 
+// device right-hand side of the monolithic system (assemble.cu), bitwise setup.cpp's
+void launch_assemble_rhs(Context& c, const sdg_scenario& sc, const double* v_prev, double* rhs);
+
 struct BiWork;     // krylov.cu: cached BiCGSTAB workspace + captured iteration graph
 struct GmresWork;  // krylov.cu: cached GMRES basis / workspace + captured Arnoldi-step graphs
 
@@ -79,6 +82,29 @@ protected:
 
 private:
     int n_;
+};
+
+// ILU(0) (precond.hpp:18-30, precond.cpp:13-87): factors from the host
+// restatement (setup.cpp ilu0_factor, bitwise the reference's); each apply is
+// the unit-lower forward solve and the upper backward solve as two sweeps of
+// the Gauss-Seidel lower-solve machinery: L + I as it is, U with its rows and
+// columns reversed (its strict upper part becomes a lower triangle, 1/u_ii the
+// scaling), so the structured 5-point D' runs both on the multi-SM wavefront.
+class Ilu0Precond final : public Precond {
+public:
+    Ilu0Precond(CtxPtr c, const HostCsr& a);
+    int rows() const override { return n_; }
+    int64_t setup_memory_doubles() const override { return nnz_; }
+    int64_t work_per_apply() const override { return 2 * nnz_; }
+
+protected:
+    void do_apply(const double* r, double* z) override;
+
+private:
+    int n_ = 0;
+    int64_t nnz_ = 0;
+    GsPlan lower_, upper_rev_;
+    DevBuf<double> y_, t_;
 };
 
 // Aggregation AMG, V(1,1) (precond.hpp:101-120, precond.cpp:233-259).

@@ -132,6 +132,7 @@ def lib():
         p("sdg_uzawa_create", _i, [_vp, _vp, _vp, P(_UzawaOpts), P(_vp)])
         p("sdg_block_create", _i, [_i, _vp, _i, _i, _i, _vp, _vp, P(_vp)])
         p("sdg_identity_create", _i, [_vp, _i, P(_vp)])
+        p("sdg_ilu0_create", _i, [_vp, P(_vp)])
         p("sdg_ground_dof_host", _i, [_i, _ip, _ip, _dp, _i])
         p("sdg_gs_merged_sweep_host", _i, [_i, _ip, _ip, _dp, _i, _i, _dp, _vp, _dp, P(_i)])
         p("sdg_td_create", _i, [_vp, _i, _i, _i, _i, _i, _i, _i, _d, P(_vp)])
@@ -156,6 +157,7 @@ def lib():
         p("sdg_bicgstab_warm_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Report)])
         p("sdg_bicgstab_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Report)])
         p("sdg_power_iteration", _i, [_vp, _d, _i, C.c_uint, P(_d), P(_i), P(_i)])
+        p("sdg_assemble_rhs_device", _i, [_vp, P(_Scenario), _vp, _vp])
         p("sdg_assemble_monolithic", _i, [P(_Scenario), _vp, _vp, P(_i), P(_i64), P(_i), P(_i), P(_i),
                                           P(_i), _vp, _vp, _vp, _vp])
         p("sdg_assemble_stokes", _i, [P(_Scenario), _vp, _vp, P(_i), P(_i64), _vp, _vp, _vp, _vp])
@@ -507,6 +509,19 @@ class IdentityPreconditioner(Preconditioner):
         super().__init__(h, ctx)
 
 
+class Ilu0Preconditioner(Preconditioner):
+    """Ilu0Preconditioner (precond.hpp:18-30, precond.cpp:13-87): the
+    reference's ILU(0) factors; the two triangular solves on the device."""
+
+    def __init__(self, a: "SparseMatrix", ctx: Optional[Context] = None):
+        ctx = ctx or default_context()
+        if a.n_rows != a.n_cols:
+            raise ValueError("ilu0: matrix must be square")
+        h = _vp()
+        _check(lib().sdg_ilu0_create(a.device(ctx).h, C.byref(h)))
+        super().__init__(h, ctx, [a])
+
+
 @dataclass
 class AmgOptions:
     max_levels: int = 3
@@ -635,7 +650,7 @@ class TdPreconditioner(Preconditioner):
     def __init__(self, system: "CoupledSystem", kind: str = "td_bgs", v_max_levels: int = 3,
                  d_max_levels: int = 3, omega_override: float = float("nan"), ctx: Optional[Context] = None):
         ctx = ctx or default_context()
-        k = {"td_bj": 0, "td_bgs": 1}[kind]
+        k = {"td_bj": 0, "td_bgs": 1, "td_bj_ilu0": 0 | 16, "td_bgs_ilu0": 1 | 16}[kind]  # SDG_TD_ILU0
         h = _vp()
         s = system
         _check(lib().sdg_td_create(s.matrix.device(ctx).h, s.n_u, s.n_vel, s.n_pff, s.n_ppm, k, v_max_levels,
@@ -893,6 +908,17 @@ def assemble_monolithic(cfg: ScenarioConfig, t: Optional[float] = None, v_prev=N
                                      rhs.ctypes.data_as(_vp)))
     return CoupledSystem(SparseMatrix(N.value, N.value, rp, ci, vv), rhs, n, nu.value, nv.value, npf.value,
                          npm.value)
+
+
+def assemble_rhs_device(cfg: ScenarioConfig, rhs_ptr: int, v_prev_ptr: Optional[int] = None,
+                        t: Optional[float] = None, ctx: Optional[Context] = None) -> None:
+    """The right-hand side of assemble_monolithic on the device (stream-ordered on
+    the context's stream), from the previous velocity at device address
+    ``v_prev_ptr`` (None: zero); bitwise the host assembly's rhs."""
+    ctx = ctx or default_context()
+    sc = _scenario_c(cfg, t)
+    _check(lib().sdg_assemble_rhs_device(ctx.h, C.byref(sc), None if v_prev_ptr is None else C.c_void_p(v_prev_ptr),
+                                         C.c_void_p(rhs_ptr)))
 
 
 def _scenario_c(cfg: "ScenarioConfig", t: Optional[float]) -> _Scenario:

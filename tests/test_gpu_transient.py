@@ -93,3 +93,24 @@ def test_c4s_transient_within_reference_spread():
         smp = np.asarray(ref_step["sample"])
         assert np.linalg.norm(x[:: ref_step["sample_stride"]] - smp) <= 1e-6 * np.linalg.norm(smp), k
     assert within_spread(sum(its), min(ens["totals"]), max(ens["totals"])), (its, ens["totals"])
+
+
+@pytest.mark.parametrize("n", [16, 50])
+def test_device_rhs_assembly_bitwise(n):
+    """sdg_assemble_rhs_device (assemble.cu) equals the host assembly's rhs
+    (setup.cpp, itself bitwise the reference's assemble_monolithic) bit for
+    bit, stationary and transient, with and without a previous velocity."""
+    import torch
+    for dt, t in ((float("inf"), 1.0), (0.1, 0.1), (0.1, 0.7)):
+        cfg = sdc.ScenarioConfig(cells_per_unit_square=n, permeability=1e-2, alpha_bj=1.0, kinematic_viscosity=1.0,
+                                 density=1.0, dt=dt, t_end=1.0, dp_max=1.0)
+        n_vel = 2 * n * (n + 1)
+        for v_prev in (None, np.random.default_rng(n).standard_normal(n_vel)):
+            host = sdc.assemble_monolithic(cfg, t=t, v_prev=v_prev).rhs
+            ctx = sdc.default_context()
+            out = torch.full((host.size,), float("nan"), dtype=torch.float64, device="cuda")
+            vp = None if v_prev is None else torch.from_numpy(v_prev).cuda()
+            sdc.assemble_rhs_device(cfg, out.data_ptr(), None if vp is None else vp.data_ptr(), t=t, ctx=ctx)
+            ctx.synchronize()
+            dev = out.cpu().numpy()
+            assert np.array_equal(dev.view(np.uint64), host.view(np.uint64)), (n, dt, t, v_prev is None)

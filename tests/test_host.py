@@ -199,3 +199,41 @@ def test_gs_level_merging_equals_reference_sweep(ref, block, k, cap):
     assert groups < g1 if (cap == 0 or block == "D") else groups <= g1
     if cap == 0:
         assert groups == -(-g1 // k)
+
+
+@pytest.mark.parametrize("cfg_name", ["c1", "c2"])
+def test_lattice_planner_host_check(cfg_name):
+    """The lattice planner (gs_lattice.cu) emulated on the host equals the
+    sequential lower solve z_i = b_i - sum_{j<i} a_ij z_j / a_ii to rounding on
+    every block / level of the config that is a lattice (no GPU)."""
+    import ctypes as C
+    import scipy.sparse as sp
+    from paper_2108_13229_b200 import scenarios, sdc
+    cfg = scenarios.CONFIGS[cfg_name]
+    s = scenarios.build_system(cfg)
+    L = sdc.lib()
+    L.sdg_lattice_check_host.restype = C.c_double
+
+    def sub(A, lo, hi):
+        m = sp.csr_matrix((A.values, A.col_indices, A.row_offsets), shape=(A.n_rows, A.n_rows))[lo:hi, lo:hi].tocsr()
+        m.sort_indices()
+        return sdc.SparseMatrix(hi - lo, hi - lo, m.indptr.astype(np.int32), m.indices.astype(np.int32), m.data)
+
+    V = sdc.submatrix(s.matrix, 0, s.n_vel, 0, s.n_vel)
+    hv = sdc.host_hierarchy(V, sdc.AmgOptions(components=[0] * s.n_u + [1] * (s.n_vel - s.n_u),
+                                              max_levels=cfg.v_max_levels))
+    nu1 = int(hv[0].aggregate_of[: s.n_u].max()) + 1
+    D = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
+    checked = 0
+    for A in (sub(V, 0, s.n_u), sub(hv[1].a, nu1, hv[1].a.n_rows), D):
+        b = np.random.default_rng(0).standard_normal(A.n_rows)
+        P = C.c_void_p
+        rp, ci, v = (np.ascontiguousarray(A.row_offsets, np.int32), np.ascontiguousarray(A.col_indices, np.int32),
+                     np.ascontiguousarray(A.values))
+        e = L.sdg_lattice_check_host(A.n_rows, rp.ctypes.data_as(P), ci.ctypes.data_as(P), v.ctypes.data_as(P),
+                                     b.ctypes.data_as(P))
+        if e < 0:
+            continue
+        checked += 1
+        assert e <= 1e-13
+    assert checked >= 2
