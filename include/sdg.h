@@ -403,6 +403,14 @@ int sdg_dist_pd_gmres_device(sdg_dist_system* s, sdg_dist_precond* p, const doub
                              double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep);
 int sdg_dist_bicgstab_device(sdg_dist_system* s, sdg_dist_precond* p, const double* b_dev, double* x_dev,
                              double tol_abs, int max_iters, sdg_report* rep);
+/* Warm-started strip solves (BASELINE config 4 over strips; MonolithicDriver::
+ * advance, bench.cpp:183-238): x_dev holds this rank's rows of the previous
+ * solution; the reference solve of the correction (x0 = 0 is hard-coded,
+ * krylov.cpp:58/194) on r0 = b - A x, then x += d.  Collective. */
+int sdg_dist_pd_gmres_warm_device(sdg_dist_system* s, sdg_dist_precond* p, const double* b_dev, double* x_dev,
+                                  double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep);
+int sdg_dist_bicgstab_warm_device(sdg_dist_system* s, sdg_dist_precond* p, const double* b_dev, double* x_dev,
+                                  double tol_abs, int max_iters, sdg_report* rep);
 
 #ifdef __cplusplus
 }

@@ -237,3 +237,49 @@ int sdg_dist_bicgstab_device(sdg_dist_system* s, sdg_dist_precond* p, const doub
 }
 
 }  // extern "C"
+
+namespace {
+// r0 = b - A x over strips, solve A d = r0 from zero, x += d
+template <class Solve>
+sdg::SolveOut dist_warm(sdg::DistSystem& S, const double* b_dev, double* x_dev, Solve&& solve) {
+    sdg::Context& c = *S.ctx;
+    const int n = S.n_local();
+    sdg::DevBuf<double> r0(std::max(n, 1)), d(std::max(n, 1));
+    S.A.apply_add(c, *S.tr, x_dev, b_dev, r0.get(), -1.0);
+    sdg::SolveOut o = solve(r0.get(), d.get());
+    sdg::launch_add_inplace(c, n, x_dev, d.get());
+    c.sync();
+    return o;
+}
+}  // namespace
+
+extern "C" {
+
+int sdg_dist_pd_gmres_warm_device(sdg_dist_system* s, sdg_dist_precond* p, const double* b_dev, double* x_dev,
+                                  double tol_abs, int max_restarts, const sdg_restart* ctrl, sdg_report* rep) {
+    return guard([&] {
+        need(s, "sdg_dist_pd_gmres_warm_device");
+        auto t0 = std::chrono::steady_clock::now();
+        const int64_t apps0 = p ? p->p->applications() : 0;
+        sdg::SolveOut o = dist_warm(*s->p, b_dev, x_dev, [&](const double* r0, double* d) {
+            return sdg::dist_pd_gmres(*s->p, p ? p->p.get() : nullptr, r0, d, tol_abs, max_restarts,
+                                      restart_from(ctrl));
+        });
+        fill_report(o, seconds_since(t0), (p ? p->p->applications() : 0) - apps0, rep);
+    });
+}
+
+int sdg_dist_bicgstab_warm_device(sdg_dist_system* s, sdg_dist_precond* p, const double* b_dev, double* x_dev,
+                                  double tol_abs, int max_iters, sdg_report* rep) {
+    return guard([&] {
+        need(s, "sdg_dist_bicgstab_warm_device");
+        auto t0 = std::chrono::steady_clock::now();
+        const int64_t apps0 = p ? p->p->applications() : 0;
+        sdg::SolveOut o = dist_warm(*s->p, b_dev, x_dev, [&](const double* r0, double* d) {
+            return sdg::dist_bicgstab(*s->p, p ? p->p.get() : nullptr, r0, d, tol_abs, max_iters);
+        });
+        fill_report(o, seconds_since(t0), (p ? p->p->applications() : 0) - apps0, rep);
+    });
+}
+
+}  // extern "C"

@@ -64,6 +64,8 @@ def _lib():
     p("sdg_dist_bicgstab", _i, [_vp, _vp, _dp, _dp, _d, _i, P(_Report)])
     p("sdg_dist_pd_gmres_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Restart), P(_Report)])
     p("sdg_dist_bicgstab_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Report)])
+    p("sdg_dist_pd_gmres_warm_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Restart), P(_Report)])
+    p("sdg_dist_bicgstab_warm_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Report)])
     _bound = True
     return L
 
@@ -283,19 +285,22 @@ def dist_bicgstab(ds: DistSystem, precond: Optional[DistTdPreconditioner], b_loc
 
 def dist_solve_device(ds: DistSystem, precond: Optional[DistTdPreconditioner], solver: str, b_ptr: int,
                       x_ptr: int, tol_abs: float, max_iters: int,
-                      ctrl: Optional[RestartController] = None) -> SolveReport:
-    """Device-pointer solve over strips (b, x: this rank's rows on its GPU)."""
+                      ctrl: Optional[RestartController] = None, warm: bool = False) -> SolveReport:
+    """Device-pointer solve over strips (b, x: this rank's rows on its GPU).
+    warm: x holds the previous solution; the reference solve of the correction
+    (BASELINE config 4 over strips)."""
     rep = _Report()
     hist = np.empty(1 << 14)
     rep.residual_history = hist.ctypes.data_as(C.POINTER(_d))
     rep.history_capacity = hist.size
     ph = precond.h if precond else None
     if solver == "bicgstab":
-        _check(_lib().sdg_dist_bicgstab_device(ds.h, ph, b_ptr, x_ptr, tol_abs, max_iters, C.byref(rep)))
+        f = _lib().sdg_dist_bicgstab_warm_device if warm else _lib().sdg_dist_bicgstab_device
+        _check(f(ds.h, ph, b_ptr, x_ptr, tol_abs, max_iters, C.byref(rep)))
     else:
         rc = (ctrl or RestartController.defaults())._c()
-        _check(_lib().sdg_dist_pd_gmres_device(ds.h, ph, b_ptr, x_ptr, tol_abs, max_iters, C.byref(rc),
-                                               C.byref(rep)))
+        f = _lib().sdg_dist_pd_gmres_warm_device if warm else _lib().sdg_dist_pd_gmres_device
+        _check(f(ds.h, ph, b_ptr, x_ptr, tol_abs, max_iters, C.byref(rc), C.byref(rep)))
     return _report(rep, hist)
 
 

@@ -201,3 +201,56 @@ def test_c2u_strips_gmres50_within_five_percent(ref, world):
         assert o["conv"] and o["spmv"] and o["it"] == outs[0]["it"]
         assert abs(o["it"] - rr.iterations) <= 0.05 * rr.iterations, (o["it"], rr.iterations)
     assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-6
+
+
+def _warm_worker(rank, world, port, out):
+    _init(rank, world, port)
+    try:
+        import torch
+        from paper_2108_13229_b200 import dist as sd
+        from paper_2108_13229_b200 import scenarios, sdc
+        cfg = scenarios.Config("c4-strip", 16, 1.0, False, "gmres50", 3, 3, dt=0.1, steps=2)
+        s1 = scenarios.build_system(cfg, t=0.1)
+        ctx = sdc.Context(0)
+        ds = sd.DistSystem(s1, sd.CallbackTransport(), ctx=ctx)
+        p = sd.DistTdPreconditioner(ds, "td_bgs")
+        ctrl = sdc.RestartController.fixed(50)
+        x = torch.zeros(ds.n_local(), dtype=torch.float64, device="cuda")
+        b = torch.from_numpy(ds.local(s1.rhs)).cuda()
+        tol1 = 1e-8 * float(np.linalg.norm(s1.rhs))
+        r1 = sd.dist_solve_device(ds, p, "gmres50", b.data_ptr(), x.data_ptr(), tol1, 400, ctrl)
+        x1 = np.zeros(s1.n_total())
+        x1[ds.rows] = x.cpu().numpy()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, {"rows": ds.rows.tolist(), "x": x.cpu().numpy().tolist()})
+        for g in gathered:
+            x1[np.asarray(g["rows"])] = np.asarray(g["x"])
+        s2 = scenarios.build_system(cfg, t=0.2, v_prev=x1[: s1.n_vel])
+        b2 = torch.from_numpy(ds.local(s2.rhs)).cuda()
+        tol2 = 1e-8 * float(np.linalg.norm(s2.rhs))
+        r2 = sd.dist_solve_device(ds, p, "gmres50", b2.data_ptr(), x.data_ptr(), tol2, 400, ctrl, warm=True)
+        out[rank] = dict(rows=ds.rows.copy(), x=x.cpu().numpy(), it=(r1.iterations, r2.iterations),
+                         conv=r1.converged and r2.converged)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_strips_warm_started_step_matches_single_gpu():
+    """BASELINE config 4 over strips: the second implicit-Euler step solved
+    warm-started over 2 strips (sdg_dist_pd_gmres_warm_device: the reference
+    solve of the correction on r0 = b - A x_prev) equals the single-GPU
+    warm-started step to 1e-6 and fewer iterations than the cold first step."""
+    from paper_2108_13229_b200 import drivers, scenarios
+    world = 2
+    out = mp.Manager().dict()
+    mp.spawn(_warm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    cfg = scenarios.Config("c4-strip", 16, 1.0, False, "gmres50", 3, 3, dt=0.1, steps=2)
+    drv = drivers.TransientDriver(cfg, warm_start=True)
+    drv.advance(0.1)
+    drv.advance(0.2)
+    x = np.zeros_like(drv.x)
+    for r in range(world):
+        x[out[r]["rows"]] = out[r]["x"]
+        assert out[r]["conv"] and out[r]["it"][1] < out[r]["it"][0]
+    assert np.linalg.norm(x - drv.x) / np.linalg.norm(drv.x) <= 1e-6
