@@ -157,6 +157,21 @@ def workload_desc(cfg, n_dof):
             f"td_bgs(Uzawa(AMG_V), AMG_D'), AMG levels V{cfg.v_max_levels}/D{cfg.d_max_levels}, tol 1e-8*||b||")
 
 
+def config_for(cfg, n_dof, nnz, args):
+    """The `config` object of the JSON line: static facts of the workload and
+    of the command line only, so both arms (ours and --impl reference) print
+    the same object."""
+    if args.gpus <= 1 and not args.sharded:
+        par = "single GPU"
+    elif args.replicas:
+        par = f"replicas x{args.gpus}"
+    else:
+        par = f"horizontal strips x{args.gpus} (processor-block GS inside strips, NCCL halos)"
+    return {"workload": workload_desc(cfg, n_dof), "dof": int(n_dof), "nnz": int(nnz), "parallelism": par,
+            "l2": "GPU arm: flushed between timed solves (256 MiB write, outside the event pair); the working set "
+                  "(operator, hierarchy, coarse inverse, interface response) also exceeds the 126 MB L2"}
+
+
 def solve_device(sdc, cfg, s, p, b_ptr, x_ptr, tol, ctx):
     if cfg.solver == "bicgstab":
         return sdc.bicgstab_device(s.matrix, p, b_ptr, x_ptr, tol, 20000, ctx=ctx)
@@ -317,8 +332,8 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": workload_desc(cfg, rs.n), "dof": rs.n, "nnz": int(len(rs.a.val)),
-                       "iterations_per_step": its, "setup_s": st.setup_s, "system": st.assembly},
+            "config": config_for(cfg, rs.n, len(rs.a.val), args),
+            "details": {"iterations_per_step": its, "setup_s": st.setup_s, "system": st.assembly},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": f"each step = {threads} concurrent samples ({SAMPLE_DESC[cfg.solver]} of "
                                        f"{cfg.name}) by the compiled reference, one per core, sharing one setup",
@@ -393,6 +408,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     launches0 = ctx.launches
     evs, iters = [], []
+    if os.environ.get("SDG_PROFILER_RANGE"):  # ncu --profile-from-start off: the timed solves only
+        torch.cuda.profiler.start()
     for _ in range(args.steps):
         with torch.cuda.stream(stream):
             flush.zero_()  # L2 flush outside the timed pair
@@ -404,6 +421,8 @@ def run_ours(args):
         evs.append((e0, e1))
         iters.append(rep.iterations)
     torch.cuda.synchronize()
+    if os.environ.get("SDG_PROFILER_RANGE"):
+        torch.cuda.profiler.stop()
     if dist:
         dist.barrier()
     launches = ctx.launches - launches0
@@ -461,10 +480,8 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg, n), "dof": n, "nnz": s.matrix.nnz(),
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "flushed between timed solves (256 MiB write, outside the event pair)",
-                   "iterations": iters, "setup_s": setup_s, "assembly_s": assembly_s,
+        "config": config_for(cfg, n, s.matrix.nnz(), args),
+        "details": {"iterations": iters, "setup_s": setup_s, "assembly_s": assembly_s,
                    "hierarchy_v": hier_v, "hierarchy_d": hier_d, "omega": p.omega(),
                    "fast_paths": sorted(p.features()),
                    "true_residual_rel": true_res / float(np.linalg.norm(s.rhs))},
@@ -751,10 +768,8 @@ def run_sharded(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg, s.n_total()), "dof": n, "nnz": s.matrix.nnz(),
-                   "parallelism": f"horizontal strips x{world} (processor-block GS inside strips, NCCL halos)",
-                   "l2": "flushed between timed solves (256 MiB write, outside the event pair)",
-                   "iterations": iters, "setup_s": setup_s, "omega": p.omega(), "local_rows": ds.n_local()},
+        "config": config_for(cfg, n, s.matrix.nnz(), args),
+        "details": {"iterations": iters, "setup_s": setup_s, "omega": p.omega(), "local_rows": ds.n_local()},
         "gpu_launches": launches, "clocks": clk, "e2e": e2e,
     }
     if rank == 0:

@@ -328,6 +328,32 @@ int sdg_host_hierarchy_level(const sdg_host_hierarchy* h, int lev, int* n, int64
                              double* val, int* agg);
 void sdg_host_hierarchy_destroy(sdg_host_hierarchy* h);
 
+/* ---- direct solve (lu.hpp:38-41: lu_factor / lu_solve) ----------------------
+ * The factorization the AMG hierarchies use on their coarsest level, as its own
+ * handle: a nested-dissection block elimination with explicit inverses of small
+ * dense blocks (batched Gauss-Jordan with partial pivoting on the device;
+ * csrc/coarse.hpp), or one dense inverse for small systems.  A singular matrix
+ * returns SDG_ESINGULAR like lu_factor's std::runtime_error (lu.cpp:142).
+ * sdg_lu_info: dense = 1 when a single dense inverse is kept, depth = levels of
+ * the dissection, stored_doubles = dense block storage. */
+typedef struct sdg_lu sdg_lu;
+int sdg_lu_factor(sdg_context* ctx, int n, const int* rowptr, const int* col, const double* val, sdg_lu** out);
+int sdg_lu_solve(sdg_lu* lu, const double* b_host, double* x_host);
+int sdg_lu_info(const sdg_lu* lu, int* dense, int* depth, int64_t* stored_doubles);
+void sdg_lu_destroy(sdg_lu* lu);
+
+/* Host check of the coarse direct solve (no GPU): the nested-dissection block
+ * elimination that replaces lu_factor / lu_solve on the coarsest AMG level
+ * (lu.cpp:91-203; csrc/coarse.hpp).  Orders the matrix (nodes split while they
+ * have more than leaf_rows rows, at most max_depth times), solves A x = b
+ * through the ordering and reports the tree: perm (new -> old, n ints, may be
+ * NULL), node count, depth, the widest separator and the doubles a device
+ * build stores.  nodes_out (may be NULL, up to max_nodes x 4 ints): lo, mid,
+ * hi, depth per node in post-order.  SDG_ESINGULAR when a block is singular. */
+int sdg_nd_solve_host(int n, const int* rowptr, const int* col, const double* val, int leaf_rows, int max_depth,
+                      const double* b, double* x, int* perm, int* n_nodes, int* depth, int* max_separator,
+                      int64_t* stored_doubles, int* nodes_out, int max_nodes);
+
 /* ---- strip-sharded multi-GPU solve ----------------------
  * One process (and one sdg_context) per GPU.  Every rank passes the same
  * assembled system and the same ownership map (owner rank per global dof;

@@ -22,7 +22,7 @@ LIB = os.path.join(PKG, "libsdgpu.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
                      "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
-LIBS = ["-L/usr/local/cuda/lib64", "-lcusolver", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+LIBS = []  # no CUDA math libraries: every kernel on the path is in csrc/
 
 
 def nvcc() -> str:

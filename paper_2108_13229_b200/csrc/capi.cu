@@ -3,9 +3,11 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <new>
 #include <string>
 
+#include "coarse.hpp"
 #include "power.cuh"
 #include "sdg.h"
 #include "setup.hpp"
@@ -679,5 +681,79 @@ int sdg_host_hierarchy_level(const sdg_host_hierarchy* h, int lev, int* n, int64
 }
 
 void sdg_host_hierarchy_destroy(sdg_host_hierarchy* h) { delete h; }
+
+int sdg_lu_factor(sdg_context* ctx, int n, const int* rowptr, const int* col, const double* val, sdg_lu** out) {
+    return guard([&] {
+        need(ctx, "sdg_lu_factor");
+        need(out, "sdg_lu_factor");
+        sdg::HostCsr h = make_csr(n, n, rowptr, col, val);
+        h.check();
+        auto lu = std::make_unique<sdg_lu>();
+        lu->ctx = ctx->p;
+        SDG_CUDA(cudaSetDevice(ctx->p->device));
+        lu->solver.build(*ctx->p, h);
+        lu->b.resize(std::max(n, 1));
+        lu->x.resize(std::max(n, 1));
+        *out = lu.release();
+    });
+}
+
+int sdg_lu_solve(sdg_lu* lu, const double* b_host, double* x_host) {
+    return guard([&] {
+        need(lu, "sdg_lu_solve");
+        const int n = lu->solver.n();
+        if (n == 0) return;
+        need(b_host, "sdg_lu_solve");
+        need(x_host, "sdg_lu_solve");
+        sdg::Context& cx = *lu->ctx;
+        SDG_CUDA(cudaSetDevice(cx.device));
+        SDG_CUDA(cudaMemcpyAsync(lu->b.get(), b_host, sizeof(double) * n, cudaMemcpyHostToDevice, cx.stream));
+        lu->solver.solve(cx, lu->b.get(), lu->x.get());
+        SDG_CUDA(cudaMemcpyAsync(x_host, lu->x.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, cx.stream));
+        cx.sync();
+    });
+}
+
+int sdg_lu_info(const sdg_lu* lu, int* dense, int* depth, int64_t* stored_doubles) {
+    return guard([&] {
+        need(lu, "sdg_lu_info");
+        if (dense) *dense = lu->solver.dense() ? 1 : 0;
+        if (depth) *depth = lu->solver.depth();
+        if (stored_doubles) *stored_doubles = lu->solver.doubles();
+    });
+}
+
+void sdg_lu_destroy(sdg_lu* lu) { delete lu; }
+
+int sdg_nd_solve_host(int n, const int* rowptr, const int* col, const double* val, int leaf_rows, int max_depth,
+                      const double* b, double* x, int* perm, int* n_nodes, int* depth, int* max_separator,
+                      int64_t* stored_doubles, int* nodes_out, int max_nodes) {
+    return guard([&] {
+        sdg::HostCsr h = make_csr(n, n, rowptr, col, val);
+        h.check();
+        const sdg::NdTree t = sdg::nd_order(h, leaf_rows, max_depth);
+        if (perm) std::memcpy(perm, t.perm.data(), sizeof(int) * t.perm.size());
+        int ms = 0;
+        int64_t doubles = 0;
+        for (size_t i = 0; i < t.nodes.size(); ++i) {
+            const sdg::NdNode& nd = t.nodes[i];
+            const int64_t ni = nd.mid - nd.lo, ns = nd.hi - nd.mid;
+            ms = std::max<int>(ms, static_cast<int>(ns));
+            doubles += nd.leaf() ? (nd.hi - nd.lo) * static_cast<int64_t>(nd.hi - nd.lo) : ns * ns + ni * ns;
+            if (nodes_out && static_cast<int>(i) < max_nodes) {
+                nodes_out[4 * i + 0] = nd.lo;
+                nodes_out[4 * i + 1] = nd.mid;
+                nodes_out[4 * i + 2] = nd.hi;
+                nodes_out[4 * i + 3] = nd.depth;
+            }
+        }
+        if (n_nodes) *n_nodes = static_cast<int>(t.nodes.size());
+        if (depth) *depth = t.max_depth;
+        if (max_separator) *max_separator = ms;
+        if (stored_doubles) *stored_doubles = doubles;
+        if (b && x && !sdg::nd_solve_host(h, t, b, x))
+            sdg::fail(SDG_ESINGULAR, "coarse solve: a nested-dissection block is singular");
+    });
+}
 
 }  // extern "C"

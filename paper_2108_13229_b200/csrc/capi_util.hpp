@@ -21,6 +21,11 @@ struct sdg_matrix {
 struct sdg_precond {
     sdg::PrecondPtr p;
 };
+struct sdg_lu {
+    sdg::CtxPtr ctx;
+    sdg::CoarseSolver solver;
+    sdg::DevBuf<double> b, x;
+};
 struct sdg_host_hierarchy {
     std::vector<sdg::HostLevel> levels;
 };

@@ -124,7 +124,6 @@ struct Context {
     cudaStream_t stream = nullptr;
     std::atomic<int64_t> launches{0};
     std::unique_ptr<PinnedBuf> pinned;   // status words, small host reads
-    void* cusolver = nullptr;            // lazily created cusolverDnHandle_t
     bool pdl = true;                     // programmatic dependent launch (launch.cuh; SDG_PDL=0 off)
 
     // live profiler: CUDA events bracketing every launch of a family

@@ -564,10 +564,10 @@ DistAmg::DistAmg(CtxPtr c, TransportPtr t, const HostCsr& a, const Ownership& ow
         V.reff.resize(std::max(n, 1));
     }
 
-    // coarsest level: replicated explicit inverse, allgathered right-hand side
+    // coarsest level: replicated direct solve (coarse.hpp), allgathered right-hand side
     const HostCsr& Ac = hl.back().a;
     n_c_ = Ac.n_rows;
-    dense_inverse(cx, Ac, inv_);
+    coarse_.build(cx, Ac);
     const Ownership& Oc = O.back();
     c_owned_ = static_cast<int>(Oc.owned[rank].size());
     c_max_ = 1;
@@ -590,7 +590,7 @@ void DistAmg::coarse_solve(const double* r_owned) {
     launch_copy(cx, c_send_.get(), r_owned, c_owned_);
     tr_->allgather(cx, c_send_.get(), c_max_, c_gather_.get());
     launch_scatter(cx, tr_->size * c_max_, c_slot_gid_.get(), c_gather_.get(), c_full_.get());
-    launch_dense_gemv(cx, n_c_, inv_.get(), c_full_.get(), c_sol_.get());
+    coarse_.solve(cx, c_full_.get(), c_sol_.get());
 }
 
 void DistAmg::vcycle(int l, const double* r, double* z) {

@@ -151,7 +151,8 @@ private:
     std::vector<Level> lv_;
     // coarsest level, solved redundantly on every rank
     int n_c_ = 0, c_max_ = 0, c_owned_ = 0;
-    DevBuf<double> inv_, c_send_, c_gather_, c_full_, c_sol_;
+    CoarseSolver coarse_;
+    DevBuf<double> c_send_, c_gather_, c_full_, c_sol_;
     DevBuf<int> c_slot_gid_;              // gathered slot -> global coarse id (-1 = padding)
     DevBuf<int> c_own_gid_;               // owned coarse rows (global ids), when the hierarchy has one level
 };

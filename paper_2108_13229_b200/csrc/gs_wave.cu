@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
     if constexpr (KIND == 1) {
         const int nx = a.nx;
         // block q, step s = q KU + u: lane 0 reads z(s, j - 1) = sb[u]
-        double sb[KU], nsb[KU], nsb2[KU];  // this block's, the next's (settled), the one after (in flight)
+        double sb[KU], nsb[KU];
         auto load_bnd = [&](int q, double (&o)[KU]) {
             const bool on = has_src && lane == 0 && q < a.nblocks;
 #pragma unroll
@@ -203,14 +203,13 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
         };
         load_bnd(0, sb);
         settle(0, sb);
-        load_bnd(1, nsb);  // two blocks of look-ahead hide the L2 round trip behind a block
         if (a.tl) t_first = gtimer();
         double last = 0.0;
         double* zrow = a.z + static_cast<size_t>(j) * nx;
         const bool row_ok = j < a.ny;
         const bool pub = has_dst && lane == 31;
         for (int q = 0; q < a.nblocks; ++q) {
-            load_bnd(q + 2, nsb2);  // in flight during this block and the next
+            load_bnd(q + 1, nsb);  // in flight during this block
             const int slot = q % kWaveDepth;
             ptx::mbar_wait(bars + slot, (q / kWaveDepth) & 1);
             const double2* B = reinterpret_cast<const double2*>(ring + slot * BLK) + lane;
@@ -244,10 +243,7 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
                          lane == 0 && q + kWaveDepth < a.nblocks);
             settle(q + 1, nsb);
 #pragma unroll
-            for (int u = 0; u < KU; ++u) {
-                sb[u] = nsb[u];
-                nsb[u] = nsb2[u];
-            }
+            for (int u = 0; u < KU; ++u) sb[u] = nsb[u];
         }
     } else {
         const int m = a.nx;
@@ -255,7 +251,7 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
         const double* sv_in = sb_in + a.bcols;    // v(., j-1), m slots
         double* su_out = sb_out;
         double* sv_out = sb_out + a.bcols;
-        double bu[KU + 1], bv[KU], nbu[KU + 1], nbv[KU], nbu2[KU + 1], nbv2[KU];
+        double bu[KU + 1], bv[KU], nbu[KU + 1], nbv[KU];
         // block q, step s = q KU + u (lane 0: u column s, v column s - 1) reads
         // u(s, j-1) = bu[u + 1], u(s - 1, j-1) = bu[u], v(s - 1, j-1) = bv[u]
         auto load_bnd = [&](int q, double (&ou)[KU + 1], double (&ov)[KU]) {
@@ -284,7 +280,6 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
         };
         load_bnd(0, bu, bv);
         settle(0, bu, bv);
-        load_bnd(1, nbu, nbv);  // two blocks of look-ahead hide the L2 round trip behind a block
         if (a.tl) t_first = gtimer();
         double u_last = 0.0, u_last2 = 0.0, v_last = 0.0;
         double* zu = a.z + static_cast<size_t>(j) * (m + 1);
@@ -292,7 +287,7 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
         const bool u_row = j < m, v_row = j <= m;
         const bool pub = has_dst && lane == 31;
         for (int q = 0; q < a.nblocks; ++q) {
-            load_bnd(q + 2, nbu2, nbv2);  // in flight during this block and the next
+            load_bnd(q + 1, nbu, nbv);  // in flight during this block
             const int slot = q % kWaveDepth;
             const long long c0 = a.tl ? clock64() : 0;
             ptx::mbar_wait(bars + slot, (q / kWaveDepth) & 1);
@@ -354,15 +349,9 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
                          lane == 0 && q + kWaveDepth < a.nblocks);
             settle(q + 1, nbu, nbv);
 #pragma unroll
-            for (int k = 0; k <= KU; ++k) {
-                bu[k] = nbu[k];
-                nbu[k] = nbu2[k];
-            }
+            for (int k = 0; k <= KU; ++k) bu[k] = nbu[k];
 #pragma unroll
-            for (int k = 0; k < KU; ++k) {
-                bv[k] = nbv[k];
-                nbv[k] = nbv2[k];
-            }
+            for (int k = 0; k < KU; ++k) bv[k] = nbv[k];
         }
     }
     if (a.tl && lane == 0) {

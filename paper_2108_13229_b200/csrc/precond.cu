@@ -1,11 +1,10 @@
 // Device preconditioners: AMG V(1,1), inexact Uzawa, td_*/pv_* block
 // combinators.  Setup (aggregation, Galerkin, schedules) is host C++
-// (setup.cpp); the coarse factorization is a dense LU on the device
-// followed by an explicit inverse, so each coarse solve is one fully
-// parallel GEMV instead of two sequential triangular solves (SURVEY.md §7
-// hard part 2: at the reference's 3 levels the coarse factor is ~58% dense).
-#include <cusolverDn.h>
-
+// (setup.cpp); the coarse factorization is the nested-dissection block
+// elimination of coarse.hpp (explicit inverses of small dense blocks computed
+// on the device), so each coarse solve is a few fully parallel batched
+// products instead of two sequential triangular solves (SURVEY.md §7 hard
+// part 2: at the reference's 3 levels the coarse factor is ~58% dense).
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -40,7 +39,6 @@ Context::~Context() {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
-    if (cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(cusolver));
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -232,59 +230,19 @@ AmgPrecond::AmgPrecond(CtxPtr c, const HostCsr& a, const AmgOpts& o) : Precond(s
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
-void dense_inverse(Context& cx, const HostCsr& coarse, DevBuf<double>& coarse_inv_) {
-    const int n_c_ = coarse.n_rows;
-    if (n_c_ == 0) return;
-    const size_t nn = static_cast<size_t>(n_c_) * n_c_;
-    DevCsr dc;
-    dc.upload(coarse, cx.stream);
-    // Row-major A is column-major A^T: factor A^T and solve A^T X = I, so X
-    // (column-major) = A^{-T}, i.e. row-major A^{-1}.
-    DevBuf<double> lu(nn);
-    coarse_inv_.resize(nn);
-    SDG_CUDA(cudaMemsetAsync(lu.get(), 0, nn * sizeof(double), cx.stream));
-    SDG_CUDA(cudaMemsetAsync(coarse_inv_.get(), 0, nn * sizeof(double), cx.stream));
-    launch_csr_to_dense(cx, dc, lu.get());
-    launch_set_identity(cx, n_c_, coarse_inv_.get());
-    if (!cx.cusolver) {
-        cusolverDnHandle_t h;
-        if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(SDG_ECUDA, "cusolverDnCreate failed");
-        cx.cusolver = h;
-    }
-    auto h = static_cast<cusolverDnHandle_t>(cx.cusolver);
-    cusolverDnSetStream(h, cx.stream);
-    int lwork = 0;
-    if (cusolverDnDgetrf_bufferSize(h, n_c_, n_c_, lu.get(), n_c_, &lwork) != CUSOLVER_STATUS_SUCCESS)
-        fail(SDG_ECUDA, "cusolverDnDgetrf_bufferSize failed");
-    DevBuf<double> work(std::max(lwork, 1));
-    DevBuf<int> ipiv(n_c_), info(1);
-    if (cusolverDnDgetrf(h, n_c_, n_c_, lu.get(), n_c_, work.get(), ipiv.get(), info.get()) !=
-        CUSOLVER_STATUS_SUCCESS)
-        fail(SDG_ECUDA, "cusolverDnDgetrf failed");
-    int hinfo = 0;
-    SDG_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, cx.stream));
-    cx.sync();
-    if (hinfo > 0)
-        fail(SDG_ESINGULAR, "lu_factor: matrix is singular, zero pivot in row " + std::to_string(hinfo - 1));
-    if (cusolverDnDgetrs(h, CUBLAS_OP_N, n_c_, n_c_, lu.get(), n_c_, ipiv.get(), coarse_inv_.get(),
-                         n_c_, info.get()) != CUSOLVER_STATUS_SUCCESS)
-        fail(SDG_ECUDA, "cusolverDnDgetrs failed");
-    cx.sync();
-}
-
 void AmgPrecond::factor_coarse(const HostCsr& coarse) {
     n_c_ = coarse.n_rows;
-    dense_inverse(*ctx_, coarse, coarse_inv_);
+    coarse_.build(*ctx_, coarse);
 }
 
 int64_t AmgPrecond::setup_memory_doubles() const {
-    int64_t s = static_cast<int64_t>(n_c_) * n_c_;
+    int64_t s = coarse_.doubles() + coarse_.sparse_entries();
     for (const auto& l : levels_) s += l.a.nnz;
     return s;
 }
 
 int64_t AmgPrecond::work_per_apply() const {
-    int64_t s = static_cast<int64_t>(n_c_) * n_c_;
+    int64_t s = coarse_.doubles() + coarse_.sparse_entries();
     for (const auto& l : levels_) s += 5 * l.a.nnz;
     return s;
 }
@@ -292,7 +250,7 @@ int64_t AmgPrecond::work_per_apply() const {
 void AmgPrecond::vcycle(int lev, const double* r, double* z) {
     Context& cx = *ctx_;
     if (lev + 1 == num_levels()) {
-        launch_dense_gemv(cx, n_c_, coarse_inv_.get(), r, z);
+        coarse_.solve(cx, r, z);
         return;
     }
     Level& L = levels_[lev];

@@ -8,6 +8,7 @@
 #include <memory>
 #include <vector>
 
+#include "coarse.hpp"
 #include "common.hpp"
 #include "gs.cuh"
 #include "kernels.cuh"
@@ -162,7 +163,7 @@ private:
     bool exact_ = false;  // SDG_GS_EXACT=1: bitwise smoother path throughout
     std::vector<Level> levels_;
     int n_c_ = 0;
-    DevBuf<double> coarse_inv_;  // row-major inverse of the coarsest matrix
+    CoarseSolver coarse_;  // direct solve of the coarsest matrix (coarse.hpp)
 };
 
 // Inexact Uzawa sweep (precond.cpp:264-299).
@@ -256,7 +257,6 @@ SolveOut bicgstab(Matrix& a, Precond* p, const double* b_dev, double* x_dev, dou
 
 // Row-major explicit inverse of a (small, coarsest-level) matrix: dense LU on
 // the device (cuSOLVER getrf) + getrs against I.  Throws SDG_ESINGULAR.
-void dense_inverse(Context& c, const HostCsr& a, DevBuf<double>& inv);
 
 struct PowerOut {
     double value = 0.0;

@@ -135,6 +135,11 @@ def lib():
         p("sdg_ilu0_create", _i, [_vp, P(_vp)])
         p("sdg_ground_dof_host", _i, [_i, _ip, _ip, _dp, _i])
         p("sdg_gs_merged_sweep_host", _i, [_i, _ip, _ip, _dp, _i, _i, _dp, _vp, _dp, P(_i)])
+        p("sdg_lu_factor", _i, [_vp, _i, _ip, _ip, _dp, P(_vp)])
+        p("sdg_lu_solve", _i, [_vp, _dp, _dp])
+        p("sdg_lu_info", _i, [_vp, P(_i), P(_i), P(_i64)])
+        p("sdg_lu_destroy", None, [_vp])
+        p("sdg_nd_solve_host", _i, [_i, _ip, _ip, _dp, _i, _i, _vp, _vp, _vp, P(_i), P(_i), P(_i), P(_i64), _vp, _i])
         p("sdg_td_create", _i, [_vp, _i, _i, _i, _i, _i, _i, _i, _d, P(_vp)])
         p("sdg_precond_destroy", _i, [_vp])
         p("sdg_precond_rows", _i, [_vp])
@@ -407,6 +412,78 @@ def gs_merged_sweep_host(a: SparseMatrix, r, k: int, dyn_cap: int = 0, z_old=Non
     _check(lib().sdg_gs_merged_sweep_host(a.n_rows, a.row_offsets, a.col_indices, a.values, int(k), int(dyn_cap), r,
                                           None if zo is None else zo.ctypes.data, z, C.byref(g)))
     return z, g.value
+
+
+class LUFactorization:
+    """lu_factor / lu_solve (lu.hpp:38-41) on the GPU: the direct solve the AMG
+    hierarchies use on their coarsest level (csrc/coarse.hpp)."""
+
+    def __init__(self, a: SparseMatrix, ctx: Optional[Context] = None):
+        if a.n_rows != a.n_cols:
+            raise ValueError("lu_factor: matrix must be square")
+        self.ctx = ctx or default_context()
+        self.n = a.n_rows
+        self.h = _vp()
+        _check(lib().sdg_lu_factor(self.ctx.h, a.n_rows, a.row_offsets, a.col_indices,
+                                   a.values if a.values.size else np.zeros(1), C.byref(self.h)))
+
+    def rows(self) -> int:
+        return self.n
+
+    def solve(self, b) -> np.ndarray:
+        b = _f64(b)
+        if b.size != self.n:
+            raise ValueError("lu_solve: dimension mismatch")
+        x = np.empty(self.n)
+        if self.n:
+            _check(lib().sdg_lu_solve(self.h, b, x))
+        return x
+
+    def info(self) -> dict:
+        d, k, s = _i(), _i(), _i64()
+        _check(lib().sdg_lu_info(self.h, C.byref(d), C.byref(k), C.byref(s)))
+        return {"dense": bool(d.value), "depth": k.value, "stored_doubles": s.value}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().sdg_lu_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def lu_factor(a: SparseMatrix, ctx: Optional[Context] = None) -> LUFactorization:
+    return LUFactorization(a, ctx)
+
+
+def lu_solve(f: LUFactorization, b) -> np.ndarray:
+    return f.solve(b)
+
+
+def nd_solve_host(a: SparseMatrix, b=None, leaf_rows: int = 1024, max_depth: int = 32):
+    """Host check of the coarse direct solve (csrc/coarse.hpp, replaces
+    lu_factor/lu_solve lu.cpp:91-203): nested-dissection order of `a` and, when
+    b is given, A^{-1} b through the block elimination.  Returns a dict with
+    x, perm (new -> old), nodes (lo, mid, hi, depth per node, post-order),
+    depth, max_separator and stored_doubles."""
+    n = a.n_rows
+    perm = np.empty(max(n, 1), np.int32)
+    nn, dep, ms, sd = _i(), _i(), _i(), _i64()
+    x = None
+    if b is not None:
+        b = _f64(b)
+        if b.size != n:
+            raise ValueError("nd_solve_host: dimension mismatch")
+        x = np.empty(n)
+    cap = 4 * max(1, n)
+    nodes = np.empty((cap, 4), np.int32)
+    _check(lib().sdg_nd_solve_host(n, a.row_offsets, a.col_indices, a.values, int(leaf_rows), int(max_depth),
+                                   None if b is None else b.ctypes.data, None if x is None else x.ctypes.data,
+                                   perm.ctypes.data, C.byref(nn), C.byref(dep), C.byref(ms), C.byref(sd),
+                                   nodes.ctypes.data, cap))
+    return {"x": x, "perm": perm[:n], "nodes": nodes[:nn.value].copy(), "depth": dep.value,
+            "max_separator": ms.value, "stored_doubles": sd.value}
 
 
 def sor_sweep(a: SparseMatrix, z, r, omega: float) -> np.ndarray:

@@ -74,7 +74,7 @@ def test_gpus_flag_relaunches_as_ranks():
     assert len(lines) == 1
     line = json.loads(lines[0])
     assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
-    assert line["config"]["system"].startswith("reference assemble_monolithic")
+    assert line["details"]["system"].startswith("reference assemble_monolithic")
 
 
 def test_launcher_command():

@@ -410,3 +410,102 @@ def _sub(a, r0, r1, c0, c1):
     m = sp.csr_matrix((a.val, a.col, a.rowptr), shape=(a.n_rows, a.n_cols))[r0:r1, c0:c1].tocsr()
     m.sort_indices()
     return m.indptr.astype(np.int32), m.indices.astype(np.int32), m.data
+
+
+# ---------------------------------------------------------------------------
+# coarse direct solve on the device (csrc/coarse.cu; lu_factor / lu_solve, lu.cpp:91-203)
+
+def _coarse_level(cfg_name, which):
+    from paper_2108_13229_b200 import scenarios
+    cfg = scenarios.CONFIGS[cfg_name]
+    s = scenarios.build_system(cfg)
+    if which == "V":
+        m = sdc.submatrix(s.matrix, 0, s.n_vel, 0, s.n_vel)
+        o = sdc.AmgOptions(components=[0] * s.n_u + [1] * (s.n_vel - s.n_u), max_levels=cfg.v_max_levels)
+    else:
+        m = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
+        o = sdc.AmgOptions(max_levels=cfg.d_max_levels)
+    return sdc.host_hierarchy(m, o)[-1].a
+
+
+def _host_spmv(a, x):
+    import scipy.sparse as sp
+    return sp.csr_matrix((a.values, a.col_indices, a.row_offsets), shape=(a.n_rows, a.n_cols)) @ x
+
+
+@pytest.mark.parametrize("mode", [{"SDG_COARSE": "dense"}, {"SDG_COARSE": "nd", "SDG_ND_LEAF": "128"},
+                                  {"SDG_COARSE": "nd", "SDG_ND_LEAF": "40"}], ids=["dense", "nd128", "nd40"])
+def test_lu_solve_matches_reference(ref, monkeypatch, mode):
+    """Device direct solve (dense Gauss-Jordan inverse, and the nested-dissection
+    block elimination at two leaf sizes) against the reference's lu_factor +
+    lu_solve on the coarsest matrices of the c2 hierarchies, and bitwise against
+    a second solve (deterministic)."""
+    from oracle.refpy import Csr
+    for k, v in mode.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(11)
+    for which in ("V", "D"):
+        a = _coarse_level("c2", which)
+        f = sdc.lu_factor(a)
+        info = f.info()
+        assert info["dense"] == (mode["SDG_COARSE"] == "dense")
+        if not info["dense"]:
+            assert info["depth"] >= 3 and info["stored_doubles"] < 0.4 * a.n_rows ** 2
+        b = rng.standard_normal(a.n_rows)
+        x = f.solve(b)
+        x_ref = ref.lu_solve(Csr(a.n_rows, a.n_cols, a.row_offsets, a.col_indices, a.values), b)
+        assert rel_l2(x, x_ref) < 1e-10
+        assert bitwise_equal(x, f.solve(b))
+
+
+def test_lu_solve_c3_coarse_levels_residual():
+    """Default policy at c3 (V: 12,246 rows, D: 4,704 rows -> nested dissection):
+    the residual of the device solve is at rounding level."""
+    rng = np.random.default_rng(12)
+    for which in ("V", "D"):
+        a = _coarse_level("c3", which)
+        f = sdc.lu_factor(a)
+        info = f.info()
+        assert not info["dense"] and info["stored_doubles"] < 0.2 * a.n_rows ** 2
+        b = rng.standard_normal(a.n_rows)
+        x = f.solve(b)
+        assert np.linalg.norm(_host_spmv(a, x) - b) <= 1e-11 * np.linalg.norm(b) * max(1.0, np.abs(x).max())
+        xh = sdc.nd_solve_host(a, b)["x"] if which == "D" else None
+        if xh is not None:  # same algebra on the host (different rounding: FMA, reduction trees)
+            assert rel_l2(x, xh) < 1e-10
+
+
+def test_lu_factor_pivoting_and_errors(ref):
+    # needs row exchanges: zero diagonal
+    p = np.array([[0.0, 2.0, 0.0, 0.0], [1.0, 0.0, 0.0, 3.0], [0.0, 0.0, 0.0, 1.0], [0.0, 1.0, 5.0, 0.0]])
+    f = sdc.lu_factor(sdc.SparseMatrix.from_dense(p))
+    b = np.array([1.0, 2.0, 3.0, 4.0])
+    assert np.allclose(p @ f.solve(b), b, atol=1e-13)
+    # nonsymmetric KAT matrix (test_krylov.cpp:75-93 generator)
+    a = ref.random_dominant(200, 0.05, 3)
+    r = ref.random_vector(200, 4)
+    x = sdc.lu_solve(sdc.lu_factor(to_sdc(a)), r)
+    assert rel_l2(x, ref.lu_solve(a, r)) < 1e-12
+    with pytest.raises(RuntimeError):  # lu.cpp:142
+        sdc.lu_factor(sdc.SparseMatrix.from_dense(np.array([[1.0, 2.0], [2.0, 4.0]])))
+    with pytest.raises(ValueError):
+        sdc.lu_factor(sdc.SparseMatrix.from_dense(np.ones((2, 3))))
+    assert sdc.lu_factor(sdc.SparseMatrix(0, 0, np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0))).solve(
+        np.zeros(0)).size == 0
+
+
+def test_forced_nd_singular_block_falls_back_to_dense(monkeypatch):
+    """An indefinite but regular matrix whose diagonal blocks are singular: the
+    dissection's blocks cannot be inverted, the whole-matrix pivoting can."""
+    monkeypatch.setenv("SDG_COARSE", "nd")
+    monkeypatch.setenv("SDG_ND_LEAF", "32")
+    n = 120
+    d = np.zeros((n, n))
+    for i in range(n):  # a chain of 2-cycles: zero diagonal everywhere
+        j = i + 1 if i % 2 == 0 else i - 1
+        d[i, j] = 2.0 + i
+        if i + 2 < n:
+            d[i, i + 2] = 0.5
+    f = sdc.lu_factor(sdc.SparseMatrix.from_dense(d))
+    b = np.arange(1.0, n + 1)
+    assert np.allclose(d @ f.solve(b), b, atol=1e-9)

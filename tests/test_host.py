@@ -237,3 +237,95 @@ def test_lattice_planner_host_check(cfg_name):
         checked += 1
         assert e <= 1e-13
     assert checked >= 2
+
+
+# ---------------------------------------------------------------------------
+# coarse direct solve (csrc/coarse.hpp; replaces lu_factor / lu_solve, lu.cpp:91-203)
+
+def _coarse_matrices(cfg_name):
+    cfg = scenarios.CONFIGS[cfg_name]
+    s = scenarios.build_system(cfg)
+    V = sdc.submatrix(s.matrix, 0, s.n_vel, 0, s.n_vel)
+    D = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
+    hv = sdc.host_hierarchy(V, sdc.AmgOptions(components=[0] * s.n_u + [1] * (s.n_vel - s.n_u),
+                                              max_levels=cfg.v_max_levels))
+    hd = sdc.host_hierarchy(D, sdc.AmgOptions(max_levels=cfg.d_max_levels))
+    return hv[-1].a, hd[-1].a
+
+
+def _check_dissection(a, r):
+    import scipy.sparse as sp
+    n = a.n_rows
+    perm, nodes = r["perm"], r["nodes"]
+    assert sorted(perm.tolist()) == list(range(n))
+    A = sp.csr_matrix((a.values, a.col_indices, a.row_offsets), shape=(n, n))
+    P = (abs(A) + abs(A).T)[perm][:, perm].tocsr()
+    # post-order: the last node is the root and covers everything
+    assert nodes[-1][0] == 0 and nodes[-1][2] == n
+    stack = []
+    for lo, mid, hi, depth in nodes.tolist():
+        assert lo <= mid <= hi
+        kids = []
+        while stack and stack[-1][0] >= lo:
+            kids.append(stack.pop())
+        if kids:  # internal: its two subtrees tile [lo, mid) and do not touch each other
+            assert len(kids) == 2
+            (l2, h2), (l1, h1) = kids
+            assert l1 == lo and h1 == l2 and h2 == mid
+            assert P[l1:h1][:, l2:h2].nnz == 0
+        else:
+            assert mid == hi
+        stack.append((lo, hi))
+    assert len(stack) == 1
+
+
+@pytest.mark.parametrize("leaf", [64, 128, 1024])
+def test_nd_host_solve_matches_reference_lu(ref, leaf):
+    """The block elimination equals the reference's lu_factor + lu_solve on the
+    coarsest matrices of the c2 hierarchies (n = 1,407 and 1,903)."""
+    from oracle.refpy import Csr
+    rng = np.random.default_rng(5)
+    for a in _coarse_matrices("c2"):
+        b = rng.standard_normal(a.n_rows)
+        r = sdc.nd_solve_host(a, b, leaf_rows=leaf)
+        _check_dissection(a, r)
+        if leaf < 1024:
+            assert r["depth"] >= 3 and r["stored_doubles"] < 0.35 * a.n_rows ** 2
+        x_ref = ref.lu_solve(Csr(a.n_rows, a.n_cols, a.row_offsets, a.col_indices, a.values), b)
+        assert np.linalg.norm(r["x"] - x_ref) <= 1e-10 * np.linalg.norm(x_ref)
+
+
+def test_nd_host_solve_edge_cases(ref):
+    # nonsymmetric KAT matrix (test_krylov.cpp:75-93 generator), forced deep dissection
+    a = to_sdc(ref.random_dominant(300, 0.02, 7))
+    b = ref.random_vector(300, 8)
+    r = sdc.nd_solve_host(a, b, leaf_rows=16)
+    _check_dissection(a, r)
+    assert np.allclose(sdc_spmv_host(a, r["x"]), b, rtol=0, atol=1e-11)
+    # disconnected graph: block diagonal, empty separators
+    d = np.zeros((40, 40))
+    for k in range(4):
+        blk = np.random.default_rng(k).standard_normal((10, 10)) + 10 * np.eye(10)
+        d[10 * k:10 * k + 10, 10 * k:10 * k + 10] = blk
+    a = sdc.SparseMatrix.from_dense(d)
+    b = np.arange(40.0)
+    r = sdc.nd_solve_host(a, b, leaf_rows=8)
+    _check_dissection(a, r)
+    assert np.allclose(d @ r["x"], b, atol=1e-11)
+    # tiny and empty systems
+    r = sdc.nd_solve_host(sdc.SparseMatrix.from_dense(np.array([[4.0]])), np.array([2.0]))
+    assert r["x"][0] == 0.5
+    r = sdc.nd_solve_host(sdc.SparseMatrix(0, 0, np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0)), np.zeros(0))
+    assert r["x"].size == 0
+    # partial pivoting inside a block: zero diagonal
+    p = np.array([[0.0, 2.0, 0.0], [1.0, 0.0, 0.0], [0.0, 0.0, 3.0]])
+    r = sdc.nd_solve_host(sdc.SparseMatrix.from_dense(p), np.array([2.0, 1.0, 3.0]))
+    assert np.allclose(r["x"], [1.0, 1.0, 1.0])
+    # singular: like lu_factor's runtime_error (lu.cpp:142)
+    with pytest.raises(RuntimeError):
+        sdc.nd_solve_host(sdc.SparseMatrix.from_dense(np.array([[1.0, 2.0], [2.0, 4.0]])), np.ones(2))
+
+
+def sdc_spmv_host(a, x):
+    import scipy.sparse as sp
+    return sp.csr_matrix((a.values, a.col_indices, a.row_offsets), shape=(a.n_rows, a.n_cols)) @ x
