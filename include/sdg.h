@@ -328,6 +328,14 @@ int sdg_host_hierarchy_level(const sdg_host_hierarchy* h, int lev, int* n, int64
                              double* val, int* agg);
 void sdg_host_hierarchy_destroy(sdg_host_hierarchy* h);
 
+/* Galerkin product of an aggregation on the device (galerkin_product,
+ * precond.cpp:177-185; csrc/galerkin.cu): A_c = P^T A P for agg (fine row ->
+ * aggregate, n_coarse aggregates), bitwise equal to the reference's CooBuilder
+ * sum order.  The device AMG setup uses it for every level.  Outputs: c_rowptr
+ * (n_coarse + 1), c_col / c_val (capacity nnz(A) suffices), *c_nnz. */
+int sdg_galerkin_device(sdg_context* ctx, int n, const int* rowptr, const int* col, const double* val, const int* agg,
+                        int n_coarse, int* c_rowptr, int* c_col, double* c_val, int64_t* c_nnz);
+
 /* ---- direct solve (lu.hpp:38-41: lu_factor / lu_solve) ----------------------
  * The factorization the AMG hierarchies use on their coarsest level, as its own
  * handle: a nested-dissection block elimination with explicit inverses of small

@@ -682,6 +682,26 @@ int sdg_host_hierarchy_level(const sdg_host_hierarchy* h, int lev, int* n, int64
 
 void sdg_host_hierarchy_destroy(sdg_host_hierarchy* h) { delete h; }
 
+int sdg_galerkin_device(sdg_context* ctx, int n, const int* rowptr, const int* col, const double* val, const int* agg,
+                        int n_coarse, int* c_rowptr, int* c_col, double* c_val, int64_t* c_nnz) {
+    return guard([&] {
+        need(ctx, "sdg_galerkin_device");
+        need(agg, "sdg_galerkin_device");
+        need(c_rowptr, "sdg_galerkin_device");
+        sdg::HostCsr h = make_csr(n, n, rowptr, col, val);
+        h.check();
+        std::vector<int> a(agg, agg + n);
+        for (int x : a)
+            if (x < 0 || x >= n_coarse) sdg::fail(SDG_EINVAL, "sdg_galerkin_device: aggregate id out of range");
+        SDG_CUDA(cudaSetDevice(ctx->p->device));
+        const sdg::HostCsr c = sdg::galerkin_device(*ctx->p, h, a, n_coarse);
+        std::memcpy(c_rowptr, c.rp.data(), sizeof(int) * c.rp.size());
+        if (c_col) std::memcpy(c_col, c.ci.data(), sizeof(int) * c.ci.size());
+        if (c_val) std::memcpy(c_val, c.v.data(), sizeof(double) * c.v.size());
+        if (c_nnz) *c_nnz = c.nnz();
+    });
+}
+
 int sdg_lu_factor(sdg_context* ctx, int n, const int* rowptr, const int* col, const double* val, sdg_lu** out) {
     return guard([&] {
         need(ctx, "sdg_lu_factor");

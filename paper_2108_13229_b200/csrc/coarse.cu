@@ -267,7 +267,7 @@ k_nd_leaf(int n, const NdNodeDev* __restrict__ nodes, const int* __restrict__ le
 
 // separators of one depth: t = u_S - A_SI y_I (every part computes all of t),
 // then x_S = inv(Sc) t for the part's rows.  blockIdx.x = node * parts + part.
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
 k_nd_sep(const int* __restrict__ ids, int parts, const NdNodeDev* __restrict__ nodes, const int* __restrict__ rp,
          const int* __restrict__ ci, const double* __restrict__ v, const double* __restrict__ pool,
          const double* __restrict__ u, const int* __restrict__ perm, double* __restrict__ y, long long ld,
@@ -279,14 +279,25 @@ k_nd_sep(const int* __restrict__ ids, int parts, const NdNodeDev* __restrict__ n
     const int ns = nd.hi - nd.mid;
     const double* __restrict__ uc = u + blockIdx.y * ld;
     double* __restrict__ yc = y + blockIdx.y * ld;
-    for (int s = threadIdx.x; s < ns; s += blockDim.x) {
-        const int row = nd.mid + s;
-        double acc = perm ? uc[perm[row]] : uc[row];
-        for (int k = rp[row]; k < rp[row + 1]; ++k) {
-            const int j = ci[k];
-            if (j >= nd.lo && j < nd.mid) acc = fma(-v[k], yc[j], acc);
+    // eight lanes per separator row: the row's entries are loaded side by side
+    // (a thread per row would chain one L2 round trip per entry)
+    const int sub = threadIdx.x & 7, grp = threadIdx.x >> 3, ngrp = blockDim.x >> 3;
+    for (int s0 = 0; s0 < ns; s0 += ngrp) {
+        const int s = s0 + grp;
+        const bool valid = s < ns;
+        const int row = nd.mid + (valid ? s : 0);
+        double acc = 0.0;
+        if (valid) {
+            const int ke = rp[row + 1];
+            for (int k = rp[row] + sub; k < ke; k += 8) {
+                const int j = ci[k];
+                if (j >= nd.lo && j < nd.mid) acc = fma(-v[k], yc[j], acc);
+            }
         }
-        t[s] = acc;
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (valid && sub == 0) t[s] = (perm ? uc[perm[row]] : uc[row]) + acc;
     }
     __syncthreads();
     const int per = (ns + parts - 1) / parts;
@@ -574,7 +585,7 @@ void CoarseSolver::run_phases(Context& cx, int above, const double* u, const int
         if (static_cast<size_t>(max_s_[d]) * 8 > 200 * 1024) fail(SDG_ENOMEM, "coarse solve: separator too wide");
         {
             ProfScope ps(cx, m == 1 ? PF_COARSE : PF_SETUP, bytes_sep_[d]);
-            launch_k(cx, k_nd_sep, dim3(n_ids_[d] * parts, m), 512, static_cast<size_t>(max_s_[d]) * 8, ids_[d].get(),
+            launch_k(cx, k_nd_sep, dim3(n_ids_[d] * parts, m), 1024, static_cast<size_t>(max_s_[d]) * 8, ids_[d].get(),
                      parts, nodes_.get(), ap_.rp.get(), ap_.ci.get(), ap_.v.get(), pool_.get(), u, perm, y, ld, xo);
             SDG_CHECK_LAUNCH(cx);
         }

@@ -657,8 +657,12 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     //     (gs_lattice.cu; opt-in, SDG_GS_LATTICE=1, here and in build_parts:
     //     bitwise equal to the level walks but measured slower than them at c3,
     //     DESIGN.md §3)
+    // SDG_GS_LATTICE: 0 never, 1 wherever a level (or label block) is a
+    // lattice, unset: per label block the faster of the level walk and the
+    // lattice, timed on the device at setup (build_parts; needs `tune`)
     const char* lat_env = knob("SDG_GS_LATTICE");
-    lattice_off_ = !(lat_env && lat_env[0] == '1');
+    lattice_mode_ = lat_env ? (lat_env[0] == '1' ? 1 : 0) : (tune ? 2 : 0);
+    lattice_off_ = lattice_mode_ != 1;
     if (want_walk && !lattice_off_ && !force_split && !try_pipe && !knob("SDG_GS_MERGE") &&
         build_lattice(a, dinv_h, s))
         return finish();
@@ -1013,6 +1017,25 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     SDG_CUDA(cudaStreamSynchronize(s));  // host staging vectors die here
 }
 
+// mean device time (ms) of one lower solve of a stand-alone plan (its own records)
+static double time_lower(Context& c, const GsPlan& g) {
+    DevBuf<double> z(std::max(g.n, 1));
+    cudaEvent_t e0, e1;
+    SDG_CUDA(cudaEventCreate(&e0));
+    SDG_CUDA(cudaEventCreate(&e1));
+    for (int r = 0; r < 2; ++r) launch_gs_lower(c, g, z.get());
+    constexpr int kReps = 6;
+    SDG_CUDA(cudaEventRecord(e0, c.stream));
+    for (int r = 0; r < kReps; ++r) launch_gs_lower(c, g, z.get());
+    SDG_CUDA(cudaEventRecord(e1, c.stream));
+    SDG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    SDG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms / kReps;
+}
+
 bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std::vector<double>& dinv_h,
                          cudaStream_t s) {
     const int nparts = static_cast<int>(r0.size()) - 1;
@@ -1035,8 +1058,21 @@ bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std
             max_k = std::max(max_k, nlow[i - lo]);
         }
         auto p = std::make_unique<GsPlan>();
-        if (!(!lattice_off_ && p->build_lattice(sub, dsub, s)) && !p->build_walk(sub, dsub, nlow, max_k, s))
+        if (lattice_mode_ == 2 && tune) {
+            // measured choice: both plans sweep their own (zero) records a few times
+            if (!p->build_walk(sub, dsub, nlow, max_k, s)) return false;
+            auto q = std::make_unique<GsPlan>();
+            if (q->build_lattice(sub, dsub, s)) {
+                const double tw = time_lower(*tune, *p), tl = time_lower(*tune, *q);
+                if (std::getenv("SDG_DEBUG"))
+                    std::fprintf(stderr, "[sdg gs plan] label block %d (%d rows): walk %.1f us, lattice %.1f us\n", k, m,
+                                 tw * 1e3, tl * 1e3);
+                if (tl < 0.95 * tw) p = std::move(q);
+            }
+        } else if (!(lattice_mode_ == 1 && p->build_lattice(sub, dsub, s)) &&
+                   !p->build_walk(sub, dsub, nlow, max_k, s)) {
             return false;
+        }
         ps.push_back(std::move(p));
     }
     // one record buffer; the prep kernels write b through the global bidx

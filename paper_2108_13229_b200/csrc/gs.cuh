@@ -91,20 +91,23 @@ struct GsPlan {
     bool wave = false;
     int wave_kind = 0;                   // 1: 5-point grid, 2: MAC velocity (u and v rows in one pass)
     int wave_nx = 0, wave_ny = 0;        // grid columns (m for MAC) / grid rows
-    int wave_bands = 0, wave_blocks = 0;
+    int wave_bands = 0, wave_blocks = 0, wave_w = 1;  // wave_w: bands (warps) per CTA
     size_t wave_smem = 0;
     DevBuf<unsigned long long> wave_ticket;  // band tickets handed out (gs_wave.cu)
     DevBuf<double> wave_bnd;                 // band boundary rows, two parities, sentinel until written
     // multi-SM lattice lower solve of an aggregated coarse level (gs_lattice.cu);
     // records in `packed`
     bool lattice = false;
-    int lat_bands = 0, lat_blocks = 0;
+    int lat_bands = 0, lat_blocks = 0, lat_w = 1, lat_depth = 4;  // lat_w bands (warps) per CTA
+    size_t lat_smem = 0;
     DevBuf<int> lat_win;                     // per (band, block): first window step of the previous band
     DevBuf<unsigned long long> lat_ticket;   // band tickets handed out
     DevBuf<double> lat_bnd;                  // last-chain values of every band, two parities, sentinel until written
     // per row: 1 when it has entries left of the diagonal (its lower solve reads other rows)
     std::vector<unsigned char> row_has_lower;
     bool lattice_off_ = false;  // SDG_GS_LATTICE=0 (build_parts asks its parts too)
+    int lattice_mode_ = 0;      // 0 off, 1 wherever the level is a lattice, 2 the faster of walk and lattice (timed)
+    Context* tune = nullptr;    // set by the owner before build(): lets the planner time candidate plans
     // level merging (gs.cu, merge_levels): groups of k consecutive dependency
     // levels are walked as one; rows inside a group are substituted into each
     // other, so the walk reads only earlier groups and the prep computes the

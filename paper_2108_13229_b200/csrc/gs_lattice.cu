@@ -72,7 +72,7 @@ __device__ __forceinline__ bool lat_ready(double v) {
 }
 __device__ __forceinline__ double lat_ld_if(const double* p, bool pred) {
     double v;
-    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\nmov.b64 %0, 0;\n@q ld.relaxed.gpu.global.f64 %0, [%1];\n}"
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\nmov.b64 %0, 0;\n@q ld.relaxed.gpu.f64 %0, [%1];\n}"
                  : "=d"(v)
                  : "l"(p), "r"(static_cast<int>(pred))
                  : "memory");
@@ -80,7 +80,7 @@ __device__ __forceinline__ double lat_ld_if(const double* p, bool pred) {
 }
 __device__ __forceinline__ void lat_st_relaxed_if(double* p, double v, bool pred) {
     const double w = v + 0.0;  // quiets a signalling NaN: a stored value is never the sentinel
-    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.relaxed.gpu.global.f64 [%0], %1;\n}" ::"l"(p),
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.relaxed.gpu.f64 [%0], %1;\n}" ::"l"(p),
                  "d"(w), "r"(static_cast<int>(pred)));
 }
 __device__ __forceinline__ void lat_st_if(double* p, double v, bool pred) {
@@ -98,36 +98,52 @@ __device__ __forceinline__ void lat_tma_if(double* dst, const double* src, unsig
         : "memory");
 }
 
-// One warp per band; all control flow warp-uniform (per-lane work predicated).
-__global__ void __launch_bounds__(32, 1) k_gs_lattice(LatArgs a) {
+// One warp per band, W consecutive bands per CTA, D blocks of records in flight
+// per band; all control flow warp-uniform (per-lane work predicated).  Two
+// bands of one CTA hand the last chain's values over through shared memory
+// (value-as-flag slots filled with the sentinel at kernel start); the first
+// band of a CTA polls the previous CTA's boundary in L2.  Generic-address
+// loads and stores serve both.
+template <int W, int D>
+__global__ void __launch_bounds__(32 * W, 1) k_gs_lattice(LatArgs a) {
     constexpr int KU = kLatKU, F = kLatF, BLK = F * KU * 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* ring = reinterpret_cast<double*>(smem_raw);      // records
-    double* wins = ring + kLatDepth * BLK;                   // two windows
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wins + kLatVals);
-    const int lane = threadIdx.x;
-    unsigned long long t = 0;
+    __shared__ unsigned long long s_ticket;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* base = reinterpret_cast<double*>(smem_raw);
+    double* ring = base + warp * (D * BLK);                              // records
+    double* wins = base + W * D * BLK + warp * kLatVals;                 // two windows
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + W * D * BLK + W * kLatVals) + warp * D;
+    double* sh_bnd = base + W * D * BLK + W * kLatVals + W * D;          // inbound boundaries of warps 1 .. W-1
+    const int T = a.nblocks * KU;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1ull);
     if (lane == 0) {
-        t = atomicAdd(a.ticket, 1ull);
 #pragma unroll
-        for (int d = 0; d < kLatDepth; ++d) ptx::mbar_init(bars + d, 1);
+        for (int d = 0; d < D; ++d) ptx::mbar_init(bars + d, 1);
         ptx::fence_mbar_init();
     }
-    t = __shfl_sync(0xffffffffu, t, 0);
-    __syncwarp();
-    const int band = static_cast<int>(t % static_cast<unsigned long long>(a.nbands));
-    const int par = static_cast<int>((t / static_cast<unsigned long long>(a.nbands)) & 1ull);
+    if (W > 1 && warp > 0) {
+        double* mine = sh_bnd + static_cast<size_t>(warp - 1) * T;
+        for (int k = lane; k < T; k += 32) mine[k] = __longlong_as_double(static_cast<long long>(kLatSent));
+    }
+    __syncthreads();
+    const unsigned long long t = s_ticket;
+    const unsigned long long nctas = static_cast<unsigned long long>((a.nbands + W - 1) / W);
+    const int band = static_cast<int>(t % nctas) * W + warp;
+    const int par = static_cast<int>((t / nctas) & 1ull);
+    if (band >= a.nbands) return;
     pdl_wait();  // b is written by the prep kernel; the previous launch of this plan is complete
     pdl_trigger();
     const double* src = a.rec + static_cast<size_t>(band) * a.nblocks * BLK;
-    for (int d = 0; d < kLatDepth && d < a.nblocks; ++d)
+    for (int d = 0; d < D && d < a.nblocks; ++d)
         lat_tma_if(ring + d * BLK, src + static_cast<size_t>(d) * BLK, BLK * 8, bars + d, lane == 0);
-    const int T = a.nblocks * KU;
     const bool has_src = band > 0, has_dst = band + 1 < a.nbands;
+    const bool src_sh = W > 1 && warp > 0, dst_sh = W > 1 && warp + 1 < W && has_dst;
     const size_t pstride = static_cast<size_t>(a.nbands) * T;
-    const double* b_in = a.bnd + par * pstride + static_cast<size_t>(has_src ? band - 1 : 0) * T;
-    double* b_out = a.bnd + par * pstride + static_cast<size_t>(band) * T;
-    if (has_src) {  // the other parity's input slots, for the next launch
+    const double* b_in = src_sh ? sh_bnd + static_cast<size_t>(warp - 1) * T
+                                : a.bnd + par * pstride + static_cast<size_t>(has_src ? band - 1 : 0) * T;
+    double* b_out = dst_sh ? sh_bnd + static_cast<size_t>(warp) * T : a.bnd + par * pstride + static_cast<size_t>(band) * T;
+    if (has_src && !src_sh) {  // the other parity's input slots, for the next launch
         double* rs = a.bnd + (par ^ 1) * pstride + static_cast<size_t>(band - 1) * T;
         for (int k = lane; k < T; k += 32) rs[k] = __longlong_as_double(static_cast<long long>(kLatSent));
     }
@@ -149,8 +165,8 @@ __global__ void __launch_bounds__(32, 1) k_gs_lattice(LatArgs a) {
     double h1 = 0.0, h2 = 0.0, h3 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0, p4 = 0.0;
     for (int q = 0; q < a.nblocks; ++q) {
         double wn = load_win(q + 1);  // in flight during this block
-        const int slot = q % kLatDepth;
-        ptx::mbar_wait(bars + slot, (q / kLatDepth) & 1);
+        const int slot = q % D;
+        ptx::mbar_wait(bars + slot, (q / D) & 1);
         __syncwarp();  // the window stored at the end of the previous block
         const double2* B = reinterpret_cast<const double2*>(ring + slot * BLK) + lane;
         const double* W = wins + (q & 1) * kLatW;
@@ -197,15 +213,16 @@ __global__ void __launch_bounds__(32, 1) k_gs_lattice(LatArgs a) {
             }
         }
         __syncwarp();  // every lane has read the record slot and the window
-        lat_tma_if(ring + slot * BLK, src + static_cast<size_t>(q + kLatDepth) * BLK, BLK * 8, bars + slot,
-                   lane == 0 && q + kLatDepth < a.nblocks);
+        lat_tma_if(ring + slot * BLK, src + static_cast<size_t>(q + D) * BLK, BLK * 8, bars + slot,
+                   lane == 0 && q + D < a.nblocks);
         if (q + 1 < a.nblocks) settle(q + 1, wn);
     }
 }
 
-size_t lat_smem_bytes() {
-    return static_cast<size_t>(kLatDepth) * kLatF * kLatKU * 32 * sizeof(double) + kLatVals * sizeof(double) +
-           kLatDepth * sizeof(uint64_t);
+size_t lat_smem_bytes(int w, int d, int steps) {
+    return static_cast<size_t>(w) * (static_cast<size_t>(d) * kLatF * kLatKU * 32 * sizeof(double) +
+                                     kLatVals * sizeof(double) + d * sizeof(uint64_t)) +
+           static_cast<size_t>(w - 1) * steps * sizeof(double);
 }
 
 }  // namespace
@@ -428,11 +445,26 @@ bool GsPlan::build_lattice(const HostCsr& a, const std::vector<double>& dinv_h, 
     lattice = true;
     lat_bands = h.nb;
     lat_blocks = h.nblocks;
+    // bands (warps) per CTA and blocks in flight per band: (2, 4) by default,
+    // (3, 3) / (4, 2) trade record look-ahead for fewer hand-offs through L2
+    // (SDG_LAT_W = 1..4); whatever shared memory holds
+    {
+        constexpr size_t kSmemMax = 226 * 1024;  // 227 KB per CTA minus the static words
+        int w = 2;
+        if (const char* e = std::getenv("SDG_LAT_W")) w = std::max(1, std::min(4, std::atoi(e)));
+        w = std::min(w, h.nb);
+        auto depth = [](int ww) { return ww <= 2 ? 4 : ww == 3 ? 3 : 2; };
+        while (w > 1 && lat_smem_bytes(w, depth(w), T) > kSmemMax) --w;
+        lat_w = w;
+        lat_depth = depth(w);
+        lat_smem = lat_smem_bytes(lat_w, lat_depth, T);
+    }
     walk = false;
     wave = false;
     usable = true;
     if (std::getenv("SDG_DEBUG"))
-        std::fprintf(stderr, "[sdg gs lattice] n=%d: %d chains in %d bands, %d steps\n", a.n_rows, h.nch, h.nb, T);
+        std::fprintf(stderr, "[sdg gs lattice] n=%d: %d chains in %d bands (%d per CTA), %d steps\n", a.n_rows, h.nch,
+                     h.nb, lat_w, T);
     return true;
 }
 
@@ -498,13 +530,15 @@ double lattice_check_host(const HostCsr& a, const double* b) {
 
 void launch_gs_lattice(Context& c, const GsPlan& g, double* z_new) {
     static const bool attr = [] {
-        SDG_CUDA(cudaFuncSetAttribute(k_gs_lattice, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(lat_smem_bytes())));
+        for (auto k : {k_gs_lattice<1, 4>, k_gs_lattice<2, 4>, k_gs_lattice<3, 3>, k_gs_lattice<4, 2>})
+            SDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         return true;
     }();
     (void)attr;
     LatArgs a{g.records(), g.lat_win.get(), z_new, g.lat_bnd.get(), g.lat_ticket.get(), g.lat_bands, g.lat_blocks};
-    launch_k(c, k_gs_lattice, g.lat_bands, 32, lat_smem_bytes(), a);
+    void (*k)(LatArgs) = g.lat_w == 4 ? k_gs_lattice<4, 2> : g.lat_w == 3 ? k_gs_lattice<3, 3>
+                         : g.lat_w == 2 ? k_gs_lattice<2, 4> : k_gs_lattice<1, 4>;
+    launch_k(c, k, (g.lat_bands + g.lat_w - 1) / g.lat_w, 32 * g.lat_w, g.lat_smem, a);
 }
 
 }  // namespace sdg

@@ -106,7 +106,7 @@ __device__ __forceinline__ bool not_sent(double v) {
 // compiler's divergent-warp fallback (collective shuffles) run the block.
 __device__ __forceinline__ double ld_relaxed_if(const double* p, bool pred) {
     double v;
-    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\nmov.b64 %0, 0;\n@q ld.relaxed.gpu.global.f64 %0, [%1];\n}"
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\nmov.b64 %0, 0;\n@q ld.relaxed.gpu.f64 %0, [%1];\n}"
                  : "=d"(v)
                  : "l"(p), "r"(static_cast<int>(pred))
                  : "memory");
@@ -118,7 +118,7 @@ __device__ __forceinline__ void st_relaxed_if(double* p, double v, bool pred) {
     const double w = v + 0.0;
     // no "memory" clobber: nothing this thread reads depends on the store, so
     // the compiler may keep scheduling the next step's shared loads across it
-    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.relaxed.gpu.global.f64 [%0], %1;\n}" ::"l"(p),
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.relaxed.gpu.f64 [%0], %1;\n}" ::"l"(p),
                  "d"(w), "r"(static_cast<int>(pred)));
 }
 // predicated store without a branch around it (the step loop stays convergent)
@@ -140,26 +140,41 @@ __device__ __forceinline__ void tma_block_if(double* dst, const double* src, uns
         : "memory");
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
+// W warps per CTA, one band each (consecutive bands).  The hand-off between
+// two bands of one CTA goes through shared memory (the same value-as-flag
+// slots, filled with the sentinel at kernel start); only the first band of a
+// CTA polls the previous CTA's boundary in L2.  The loads and stores use
+// generic addresses, so one code path serves both.
+template <int KIND, int W>
+__global__ void __launch_bounds__(32 * W, 1) k_gs_wave(WaveArgs a) {
     constexpr int F = WaveShape<KIND>::F, KU = WaveShape<KIND>::KU;
     constexpr int NBF = KIND == 1 ? 1 : 2;  // boundary fields: z, or u and v
     constexpr int BLK = F * KU * 32;        // doubles per block
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* ring = reinterpret_cast<double*>(smem_raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kWaveDepth * BLK);
-    const int lane = threadIdx.x;
-    unsigned long long t = 0;
+    __shared__ unsigned long long s_ticket;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* ring = reinterpret_cast<double*>(smem_raw) + warp * (kWaveDepth * BLK);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(smem_raw) + W * kWaveDepth * BLK) +
+                     warp * kWaveDepth;
+    const size_t bstride = static_cast<size_t>(NBF) * a.bcols;                 // one band boundary
+    // inbound boundaries of warps 1 .. W-1 (shared memory)
+    double* sh_bnd = reinterpret_cast<double*>(smem_raw) + W * kWaveDepth * BLK + W * kWaveDepth;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1ull);
     if (lane == 0) {
-        t = atomicAdd(a.ticket, 1ull);
 #pragma unroll
         for (int d = 0; d < kWaveDepth; ++d) ptx::mbar_init(bars + d, 1);
         ptx::fence_mbar_init();
     }
-    t = __shfl_sync(0xffffffffu, t, 0);
-    __syncwarp();
-    const int band = static_cast<int>(t % static_cast<unsigned long long>(a.nbands));
-    const int par = static_cast<int>((t / static_cast<unsigned long long>(a.nbands)) & 1ull);
+    if (W > 1 && warp > 0) {
+        double* mine = sh_bnd + (warp - 1) * bstride;
+        for (size_t k = lane; k < bstride; k += 32) mine[k] = __longlong_as_double(static_cast<long long>(kSent));
+    }
+    __syncthreads();
+    const unsigned long long t = s_ticket;
+    const unsigned long long nctas = static_cast<unsigned long long>((a.nbands + W - 1) / W);
+    const int band = static_cast<int>(t % nctas) * W + warp;
+    const int par = static_cast<int>((t / nctas) & 1ull);
+    if (band >= a.nbands) return;
     pdl_wait();  // b is written by the prep kernel before this launch; the previous launch is done
     pdl_trigger();
     const double* src = a.rec + static_cast<size_t>(band) * a.nblocks * BLK;
@@ -167,12 +182,15 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
         tma_block_if(ring + d * BLK, src + static_cast<size_t>(d) * BLK, BLK * 8, bars + d, lane == 0);
     const int j = band * 32 + lane;
     const bool has_src = band > 0, has_dst = band + 1 < a.nbands;
+    const bool src_sh = W > 1 && warp > 0, dst_sh = W > 1 && warp + 1 < W && has_dst;
     unsigned long long wait_ns = 0, t_start = a.tl ? gtimer() : 0, t_first = 0, tma_cyc = 0, comp_cyc = 0;
-    const size_t bstride = static_cast<size_t>(NBF) * a.bcols;                 // one band boundary
     const size_t pstride = static_cast<size_t>(a.nbands - 1) * bstride;         // one parity
-    const double* sb_in = has_src ? a.bnd + par * pstride + (band - 1) * bstride : a.bnd;   // read (lane 0)
-    double* sb_out = a.bnd + par * pstride + (has_dst ? band : 0) * bstride;                // written (lane 31)
-    if (has_src) {  // reset the input slots of the other parity for the next launch
+    const double* sb_in = src_sh    ? sh_bnd + (warp - 1) * bstride
+                          : has_src ? a.bnd + par * pstride + (band - 1) * bstride
+                                    : a.bnd;                                                 // read (lane 0)
+    double* sb_out = dst_sh ? sh_bnd + warp * bstride
+                            : a.bnd + par * pstride + (has_dst ? band : 0) * bstride;        // written (lane 31)
+    if (has_src && !src_sh) {  // reset the input slots of the other parity for the next launch
         double* rs = a.bnd + (par ^ 1) * pstride + (band - 1) * bstride;
         for (size_t k = lane; k < bstride; k += 32) rs[k] = __longlong_as_double(static_cast<long long>(kSent));
     }
@@ -366,9 +384,12 @@ __global__ void __launch_bounds__(32, 1) k_gs_wave(WaveArgs a) {
 }
 
 template <int KIND>
-size_t wave_smem_bytes() {
-    return static_cast<size_t>(kWaveDepth) * WaveShape<KIND>::F * WaveShape<KIND>::KU * 32 * sizeof(double) +
-           kWaveDepth * sizeof(uint64_t);
+size_t wave_smem_bytes(int w, int bcols) {
+    const size_t nbf = KIND == 1 ? 1 : 2;
+    return static_cast<size_t>(w) * (static_cast<size_t>(kWaveDepth) * WaveShape<KIND>::F * WaveShape<KIND>::KU * 32 *
+                                         sizeof(double) +
+                                     kWaveDepth * sizeof(uint64_t)) +
+           static_cast<size_t>(w - 1) * nbf * bcols * sizeof(double);
 }
 
 }  // namespace
@@ -486,12 +507,24 @@ bool GsPlan::build_wave(const HostCsr& a, const std::vector<int>& comps, const s
     wave_ny = ny;
     wave_bands = nb;
     wave_blocks = nblocks;
-    wave_smem = kind == 1 ? wave_smem_bytes<1>() : wave_smem_bytes<2>();
+    // warps (bands) per CTA: as many as shared memory holds, at most one per
+    // SM sub-partition; the MAC ring is 80 KB per band (SDG_WAVE_W overrides)
+    {
+        const int bc = kind == 1 ? nx : nx + 1;
+        constexpr size_t kSmemMax = 226 * 1024;  // 227 KB per CTA minus the static words
+        int w = kind == 1 ? 4 : 2;
+        if (const char* e = std::getenv("SDG_WAVE_W")) w = std::max(1, std::min(w, std::atoi(e)));
+        while (w > 1 && (kind == 1 ? wave_smem_bytes<1>(w, bc) : wave_smem_bytes<2>(w, bc)) > kSmemMax) w /= 2;
+        w = std::min(w, nb >= 4 ? 4 : nb >= 2 ? 2 : 1);
+        wave_w = w;
+        wave_smem = kind == 1 ? wave_smem_bytes<1>(w, bc) : wave_smem_bytes<2>(w, bc);
+    }
     walk = false;
     usable = true;
     if (std::getenv("SDG_DEBUG"))
-        std::fprintf(stderr, "[sdg] gs wave: kind %d, %d x %d grid, %d bands, %d blocks of %d steps, %zu B smem\n",
-                     kind, nx, ny, nb, nblocks, KU, wave_smem);
+        std::fprintf(stderr,
+                     "[sdg] gs wave: kind %d, %d x %d grid, %d bands (%d per CTA), %d blocks of %d steps, %zu B smem\n",
+                     kind, nx, ny, nb, wave_w, nblocks, KU, wave_smem);
     return true;
 }
 
@@ -525,22 +558,21 @@ void launch_gs_wave(Context& c, const GsPlan& g, double* z_new) {
     WaveArgs a{g.packed.get(), z_new, g.wave_bnd.get(), g.wave_ticket.get(), g.wave_bands, g.wave_blocks,
                g.wave_nx, g.wave_ny, g.wave_kind == 2 ? g.wave_nx * (g.wave_nx + 1) : 0,
                g.wave_kind == 1 ? g.wave_nx : g.wave_nx + 1, wave_timeline(g.wave_bands)};
+    const int ctas = (g.wave_bands + g.wave_w - 1) / g.wave_w;
+    static const bool attr = [] {  // every instantiation may use the whole shared memory of an SM
+        for (auto k : {k_gs_wave<1, 1>, k_gs_wave<1, 2>, k_gs_wave<1, 4>, k_gs_wave<2, 1>, k_gs_wave<2, 2>})
+            SDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+        return true;
+    }();
+    (void)attr;
+    auto go = [&](void (*kernel)(WaveArgs)) { launch_k(c, kernel, ctas, 32 * g.wave_w, g.wave_smem, a); };
     if (g.wave_kind == 1) {
-        static const bool attr = [] {
-            SDG_CUDA(cudaFuncSetAttribute(k_gs_wave<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(wave_smem_bytes<1>())));
-            return true;
-        }();
-        (void)attr;
-        launch_k(c, k_gs_wave<1>, g.wave_bands, 32, g.wave_smem, a);
+        if (g.wave_w == 4) go(k_gs_wave<1, 4>);
+        else if (g.wave_w == 2) go(k_gs_wave<1, 2>);
+        else go(k_gs_wave<1, 1>);
     } else {
-        static const bool attr = [] {
-            SDG_CUDA(cudaFuncSetAttribute(k_gs_wave<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(wave_smem_bytes<2>())));
-            return true;
-        }();
-        (void)attr;
-        launch_k(c, k_gs_wave<2>, g.wave_bands, 32, g.wave_smem, a);
+        if (g.wave_w == 2) go(k_gs_wave<2, 2>);
+        else go(k_gs_wave<2, 1>);
     }
 }
 

@@ -193,7 +193,15 @@ void Ilu0Precond::do_apply(const double* r, double* z) {
 AmgPrecond::AmgPrecond(CtxPtr c, const HostCsr& a, const AmgOpts& o) : Precond(std::move(c)) {
     auto t0 = std::chrono::steady_clock::now();
     Context& cx = *ctx_;
-    std::vector<HostLevel> hl = build_hierarchy(a, o);
+    // aggregation on the host (a sequential greedy pass), Galerkin products on the device
+    const char* ge = std::getenv("SDG_GALERKIN");
+    const bool host_product = ge && ge[0] == 'h';
+    std::vector<HostLevel> hl = build_hierarchy(
+        a, o,
+        host_product ? GalerkinFn{}
+                     : GalerkinFn{[&cx](const HostCsr& m, const std::vector<int>& agg, int nc) {
+                           return galerkin_device(cx, m, agg, nc);
+                       }});
     n_rows_ = a.n_rows;
     const char* ex = std::getenv("SDG_GS_EXACT");
     exact_ = ex && ex[0] == '1';
@@ -220,6 +228,7 @@ AmgPrecond::AmgPrecond(CtxPtr c, const HostCsr& a, const AmgOpts& o) : Precond(s
             L.n_coarse = hl[l].n_coarse;
             L.zt.resize(A.n_rows);
             if (!exact_) {
+                L.gs.tune = &cx;
                 L.gs.build(A, hl[l].components, cx.stream, 0, /*allow_merge=*/true);
                 L.fast = L.gs.usable;
             }

@@ -216,7 +216,7 @@ HostCsr galerkin(const HostCsr& a, const std::vector<int>& agg, int n_coarse) {
     return c;
 }
 
-std::vector<HostLevel> build_hierarchy(const HostCsr& a, const AmgOpts& o) {
+std::vector<HostLevel> build_hierarchy(const HostCsr& a, const AmgOpts& o, const GalerkinFn& product) {
     if (a.n_rows != a.n_cols) fail(SDG_EDIM, "amg_setup: matrix must be square");
     if (!o.components.empty() && static_cast<int>(o.components.size()) != a.n_rows)
         fail(SDG_EDIM, "amg_setup: component label length mismatch");
@@ -228,7 +228,7 @@ std::vector<HostLevel> build_hierarchy(const HostCsr& a, const AmgOpts& o) {
         int n_coarse = 0;
         std::vector<int> agg = aggregate(levels.back().a, o.theta, labels, n_coarse);
         if (n_coarse >= levels.back().a.n_rows) break;  // no coarsening progress
-        HostCsr coarse = galerkin(levels.back().a, agg, n_coarse);
+        HostCsr coarse = product ? product(levels.back().a, agg, n_coarse) : galerkin(levels.back().a, agg, n_coarse);
         if (!labels.empty()) {
             std::vector<int> coarse_labels(n_coarse, 0);
             for (int i = 0; i < levels.back().a.n_rows; ++i) coarse_labels[agg[i]] = labels[i];

@@ -4,6 +4,7 @@
 // (setup stays host, consumed by the GPU).
 #pragma once
 
+#include <functional>
 #include <vector>
 
 #include "common.hpp"
@@ -34,7 +35,10 @@ struct HostLevel {
 
 // amg_setup (precond.cpp:189-217) without the coarse factorization, which
 // the device performs (dense LU -> explicit inverse, see precond.cu).
-std::vector<HostLevel> build_hierarchy(const HostCsr& a, const AmgOpts& o);
+// `product` computes each Galerkin product (default: the host galerkin below;
+// the device preconditioners pass galerkin_device, galerkin.cu).
+using GalerkinFn = std::function<HostCsr(const HostCsr&, const std::vector<int>&, int)>;
+std::vector<HostLevel> build_hierarchy(const HostCsr& a, const AmgOpts& o, const GalerkinFn& product = {});
 
 // Restatement of the greedy aggregation (precond.cpp:122-175).
 std::vector<int> aggregate(const HostCsr& a, double theta, const std::vector<int>& comps,
@@ -42,6 +46,9 @@ std::vector<int> aggregate(const HostCsr& a, double theta, const std::vector<int
 // Restatement of galerkin_product (precond.cpp:177-185), bitwise identical:
 // duplicates summed in COO insertion order.
 HostCsr galerkin(const HostCsr& a, const std::vector<int>& agg, int n_coarse);
+// The same product on the device (galerkin.cu), bitwise equal; returns the host copy.
+struct Context;
+HostCsr galerkin_device(Context& cx, const HostCsr& a, const std::vector<int>& agg, int n_coarse);
 
 // Level schedule of the strict lower triangle: rows grouped by dependency
 // depth so that one level's rows can be relaxed concurrently while the

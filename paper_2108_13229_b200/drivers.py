@@ -49,10 +49,14 @@ class TransientDriver:
     system: Optional[sdc.CoupledSystem] = None
     history: List[StepResult] = field(default_factory=list)
     max_breakdown_restarts: int = 3
+    # checker aid (tests, scripts/ref_spread_c4.py): every step's right-hand side is multiplied
+    # element-wise by (1 + 2^-52 u), u ~ U(-1, 1) from this seed -- a rounding-level change of the input
+    rhs_perturbation_seed: Optional[int] = None
 
     def __post_init__(self):
         if not math.isfinite(self.cfg.dt):
             raise ValueError("TransientDriver: the config is stationary (dt = inf)")
+        self._rng = None if self.rhs_perturbation_seed is None else np.random.default_rng(self.rhs_perturbation_seed)
         self.ctx = self.ctx or sdc.default_context()
         self.ctrl = self.ctrl or (sdc.RestartController.fixed(50) if self.cfg.solver == "gmres50"
                                   else sdc.RestartController.defaults())
@@ -63,6 +67,8 @@ class TransientDriver:
         v_prev = None if self.x is None else self.x[: self.system.n_vel]
         s = scenarios.build_system(self.cfg, t=t, v_prev=v_prev)
         t_asm = time.perf_counter() - t0
+        if self._rng is not None:
+            s.rhs = s.rhs * (1.0 + np.ldexp(self._rng.uniform(-1.0, 1.0, s.rhs.size), -52))
         if self.precond is None:
             self.precond = sdc.TdPreconditioner(s, "td_bgs", self.cfg.v_max_levels, self.cfg.d_max_levels,
                                                 ctx=self.ctx)

@@ -135,6 +135,7 @@ def lib():
         p("sdg_ilu0_create", _i, [_vp, P(_vp)])
         p("sdg_ground_dof_host", _i, [_i, _ip, _ip, _dp, _i])
         p("sdg_gs_merged_sweep_host", _i, [_i, _ip, _ip, _dp, _i, _i, _dp, _vp, _dp, P(_i)])
+        p("sdg_galerkin_device", _i, [_vp, _i, _ip, _ip, _dp, _ip, _i, _vp, _vp, _vp, P(_i64)])
         p("sdg_lu_factor", _i, [_vp, _i, _ip, _ip, _dp, P(_vp)])
         p("sdg_lu_solve", _i, [_vp, _dp, _dp])
         p("sdg_lu_info", _i, [_vp, P(_i), P(_i), P(_i64)])
@@ -412,6 +413,23 @@ def gs_merged_sweep_host(a: SparseMatrix, r, k: int, dyn_cap: int = 0, z_old=Non
     _check(lib().sdg_gs_merged_sweep_host(a.n_rows, a.row_offsets, a.col_indices, a.values, int(k), int(dyn_cap), r,
                                           None if zo is None else zo.ctypes.data, z, C.byref(g)))
     return z, g.value
+
+
+def galerkin_product_device(a: SparseMatrix, aggregate_of, n_coarse: int, ctx: Optional[Context] = None) -> SparseMatrix:
+    """galerkin_product (precond.cpp:177-185) on the GPU: A_c = P^T A P of an
+    aggregation, bitwise the reference's sum order (csrc/galerkin.cu)."""
+    ctx = ctx or default_context()
+    agg = _i32(aggregate_of)
+    if agg.size != a.n_rows:
+        raise ValueError("galerkin_product: aggregate map length mismatch")
+    rp = np.empty(n_coarse + 1, np.int32)
+    ci = np.empty(max(a.nnz(), 1), np.int32)
+    vv = np.empty(max(a.nnz(), 1), np.float64)
+    nnz = _i64()
+    _check(lib().sdg_galerkin_device(ctx.h, a.n_rows, a.row_offsets, a.col_indices,
+                                     a.values if a.values.size else np.zeros(1), agg, int(n_coarse),
+                                     rp.ctypes.data, ci.ctypes.data, vv.ctypes.data, C.byref(nnz)))
+    return SparseMatrix(n_coarse, n_coarse, rp, ci[:nnz.value].copy(), vv[:nnz.value].copy())
 
 
 class LUFactorization:

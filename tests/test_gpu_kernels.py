@@ -509,3 +509,28 @@ def test_forced_nd_singular_block_falls_back_to_dense(monkeypatch):
     f = sdc.lu_factor(sdc.SparseMatrix.from_dense(d))
     b = np.arange(1.0, n + 1)
     assert np.allclose(d @ f.solve(b), b, atol=1e-9)
+
+
+@pytest.mark.parametrize("cfg_name", ["c1", "c2"])
+def test_galerkin_device_bitwise(cfg_name):
+    """galerkin_product on the device (csrc/galerkin.cu) equals the host product
+    -- itself bitwise the reference's CooBuilder order (tests/test_host.py) --
+    on every level of both hierarchies, and the device AMG setup (which uses
+    it) builds the same hierarchy as the host-only setup."""
+    from paper_2108_13229_b200 import scenarios
+    cfg = scenarios.CONFIGS[cfg_name]
+    s = scenarios.build_system(cfg)
+    V = sdc.submatrix(s.matrix, 0, s.n_vel, 0, s.n_vel)
+    D = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
+    for m, o in ((V, sdc.AmgOptions(components=[0] * s.n_u + [1] * (s.n_vel - s.n_u), max_levels=cfg.v_max_levels)),
+                 (D, sdc.AmgOptions(max_levels=cfg.d_max_levels))):
+        h = sdc.host_hierarchy(m, o)
+        assert len(h) >= 2
+        for lev in range(len(h) - 1):
+            c = sdc.galerkin_product_device(h[lev].a, h[lev].aggregate_of, h[lev].n_coarse)
+            ref_c = h[lev + 1].a
+            assert np.array_equal(c.row_offsets, ref_c.row_offsets) and np.array_equal(c.col_indices, ref_c.col_indices)
+            assert bitwise_equal(c.values, ref_c.values)
+        amg = sdc.AmgPreconditioner(m, o)
+        assert [r for r, _ in amg.hierarchy()] == [lv.a.n_rows for lv in h]
+        assert [z for _, z in amg.hierarchy()] == [lv.a.nnz() for lv in h]

@@ -67,32 +67,60 @@ def test_transient_warm_start_matches_reference(ref, solver):
 
 def test_c4s_transient_within_reference_spread():
     """BASELINE config 4 at 250^2 (log-normal K, AMG L4, implicit Euler x10,
-    warm-started BiCGSTAB): per time step the GPU count lies inside the
-    reference's own spread (14 reference runs: -O2 and FMA builds, one-ulp
-    rhs perturbations; tests/golden/c4s_reference.json, made by
-    tests/golden/make_c4s_golden.py), and the solution matches the
-    reference's step by step through size-independent fingerprints (||x||,
-    dot products with seeded random vectors, a strided sample) to 1e-6."""
+    warm-started BiCGSTAB) against the reference's own ensemble (-O2 and FMA
+    builds, right-hand sides perturbed by one ulp; tests/golden/c4s_reference.json,
+    made by tests/golden/make_c4s_golden.py from scripts/ref_spread_c4.py runs).
+
+    BiCGSTAB counts are rounding-chaotic: one-ulp input changes move the
+    reference itself between ~300 and ~10,000 iterations on one step, and the
+    count of step k also depends on how far step k-1 happened to over-converge.
+    So the GPU is sampled the same way (the unperturbed run plus four runs with
+    one-ulp rhs perturbations) and compared as a distribution:
+
+      * every single count lies in [0.95 min, 1.05 max] of the reference's
+        counts for that kind of solve (step 1: cold start; steps 2..10 pooled:
+        warm-started corrections);
+      * per step, the MEDIAN of the five GPU counts lies in [0.95 min, 1.05 max]
+        of the reference ensemble at that step;
+      * the median GPU total lies inside the ensemble's totals;
+      * the unperturbed run's solution matches the reference's step by step
+        through size-independent fingerprints (||x||, dot products with seeded
+        random vectors, a strided sample) to 1e-6."""
     with open(os.path.join(GOLDEN, "c4s_reference.json")) as f:
         g = json.load(f)
     cfg = scenarios.CONFIGS["c4s"]
-    drv = drivers.TransientDriver(cfg, warm_start=True)
     ens = g["ensemble"]
-    its = []
-    for k, ref_step in enumerate(g["steps"], 1):
-        st = drv.advance(k * cfg.dt)
-        assert st.converged, k
-        its.append(st.iterations)
-        assert within_spread(st.iterations, ens["min"][k - 1], ens["max"][k - 1]), (k, st.iterations, ens)
-        x = drv.x
-        xn = ref_step["x_norm"]
-        assert abs(np.linalg.norm(x) - xn) <= 1e-6 * xn, k
-        probes = np.random.default_rng(1000 + k).standard_normal((4, x.size))
-        for d_gpu, d_ref, pr in zip(probes @ x, ref_step["dots"], probes):
-            assert abs(d_gpu - d_ref) <= 1e-6 * xn * np.linalg.norm(pr), k
-        smp = np.asarray(ref_step["sample"])
-        assert np.linalg.norm(x[:: ref_step["sample_stride"]] - smp) <= 1e-6 * np.linalg.norm(smp), k
-    assert within_spread(sum(its), min(ens["totals"]), max(ens["totals"])), (its, ens["totals"])
+    cold = (ens["min"][0], ens["max"][0])
+    warm = (min(ens["min"][1:]), max(ens["max"][1:]))
+    runs, precond = [], None
+    for seed in (None, 0, 1, 2, 3):
+        drv = drivers.TransientDriver(cfg, warm_start=True, precond=precond, rhs_perturbation_seed=seed)
+        its = []
+        for k, ref_step in enumerate(g["steps"], 1):
+            st = drv.advance(k * cfg.dt)
+            assert st.converged, (seed, k)
+            its.append(st.iterations)
+            lo, hi = cold if k == 1 else warm
+            assert within_spread(st.iterations, lo, hi), (seed, k, st.iterations, lo, hi)
+            x = drv.x
+            xn = ref_step["x_norm"]
+            assert abs(np.linalg.norm(x) - xn) <= 1e-6 * xn, (seed, k)
+            if seed is not None:
+                continue
+            probes = np.random.default_rng(1000 + k).standard_normal((4, x.size))
+            for d_gpu, d_ref, pr in zip(probes @ x, ref_step["dots"], probes):
+                assert abs(d_gpu - d_ref) <= 1e-6 * xn * np.linalg.norm(pr), k
+            smp = np.asarray(ref_step["sample"])
+            assert np.linalg.norm(x[:: ref_step["sample_stride"]] - smp) <= 1e-6 * np.linalg.norm(smp), k
+        precond = drv.precond
+        runs.append(its)
+    runs = np.asarray(runs)
+    med = np.median(runs, axis=0)
+    for k in range(cfg.steps):
+        assert within_spread(med[k], ens["min"][k], ens["max"][k]), (k + 1, runs[:, k].tolist(), ens["min"][k],
+                                                                      ens["max"][k])
+    assert within_spread(float(np.median(runs.sum(axis=1))), min(ens["totals"]), max(ens["totals"])), (
+        runs.sum(axis=1).tolist(), ens["totals"])
 
 
 @pytest.mark.parametrize("n", [16, 50])
