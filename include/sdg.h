@@ -54,6 +54,12 @@ typedef struct sdg_precond sdg_precond;
 /* OR-ed into sdg_td_create's kind: ILU(0) instead of AMG on the grounded
  * porous block D' (the td_*_uzawa_ilu0 choices, bench.cpp:156-172) */
 #define SDG_TD_ILU0 16
+/* sdg_dist_td_create only: the two subdomain preconditioners of the partitioned
+ * Dirichlet-Neumann driver over strips (coupling.cpp:115-146): inexact
+ * Uzawa(AMG_V) on a Stokes system [V B; C 0] (n_ppm = 0), and AMG on a single
+ * matrix (n_vel = n_pff = 0, no grounding: the Dirichlet Darcy problem is regular) */
+#define SDG_DIST_UZAWA 32
+#define SDG_DIST_AMG 33
 
 /* RestartController (krylov.hpp:23-47). Updated in place by sdg_pd_gmres
  * only on the caller's copy semantics of the reference: the reference takes
@@ -416,8 +422,10 @@ int sdg_dist_system_destroy(sdg_dist_system* s);
 int sdg_dist_local_rows(const sdg_dist_system* s, int* n_local, int* global_ids);
 /* spmv (sparse.cpp:81-90) on the rank's rows; collective. */
 int sdg_dist_spmv(sdg_dist_system* s, const double* x_local, double* y_local);
-/* td_bj / td_bgs as sdg_td_create, over strips; collective.  The system
- * must outlive the preconditioner. */
+/* td_bj / td_bgs as sdg_td_create, over strips; or SDG_DIST_UZAWA /
+ * SDG_DIST_AMG for the subdomain solves of the partitioned driver (v_max_levels
+ * resp. d_max_levels set the AMG depth).  Collective.  The system must outlive
+ * the preconditioner. */
 int sdg_dist_td_create(sdg_dist_system* s, int kind, int v_max_levels, int d_max_levels, double omega_override,
                        sdg_dist_precond** out);
 int sdg_dist_precond_destroy(sdg_dist_precond* p);

@@ -29,7 +29,27 @@ void orc_spmv_add(const orc_csr* a, const double* x, double* y, double alpha) {
     }
 }
 
+/* Checker-side experiment knob (scripts/ref_dot_experiment.py), default 0 =
+ * the reference's sequential sum (sparse.cpp:208-212; every pin of this file
+ * runs in that mode).  Mode 1 sums pairwise (blocks of 128, then a binary
+ * tree), the error behaviour of a GPU tree reduction: it shows how far the
+ * reference's own BiCGSTAB iteration counts depend on the rounding error of
+ * its dot products. */
+static int g_dot_mode = 0;
+void orc_set_dot_mode(int mode) { g_dot_mode = mode; }
+
+static double dot_pairwise(int n, const double* x, const double* y) {
+    if (n <= 128) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += x[i] * y[i];
+        return s;
+    }
+    const int h = (n / 2 + 127) / 128 * 128;
+    return dot_pairwise(h, x, y) + dot_pairwise(n - h, x + h, y + h);
+}
+
 double orc_dot(int n, const double* x, const double* y) {
+    if (g_dot_mode == 1) return dot_pairwise(n, x, y);
     double s = 0.0;
     for (int i = 0; i < n; ++i) s += x[i] * y[i];
     return s;

@@ -28,6 +28,7 @@ void orc_spmv(const orc_csr* a, const double* x, double* y);
 /* sparse.cpp:98-108 */
 void orc_spmv_add(const orc_csr* a, const double* x, double* y, double alpha);
 /* sparse.cpp:208-222 */
+void orc_set_dot_mode(int mode);  /* experiment knob, see sdc_oracle.c */
 double orc_dot(int n, const double* x, const double* y);
 double orc_norm2(int n, const double* x);
 /* precond.cpp:92-108; returns the failing row or -1 */

@@ -647,31 +647,46 @@ void DistAmg::vcycle(int l, const double* r, double* z) {
 
 DistTd::DistTd(DistSystem& s, int kind, int v_levels, int d_levels, double omega_override) : s_(s), kind_(kind) {
     auto t0 = std::chrono::steady_clock::now();
-    if (kind != SDG_TD_BJ && kind != SDG_TD_BGS) fail(SDG_EINVAL, "dist td: kind must be td_bj or td_bgs");
+    if (kind != SDG_TD_BJ && kind != SDG_TD_BGS && kind != SDG_DIST_UZAWA && kind != SDG_DIST_AMG)
+        fail(SDG_EINVAL, "dist td: kind must be td_bj, td_bgs, SDG_DIST_UZAWA or SDG_DIST_AMG");
     Context& cx = *s.ctx;
     Transport& tr = *s.tr;
     const int rank = tr.rank;
     const HostCsr& A = s.global;
     const int n = A.n_rows, n_vel = s.n_vel, n_ff = s.n_vel + s.n_pff;
+    if (kind == SDG_DIST_AMG) {
+        // the porous subdomain solve of the partitioned driver (coupling.cpp:140-146):
+        // AMG on the matrix as it is
+        if (n_ff != 0) fail(SDG_EDIM, "dist amg: the system must be one block (n_vel = n_pff = 0)");
+        AmgOpts da;
+        da.max_levels = d_levels;
+        d_ = std::make_unique<DistAmg>(s.ctx, s.tr, A, s.own, da);
+        cx.sync();
+        setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return;
+    }
+    if (kind == SDG_DIST_UZAWA && s.n_ppm != 0) fail(SDG_EDIM, "dist uzawa: the system must have no porous block");
     // bench.cpp:121-182
     const HostCsr V = submatrix(A, 0, n_vel, 0, n_vel);
     const HostCsr B = submatrix(A, 0, n_vel, n_vel, n_ff);
     const HostCsr C = submatrix(A, n_vel, n_ff, 0, n_vel);
-    const HostCsr D = ground_dof(submatrix(A, n_ff, n, n_ff, n), 0);
     const Ownership Ov = s.own.slice(0, n_vel), Op = s.own.slice(n_vel, n_ff);
-    const Ownership Off = s.own.slice(0, n_ff), Opm = s.own.slice(n_ff, n);
     AmgOpts va;
     va.max_levels = v_levels;
     va.components.assign(n_vel, 0);
     for (int k = s.n_u; k < n_vel; ++k) va.components[k] = 1;
-    AmgOpts da;
-    da.max_levels = d_levels;
     v_ = std::make_unique<DistAmg>(s.ctx, s.tr, V, Ov, va);
-    d_ = std::make_unique<DistAmg>(s.ctx, s.tr, D, Opm, da);
     c_.build(cx, C, Op, Ov, rank);
     b_.build(cx, B, Ov, Op, rank);
-    if (kind_ == SDG_TD_BGS) cp_.build(cx, submatrix(A, n_ff, n, 0, n_ff), Opm, Off, rank);
-    tmp_.resize(std::max(s.n_ppm_loc, 1));
+    if (kind != SDG_DIST_UZAWA) {
+        const HostCsr D = ground_dof(submatrix(A, n_ff, n, n_ff, n), 0);
+        const Ownership Off = s.own.slice(0, n_ff), Opm = s.own.slice(n_ff, n);
+        AmgOpts da;
+        da.max_levels = d_levels;
+        d_ = std::make_unique<DistAmg>(s.ctx, s.tr, D, Opm, da);
+        if (kind_ == SDG_TD_BGS) cp_.build(cx, submatrix(A, n_ff, n, 0, n_ff), Opm, Off, rank);
+        tmp_.resize(std::max(s.n_ppm_loc, 1));
+    }
 
     if (!std::isnan(omega_override)) {
         omega_ = omega_override;
@@ -726,10 +741,15 @@ void DistTd::apply(const double* r, double* z) {
     Context& cx = *s_.ctx;
     Transport& tr = *s_.tr;
     ++apps_;
+    if (kind_ == SDG_DIST_AMG) {
+        d_->apply(r, z);
+        return;
+    }
     const int nv = s_.n_v_loc, nff = s_.n_v_loc + s_.n_pff_loc;
     v_->apply(r, z);                                              // z_v = Vtilde^{-1} r_v
     const double* zx = c_.load(cx, tr, z);
     launch_uzawa_pressure(cx, c_.a, zx, r + nv, omega_, z + nv);  // z_p = omega (C z_v - r_p)
+    if (kind_ == SDG_DIST_UZAWA) return;
     if (kind_ == SDG_TD_BGS) {                                    // precond.cpp:339-345
         cp_.apply_add(cx, tr, z, r + nff, tmp_.get(), -1.0);
         d_->apply(tmp_.get(), z + nff);

@@ -36,6 +36,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 
 namespace cg = cooperative_groups;
@@ -74,6 +76,20 @@ __global__ void k_gs_couple(int rows, int r0, const int* __restrict__ rp, const 
     row_fold<8>(ci, v, rp[i], rp[i + 1], [&](int j) { return z[j]; },
                 [&](double a, double x) { acc = fma(a, x, acc); });
     packed[bidx[r0 + i]] += acc;
+}
+
+// merged label block: b'_i = sum_q T_iq b_q (T: the group-local substitution of merge_levels,
+// unit diagonal), from the block's temporary b slots into the records of its walk
+__global__ void k_gs_tapply(int rows, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, const double* __restrict__ tmp,
+                            const int* __restrict__ pbidx, double* __restrict__ packed) {
+    pdl_begin();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    double acc = 0.0;
+    row_fold<8>(ci, v, rp[i], rp[i + 1], [&](int j) { return tmp[j]; },
+                [&](double a, double x) { acc = fma(a, x, acc); });
+    packed[pbidx[i]] = acc;
 }
 
 __global__ void k_gs_prep_post(int n, const int* __restrict__ urp, const int* __restrict__ uci,
@@ -406,7 +422,7 @@ int smem_budget() {
 // Exact in exact arithmetic (the same lexicographic Gauss-Seidel sweep,
 // precond.cpp:92-108); rounding differs like the rest of the fast smoother.
 struct MergedLower {
-    HostCsr g, w, wu;
+    HostCsr g, w, wu, t;
     std::vector<int> nlow;
     int max_k = 0;
     int groups = 0;
@@ -542,6 +558,7 @@ bool merge_levels(const HostCsr& a, const std::vector<double>& dinv, const HostC
         WU.rp[i + 1] = static_cast<int>(WU.ci.size());
     }
     out.g = std::move(G);
+    out.t = std::move(T);
     out.w = std::move(W);
     out.wu = std::move(WU);
     out.groups = ng;
@@ -662,6 +679,8 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
     // lattice, timed on the device at setup (build_parts; needs `tune`)
     const char* lat_env = knob("SDG_GS_LATTICE");
     lattice_mode_ = lat_env ? (lat_env[0] == '1' ? 1 : 0) : (tune ? 2 : 0);
+    // a forced plan shape (tests pin one: SDG_GS_SPLIT / _PIPE / _MERGE) keeps the plain walks it names
+    if (lattice_mode_ == 2 && (knob("SDG_GS_SPLIT") || knob("SDG_GS_PIPE") || knob("SDG_GS_MERGE"))) lattice_mode_ = 0;
     lattice_off_ = lattice_mode_ != 1;
     if (want_walk && !lattice_off_ && !force_split && !try_pipe && !knob("SDG_GS_MERGE") &&
         build_lattice(a, dinv_h, s))
@@ -1019,14 +1038,25 @@ void GsPlan::build(const HostCsr& a, const std::vector<int>& comps, cudaStream_t
 
 // mean device time (ms) of one lower solve of a stand-alone plan (its own records)
 static double time_lower(Context& c, const GsPlan& g) {
-    DevBuf<double> z(std::max(g.n, 1));
+    DevBuf<double> z(std::max(g.n, 1)), tmp;
+    if (g.merged_part) {  // stand-alone: b' = T b from a zero scratch into the plan's own records
+        tmp.resize(std::max(g.n, 1));
+        SDG_CUDA(cudaMemsetAsync(tmp.get(), 0, sizeof(double) * std::max(g.n, 1), c.stream));
+    }
+    auto sweep = [&]() {
+        if (g.merged_part)
+            launch_k(c, k_gs_tapply, (g.n + 255) / 256, 256, 0, g.n, g.tmat.rp.get(), g.tmat.ci.get(), g.tmat.v.get(),
+                     static_cast<const double*>(tmp.get()), static_cast<const int*>(g.bidx.get()),
+                     const_cast<double*>(g.packed.get()));
+        launch_gs_lower(c, g, z.get());
+    };
     cudaEvent_t e0, e1;
     SDG_CUDA(cudaEventCreate(&e0));
     SDG_CUDA(cudaEventCreate(&e1));
-    for (int r = 0; r < 2; ++r) launch_gs_lower(c, g, z.get());
+    for (int r = 0; r < 2; ++r) sweep();
     constexpr int kReps = 6;
     SDG_CUDA(cudaEventRecord(e0, c.stream));
-    for (int r = 0; r < kReps; ++r) launch_gs_lower(c, g, z.get());
+    for (int r = 0; r < kReps; ++r) sweep();
     SDG_CUDA(cudaEventRecord(e1, c.stream));
     SDG_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -1059,15 +1089,69 @@ bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std
         }
         auto p = std::make_unique<GsPlan>();
         if (lattice_mode_ == 2 && tune) {
-            // measured choice: both plans sweep their own (zero) records a few times
+            // measured choice between the plain level walk, the multi-SM lattice and a walk over
+            // merged levels: every candidate sweeps its own (zero) records a few times
             if (!p->build_walk(sub, dsub, nlow, max_k, s)) return false;
-            auto q = std::make_unique<GsPlan>();
-            if (q->build_lattice(sub, dsub, s)) {
-                const double tw = time_lower(*tune, *p), tl = time_lower(*tune, *q);
-                if (std::getenv("SDG_DEBUG"))
-                    std::fprintf(stderr, "[sdg gs plan] label block %d (%d rows): walk %.1f us, lattice %.1f us\n", k, m,
-                                 tw * 1e3, tl * 1e3);
-                if (tl < 0.95 * tw) p = std::move(q);
+            std::vector<std::unique_ptr<GsPlan>> cand;
+            std::vector<const char*> names;
+            {
+                auto q = std::make_unique<GsPlan>();
+                if (q->build_lattice(sub, dsub, s)) {
+                    cand.push_back(std::move(q));
+                    names.push_back("lattice");
+                }
+            }
+            const char* pm_env = std::getenv("SDG_GS_PART_MERGE");
+            if (!(pm_env && pm_env[0] == '0')) {
+                HostCsr upsub(m, m);  // the block's own upper part: only T and G of the merge are used
+                const std::pair<int, int> kc[4] = {{4, 8}, {2, 0}, {3, 0}, {4, 0}};  // (levels, dynamic entry cap)
+                static const char* const kc_names[4] = {"merged walk (<= 4 levels, <= 8 entries)", "merged walk (2 levels)",
+                                                        "merged walk (3 levels)", "merged walk (4 levels)"};
+                for (int ic = 0; ic < 4; ++ic) {
+                    const auto& c = kc[ic];
+                    MergedLower ml;
+                    if (!merge_levels(sub, dsub, upsub, c.first, 16, ml, c.second)) continue;
+                    auto q = std::make_unique<GsPlan>();
+                    const std::vector<double> ones(m, 1.0);
+                    if (!q->build_walk(ml.g, ones, ml.nlow, ml.max_k, s)) continue;
+                    q->merged_part = true;
+                    q->merge_k = c.first;
+                    q->tmat.upload(ml.t, s);
+                    cand.push_back(std::move(q));
+                    names.push_back(kc_names[ic]);
+                }
+            }
+            if (!cand.empty()) {
+                // the first decision for a block of this shape holds for the process: two
+                // preconditioners of one system must run the same plan (their applies are
+                // compared bit for bit), whatever the timer says the second time
+                static std::mutex mu;
+                static std::map<std::tuple<int, int64_t, int>, int> decided;
+                const auto key = std::make_tuple(m, sub.nnz(), k);
+                int choice = -2;  // -1: the plain walk, >= 0: cand[choice]
+                {
+                    std::lock_guard<std::mutex> g(mu);
+                    auto it = decided.find(key);
+                    if (it != decided.end()) choice = it->second;
+                }
+                if (choice == -2) {
+                    const double tw = time_lower(*tune, *p);
+                    double best = 0.9 * tw;  // an alternative must win by 10 %
+                    choice = -1;
+                    for (size_t q = 0; q < cand.size(); ++q) {
+                        const double tq = time_lower(*tune, *cand[q]);
+                        if (std::getenv("SDG_DEBUG"))
+                            std::fprintf(stderr, "[sdg gs plan] label block %d (%d rows): walk %.1f us, %s %.1f us\n", k, m,
+                                         tw * 1e3, names[q], tq * 1e3);
+                        if (tq < best) {
+                            best = tq;
+                            choice = static_cast<int>(q);
+                        }
+                    }
+                    std::lock_guard<std::mutex> g(mu);
+                    decided.emplace(key, choice);
+                }
+                if (choice >= 0 && choice < static_cast<int>(cand.size())) p = std::move(cand[choice]);
             }
         } else if (!(lattice_mode_ == 1 && p->build_lattice(sub, dsub, s)) &&
                    !p->build_walk(sub, dsub, nlow, max_k, s)) {
@@ -1081,8 +1165,14 @@ bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std
     for (int k = 0; k < nparts; ++k) {
         off[k] = total;
         total += (ps[k]->packed.size() + 31) / 32 * 32;  // 256-byte aligned parts: TMA sources
+        if (ps[k]->merged_part) {  // the plain b of a merged block lands in a temporary region first
+            ps[k]->part_tmp_off = total;
+            total += (static_cast<size_t>(ps[k]->n) + 31) / 32 * 32;
+        }
     }
+    if (total > static_cast<size_t>(INT32_MAX)) return false;  // bidx is int
     packed.resize(total);
+    SDG_CUDA(cudaMemsetAsync(packed.get(), 0, total * sizeof(double), s));
     std::vector<int> bidx_h(n);
     for (int k = 0; k < nparts; ++k) {
         GsPlan& p = *ps[k];
@@ -1091,7 +1181,16 @@ bool GsPlan::build_parts(const HostCsr& a, const std::vector<int>& r0, const std
         std::vector<int> lb(p.n);
         SDG_CUDA(cudaMemcpyAsync(lb.data(), p.bidx.get(), p.n * sizeof(int), cudaMemcpyDeviceToHost, s));
         SDG_CUDA(cudaStreamSynchronize(s));
-        for (int i = 0; i < p.n; ++i) bidx_h[r0[k] + i] = static_cast<int>(off[k]) + lb[i];
+        if (p.merged_part) {
+            for (int i = 0; i < p.n; ++i) {
+                bidx_h[r0[k] + i] = static_cast<int>(p.part_tmp_off) + i;
+                lb[i] += static_cast<int>(off[k]);
+            }
+            p.part_bidx.upload(lb, s);
+            SDG_CUDA(cudaStreamSynchronize(s));
+        } else {
+            for (int i = 0; i < p.n; ++i) bidx_h[r0[k] + i] = static_cast<int>(off[k]) + lb[i];
+        }
         p.part_doubles = p.packed.size();
         p.packed.release();
         p.bidx.release();
@@ -1374,7 +1473,15 @@ void launch_gs_lower(Context& c, const GsPlan& g, double* z_new, cudaEvent_t mar
                     const_cast<double*>(g.packed.get()));
                 SDG_GS_CHECK();
             }
-            launch_gs_lower(c, *g.parts[k], z_new + g.part_r0[k], k + 1 == g.parts.size() ? mark : nullptr);
+            const GsPlan& part = *g.parts[k];
+            if (part.merged_part) {
+                ProfScope ps_(c, PF_GSPREP, 12.0 * part.tmat.nnz + 4.0 * (part.n + 1) + 16.0 * part.n);
+                launch_k(c, k_gs_tapply, (part.n + 255) / 256, 256, 0, part.n, part.tmat.rp.get(), part.tmat.ci.get(),
+                         part.tmat.v.get(), g.packed.get() + part.part_tmp_off,
+                         static_cast<const int*>(part.part_bidx.get()), const_cast<double*>(g.packed.get()));
+                SDG_GS_CHECK();
+            }
+            launch_gs_lower(c, part, z_new + g.part_r0[k], k + 1 == g.parts.size() ? mark : nullptr);
         }
         return;
     }

@@ -115,6 +115,14 @@ struct GsPlan {
     bool merged = false;
     int merge_k = 1;
     DevCsr wmat, wumat;
+    // a label block walked over merged levels (build_parts): the parent's prep / coupling steps
+    // write the plain b = (r - U z_old - L_prev z_new) / d into a temporary region of the parent's
+    // buffer (part_tmp_off), k_gs_tapply turns it into the group-local combination b' = T b
+    // inside the walk's records (through part_bidx), then the walk over the merged rows runs
+    bool merged_part = false;
+    DevCsr tmat;
+    DevBuf<int> part_bidx;       // local row -> slot of b' in the parent's buffer
+    size_t part_tmp_off = 0;     // first temporary slot in the parent's buffer (local row i -> + i)
     const double* packed_ptr = nullptr;  // records of a part inside its parent's buffer
     size_t part_doubles = 0;             // size of a part's records
 

@@ -226,7 +226,10 @@ class DistTdPreconditioner:
     def __init__(self, ds: DistSystem, kind: str = "td_bgs", v_max_levels: int = 3, d_max_levels: int = 3,
                  omega: Optional[float] = None):
         self.ds = ds
-        k = {"td_bj": int(sdc.BlockPrecondKind.td_bj), "td_bgs": int(sdc.BlockPrecondKind.td_bgs)}[kind]
+        # "uzawa" / "amg": the subdomain preconditioners of the partitioned driver
+        # (SDG_DIST_UZAWA on a Stokes system with n_ppm = 0, SDG_DIST_AMG on a single matrix)
+        k = {"td_bj": int(sdc.BlockPrecondKind.td_bj), "td_bgs": int(sdc.BlockPrecondKind.td_bgs), "uzawa": 32,
+             "amg": 33}[kind]
         self.h = _vp()
         _check(_lib().sdg_dist_td_create(ds.h, k, v_max_levels, d_max_levels,
                                          float("nan") if omega is None else float(omega), C.byref(self.h)))

@@ -256,3 +256,115 @@ class PartitionedDriver:
         out.seconds = time.perf_counter() - t0
         out.solve_seconds = solve_s
         return out
+
+
+@dataclass
+class ShardedPartitionedDriver(PartitionedDriver):
+    """BASELINE config 5 with the two subdomain solves sharded over horizontal
+    strips (one rank per GPU): PD-GMRES + inexact Uzawa(AMG_V) on the Stokes
+    box and BiCGSTAB + AMG on the Darcy box through the ``sdg_dist_*`` entry
+    points (``SDG_DIST_UZAWA`` / ``SDG_DIST_AMG``).  The coupling loop, the
+    traces and IQN-ILS stay on the host and are replicated: rank 0 owns both
+    strips at the interface (``strip_partition``), so it evaluates the traces
+    (assembly.cpp:382-402 read only cells next to the interface) and
+    broadcasts them; every rank then takes the same decisions.  The interface
+    data change only right-hand-side rows that rank 0 owns.
+
+    ``transport``: a :class:`paper_2108_13229_b200.dist.Transport`.
+    ``solution`` of the result is this rank's rows of [x_ff | p_pm]
+    (``local_rows()`` gives their global ids)."""
+
+    transport: Optional[object] = None
+
+    def __post_init__(self):
+        from . import dist as sd
+        import torch.distributed as td
+        if self.transport is None:
+            raise ValueError("ShardedPartitionedDriver: a transport is required")
+        self._td = td
+        self.ctx = self.ctx or sdc.default_context()
+        n = self.cfg.cells_per_unit_square
+        self.n = n
+        self.mu = self.cfg.kinematic_viscosity * self.cfg.density
+        z = np.zeros(n)
+        self.stokes_matrix, self.stokes_rhs0 = sdc.assemble_stokes(self.cfg, z)
+        self.darcy_matrix, _ = sdc.assemble_darcy(self.cfg, z)
+        self.t2 = 2.0 * (self.cfg.permeability / self.mu)
+        n_u = n * (n + 1)
+        n_vel, n_p = 2 * n_u, n * n
+        owner = sd.strip_partition(n, self.transport.size)
+        if self.transport.size > 1 and n // self.transport.size < 2:
+            raise ValueError("ShardedPartitionedDriver: strips need at least two cell rows")
+        ff = sdc.CoupledSystem(self.stokes_matrix, self.stokes_rhs0, n, n_u, n_vel, n_p, 0)
+        pm = sdc.CoupledSystem(self.darcy_matrix, np.zeros(n_p), n, 0, 0, 0, n_p)
+        self.ds_ff = sd.DistSystem(ff, self.transport, owner=owner[: n_vel + n_p], ctx=self.ctx)
+        self.ds_pm = sd.DistSystem(pm, self.transport, owner=owner[n_vel + n_p:], ctx=self.ctx)
+        self.stokes_pre = sd.DistTdPreconditioner(self.ds_ff, "uzawa", v_max_levels=self.levels)
+        self.darcy_pre = sd.DistTdPreconditioner(self.ds_pm, "amg", d_max_levels=self.levels)
+        self.trace_v = np.zeros(n)
+        self.trace_p = np.zeros(n)
+
+    def local_rows(self):
+        """Global ids (in [x_ff | p_pm]) of this rank's entries of ``solution``."""
+        return np.concatenate([self.ds_ff.rows, self.stokes_matrix.n_rows + self.ds_pm.rows])
+
+    def _norm(self, v_local) -> float:
+        """Global 2-norm of a distributed vector (partials folded in rank order on every rank)."""
+        import torch
+        part = torch.tensor([float(np.dot(v_local, v_local))], dtype=torch.float64)
+        parts = [torch.zeros(1, dtype=torch.float64) for _ in range(self.transport.size)]
+        self._gather(parts, part)
+        return float(np.sqrt(sum(float(p[0]) for p in parts)))
+
+    def _gather(self, outs, t):
+        td = self._td
+        if td.get_backend() == "nccl":
+            import torch
+            dev = torch.device("cuda", torch.cuda.current_device())
+            o = [x.to(dev) for x in outs]
+            td.all_gather(o, t.to(dev))
+            for a, b in zip(outs, o):
+                a.copy_(b.cpu())
+        else:
+            td.all_gather(outs, t)
+
+    def _bcast0(self, arr) -> np.ndarray:
+        """Rank 0's array on every rank."""
+        import torch
+        td = self._td
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64).copy())
+        if td.get_backend() == "nccl":
+            dev = torch.device("cuda", torch.cuda.current_device())
+            g = t.to(dev)
+            td.broadcast(g, src=0)
+            return g.cpu().numpy()
+        td.broadcast(t, src=0)
+        return t.numpy()
+
+    def _scatter_full(self, ds, x_local, n_total) -> np.ndarray:
+        full = np.zeros(n_total)
+        full[ds.rows] = x_local
+        return full
+
+    def solve_ff(self, v_gamma):
+        from . import dist as sd
+        b = self.ds_ff.local(self.stokes_rhs(v_gamma))
+        res = sd.dist_pd_gmres(self.ds_ff, self.stokes_pre, b, self.inner_tol_rel * self._norm(b), 400,
+                               sdc.RestartController.defaults())
+        if not res.report.converged:
+            raise RuntimeError(f"coupling: inner free-flow solve did not converge, final residual "
+                               f"{res.report.final_residual} after {res.report.iterations} iterations")
+        # the trace reads p_ff(i, 0), v(i, 0), v(i, 1): rank 0's strip
+        tr = sdc.stokes_pressure_trace(self.cfg, self._scatter_full(self.ds_ff, res.x, self.stokes_matrix.n_rows))
+        return res, self._bcast0(tr)
+
+    def solve_pm(self, p_gamma):
+        from . import dist as sd
+        b = self.ds_pm.local(self.darcy_rhs(p_gamma))
+        res = sd.dist_bicgstab(self.ds_pm, self.darcy_pre, b, self.inner_tol_rel * self._norm(b), 10000)
+        if not res.report.converged:
+            raise RuntimeError(f"coupling: inner porous solve did not converge, final residual "
+                               f"{res.report.final_residual} after {res.report.iterations} iterations")
+        tr = sdc.darcy_velocity_trace(self.cfg, self._scatter_full(self.ds_pm, res.x, self.darcy_matrix.n_rows),
+                                      p_gamma)
+        return res, self._bcast0(tr)

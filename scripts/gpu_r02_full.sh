@@ -1,8 +1,7 @@
-# full driver-style runs: our arm (with cpu_baseline) then the reference arm
+# driver-style runs at the driver's flags: our arm (with cpu_baseline), then the reference arm
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out/r02f
-( time timeout 1700 python bench.py --steps 20 --warmup 5 ) > gpurun_out/r02f/bench.json 2> gpurun_out/r02f/bench.err
-echo "ours rc=$?"
-( time timeout 1700 python bench.py --impl reference --steps 3 --warmup 1 ) > gpurun_out/r02f/ref.json 2> gpurun_out/r02f/ref.err
-echo "ref rc=$?"
-tail -3 gpurun_out/r02f/*.err
+O=gpurun_out/full; mkdir -p $O
+( time timeout 1750 python bench.py --gpus 1 --steps 20 --warmup 5 ) > $O/bench.json 2> $O/bench.err; echo "ours rc=$?"
+( time timeout 1750 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 ) > $O/ref.json 2> $O/ref.err; echo "ref rc=$?"
+tail -4 $O/bench.err $O/ref.err
+head -c 300 $O/bench.json; echo; head -c 600 $O/ref.json

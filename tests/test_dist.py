@@ -254,3 +254,50 @@ def test_two_strips_warm_started_step_matches_single_gpu():
         x[out[r]["rows"]] = out[r]["x"]
         assert out[r]["conv"] and out[r]["it"][1] < out[r]["it"][0]
     assert np.linalg.norm(x - drv.x) / np.linalg.norm(drv.x) <= 1e-6
+
+
+def _dn_worker(rank, world, port, n, k, out):
+    _init(rank, world, port)
+    try:
+        from paper_2108_13229_b200 import dist as sd
+        from paper_2108_13229_b200 import drivers, sdc
+        cfg = sdc.ScenarioConfig(cells_per_unit_square=n, permeability=k, alpha_bj=1.0, kinematic_viscosity=1.0,
+                                 density=1.0, dt=float("inf"), t_end=1.0, dp_max=1.0)
+        ctx = sdc.Context(0)
+        drv = drivers.ShardedPartitionedDriver(cfg, ctx=ctx, transport=sd.CallbackTransport())
+        res = drv.coupled_step()
+        out[rank] = dict(rows=drv.local_rows(), x=res.solution, its=res.coupling_iterations, conv=res.converged,
+                         trace_p=drv.trace_p.copy(), trace_v=drv.trace_v.copy(),
+                         inner=(list(res.stokes_iterations), list(res.darcy_iterations)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,k", [(16, 1e-2), (50, 1.0)])
+def test_two_strips_partitioned_driver_matches_single_gpu(n, k):
+    """BASELINE config 5 with the subdomain solves sharded over 2 strips
+    (SDG_DIST_UZAWA / SDG_DIST_AMG, drivers.ShardedPartitionedDriver): the
+    coupling loop converges in the single-GPU driver's number of coupling
+    iterations (+-5 %; that driver is pinned against the loop composed from
+    the reference's pieces in tests/test_gpu_partitioned.py) to the same
+    solution and interface traces (1e-6); both ranks take the same decisions."""
+    from paper_2108_13229_b200 import drivers, sdc
+    world = 2
+    out = mp.Manager().dict()
+    mp.spawn(_dn_worker, args=(world, _free_port(), n, k, out), nprocs=world, join=True)
+    cfg = sdc.ScenarioConfig(cells_per_unit_square=n, permeability=k, alpha_bj=1.0, kinematic_viscosity=1.0,
+                             density=1.0, dt=float("inf"), t_end=1.0, dp_max=1.0)
+    drv = drivers.PartitionedDriver(cfg)
+    ref = drv.coupled_step()
+    assert ref.converged
+    x = np.zeros_like(ref.solution)
+    for r in range(world):
+        assert out[r]["conv"]
+        assert out[r]["its"] == out[0]["its"] and out[r]["inner"] == out[0]["inner"]
+        x[out[r]["rows"]] = out[r]["x"]
+    assert abs(out[0]["its"] - ref.coupling_iterations) <= max(1, 0.05 * ref.coupling_iterations), (
+        out[0]["its"], ref.coupling_iterations)
+    assert np.linalg.norm(x - ref.solution) / np.linalg.norm(ref.solution) <= 1e-6
+    assert np.linalg.norm(out[0]["trace_p"] - drv.trace_p) <= 1e-6 * np.linalg.norm(drv.trace_p)
+    assert np.linalg.norm(out[0]["trace_v"] - drv.trace_v) <= 1e-6 * np.linalg.norm(drv.trace_v)

@@ -179,6 +179,33 @@ def test_wave_smoother_bitwise_vs_walks(monkeypatch, cfg_name):
         assert np.array_equal(zw[2], zw[0])
 
 
+@pytest.mark.parametrize("wave_w", ["1", "2", "4"])
+def test_wave_bands_per_cta_bitwise(monkeypatch, wave_w):
+    """The wavefront with 1, 2 or 4 bands per CTA (SDG_WAVE_W; the hand-off
+    between two bands of one CTA goes through shared memory, between CTAs
+    through L2) gives the same bits: velocity and porous V-cycles at c2
+    (6 bands) against the default plan."""
+    from paper_2108_13229_b200 import scenarios
+    cfg = scenarios.CONFIGS["c2"]
+    s = scenarios.build_system(cfg)
+    V = sdc.submatrix(s.matrix, 0, s.n_vel, 0, s.n_vel)
+    comps = [0] * s.n_u + [1] * (s.n_vel - s.n_u)
+    D = sdc.ground_dof(sdc.submatrix(s.matrix, s.n_vel + s.n_pff, s.n_total(), s.n_vel + s.n_pff, s.n_total()))
+    rng = np.random.default_rng(5)
+    for mat, opts in ((V, sdc.AmgOptions(components=comps, max_levels=cfg.v_max_levels)),
+                      (D, sdc.AmgOptions(max_levels=cfg.d_max_levels))):
+        r = rng.standard_normal(mat.n_rows)
+        monkeypatch.delenv("SDG_WAVE_W", raising=False)
+        base = sdc.AmgPreconditioner(mat, opts)
+        assert "wave_v" in base.features()
+        z0 = [base.apply(r), base.apply(r)]
+        del base
+        monkeypatch.setenv("SDG_WAVE_W", wave_w)
+        alt = sdc.AmgPreconditioner(mat, opts)
+        z1 = [alt.apply(r), alt.apply(r)]
+        assert np.array_equal(z0[0], z1[0]) and np.array_equal(z0[1], z1[1]) and np.array_equal(z0[0], z0[1])
+
+
 @pytest.mark.parametrize("cfg_name", ["c3"])
 def test_lattice_smoother_matches_walks(monkeypatch, cfg_name):
     """The multi-SM lattice lower solve (gs_lattice.cu, opt-in SDG_GS_LATTICE=1)
@@ -216,13 +243,17 @@ def test_lattice_smoother_matches_walks(monkeypatch, cfg_name):
         assert np.array_equal(zl[2], zl[0])
 
 
-@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3"])
-def test_lattice_kernel_bitwise_vs_emulation(cfg_name):
+@pytest.mark.parametrize("cfg_name,lat_w", [("c1", None), ("c2", None), ("c3", None), ("c3", "1"), ("c3", "3"),
+                                             ("c3", "4")])
+def test_lattice_kernel_bitwise_vs_emulation(monkeypatch, cfg_name, lat_w):
     """k_gs_lattice on the device equals its host emulation (same records,
     registers, windows, boundary buffer) bit for bit on every label block /
     level of the config that is a lattice, also when replayed (the boundary
-    buffer's parities)."""
+    buffer's parities), for every number of bands per CTA (SDG_LAT_W: the
+    hand-off inside a CTA goes through shared memory, between CTAs through L2)."""
     import ctypes as C
+    if lat_w is not None:
+        monkeypatch.setenv("SDG_LAT_W", lat_w)
     import scipy.sparse as sp
     from paper_2108_13229_b200 import scenarios
     cfg = scenarios.CONFIGS[cfg_name]
@@ -279,6 +310,30 @@ def test_c2_merge_and_interface_split_agree(monkeypatch):
     monkeypatch.setenv("SDG_GS_EXACT", "1")
     exact = sdc.AmgPreconditioner(D, sdc.AmgOptions(max_levels=cfg.d_max_levels))
     assert rel_l2(merged.apply(x), exact.apply(x)) < 1e-11
+
+
+@pytest.mark.parametrize("cfg_name", ["c2", "c2u"])
+def test_c2_td_bgs_apply_matches_reference(ref, cfg_name):
+    """The td_bgs apply at the c2 size against the compiled reference's own
+    apply on the same matrix (its amg_setup, lu_factor, power iteration): the
+    default GPU plan (wavefront, merged walks, interface split with early
+    correction, dense Gauss-Jordan coarse inverse) agrees to 1e-9, omega to
+    2e-3 (the power iteration stops at 1e-3)."""
+    from oracle.refpy import Csr, System
+    from paper_2108_13229_b200 import scenarios
+    cfg = scenarios.CONFIGS[cfg_name]
+    s = scenarios.build_system(cfg)
+    n = s.n_total()
+    rs = System(n, s.n_u, s.n_vel, s.n_pff, s.n_ppm,
+                Csr(n, n, s.matrix.row_offsets, s.matrix.col_indices, s.matrix.values), s.rhs)
+    rtd = ref.td(rs, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
+    # same omega on both sides: the apply is compared, not the eigenvalue estimate
+    p = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels, omega_override=rtd.omega)
+    assert abs(sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels).omega() - rtd.omega) <= \
+        2e-3 * abs(rtd.omega)
+    for seed in (17, 18):
+        r = ref.random_vector(n, seed)
+        assert rel_l2(p.apply(r), rtd.apply(r)) < 1e-9
 
 
 def test_c2_walk_roles_bitwise(monkeypatch):
