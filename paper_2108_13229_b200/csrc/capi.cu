@@ -131,6 +131,9 @@ extern "C" int sdg_debug_lattice_sweep(sdg_context* ctx, int n, const int* rowpt
         if (ctx && !sdg::lattice_run_device(*ctx->p, a, b, z_dev_out, repeats)) sdg::fail(SDG_EINVAL, "not a lattice");
     });
 }
+extern "C" int sdg_debug_wave_blocks(unsigned long long* out, int max_bands) {
+    return sdg::wave_blocks_copy(out, max_bands);
+}
 extern "C" int sdg_debug_wave_timeline(unsigned long long* out, int max_bands) {
     return sdg::wave_timeline_copy(out, max_bands);
 }

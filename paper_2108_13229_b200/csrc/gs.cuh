@@ -209,6 +209,7 @@ bool lattice_emulate_host(const HostCsr& a, const double* b, double* z);
 bool lattice_run_device(Context& c, const HostCsr& a, const double* b, double* z, int repeats);
 // dev aid (SDG_WAVE_TL=1): per band {start, first block, end, waiting ns} of the last wave launch
 int wave_timeline_copy(unsigned long long* out, int max_bands);
+int wave_blocks_copy(unsigned long long* out, int max_bands);
 // single-CTA variant (plans with walk == true; gs_walk.cu)
 void launch_gs_walk(Context& c, const GsPlan& g, double* z_new);
 // the two parts of a pipe on a 2-CTA cluster (gs_walk.cu)

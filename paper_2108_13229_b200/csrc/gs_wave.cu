@@ -113,9 +113,9 @@ __device__ __forceinline__ double ld_relaxed_if(const double* p, bool pred) {
     return v;
 }
 __device__ __forceinline__ void st_relaxed_if(double* p, double v, bool pred) {
-    // v + 0 quiets a signalling NaN, so a stored value is never the sentinel
-    // (and it equals v otherwise, up to the sign of a zero)
-    const double w = v + 0.0;
+    // every stored value is the result of an fma, which never returns a
+    // signalling NaN, so a stored value is never the sentinel
+    const double w = v;
     // no "memory" clobber: nothing this thread reads depends on the store, so
     // the compiler may keep scheduling the next step's shared loads across it
     asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.relaxed.gpu.f64 [%0], %1;\n}" ::"l"(p),
@@ -140,41 +140,116 @@ __device__ __forceinline__ void tma_block_if(double* dst, const double* src, uns
         : "memory");
 }
 
-// W warps per CTA, one band each (consecutive bands).  The hand-off between
-// two bands of one CTA goes through shared memory (the same value-as-flag
-// slots, filled with the sentinel at kernel start); only the first band of a
-// CTA polls the previous CTA's boundary in L2.  The loads and stores use
-// generic addresses, so one code path serves both.
+// non-blocking test of a ring slot's mbarrier, issued a few steps before the
+// slot is needed so that its latency hides behind the steps (test_wait, not
+// try_wait: try_wait may suspend the warp for microseconds when the phase is
+// not complete)
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok)
+                 : "r"(ptx::smem_addr(bar)), "r"(parity)
+                 : "memory");
+    return ok != 0;
+}
+
+// Boundary hand-off, round-2 form.  A band reads the top row of the band below
+// from an *inbound row* in its CTA's shared memory, one block of KU steps at a
+// time, just before the block starts (the values of a step: 5-point z(s, j-1);
+// MAC the pair {u(s, j-1), v(s-1, j-1)}, 16 bytes).  Who fills the inbound row:
+//   * the band below, directly (st.shared by its lane 31), when it is a warp
+//     of the same CTA;
+//   * otherwise the CTA's poller warp (warp W): the band below stores into the
+//     L2 boundary buffer (st.relaxed.gpu), the poller's lanes each spin on one
+//     slot of the current 32-slot window (ld.relaxed.gpu) and copy it into
+//     the inbound row the moment it stops being the sentinel.
+// Every slot, in L2 and in shared memory, is its own ready flag (kSent until
+// written), so there is no fence, flag or acquire anywhere; the compute warps
+// never wait on an L2 round trip, only on shared memory.  Slots past a row's
+// last column are never written and hold 0, so no load needs a bounds test.
+// A row has S = nblocks * KU slots (steps), NBF doubles each.
+__device__ __forceinline__ bool is_sent_hi(double v) {
+    // the sentinel's high word belongs to a NaN that arithmetic never produces
+    return static_cast<unsigned>(__double2hiint(v)) == static_cast<unsigned>(kSent >> 32);
+}
+// weak shared load the compiler may not cache or merge (shared memory has no
+// cache in front of it, so a weak load always sees the latest store)
+__device__ __forceinline__ double2 lds_v2(unsigned addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void st_pair_if(double* p, double x, double y, bool pred) {
+    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q st.relaxed.gpu.v2.f64 [%0], {%1, %2};\n}" ::"l"(p),
+                 "d"(x), "d"(y), "r"(static_cast<int>(pred)));
+}
+
+// W compute warps per CTA, one band each (consecutive bands), plus the poller.
 template <int KIND, int W>
-__global__ void __launch_bounds__(32 * W, 1) k_gs_wave(WaveArgs a) {
+__global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
     constexpr int F = WaveShape<KIND>::F, KU = WaveShape<KIND>::KU;
-    constexpr int NBF = KIND == 1 ? 1 : 2;  // boundary fields: z, or u and v
+    constexpr int NBF = KIND == 1 ? 1 : 2;  // doubles per boundary slot: z, or {u, v}
     constexpr int BLK = F * KU * 32;        // doubles per block
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ unsigned long long s_ticket;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* ring = reinterpret_cast<double*>(smem_raw) + warp * (kWaveDepth * BLK);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(smem_raw) + W * kWaveDepth * BLK) +
-                     warp * kWaveDepth;
-    const size_t bstride = static_cast<size_t>(NBF) * a.bcols;                 // one band boundary
-    // inbound boundaries of warps 1 .. W-1 (shared memory)
-    double* sh_bnd = reinterpret_cast<double*>(smem_raw) + W * kWaveDepth * BLK + W * kWaveDepth;
+    const int S = a.nblocks * KU;                              // steps = slots per boundary row
+    const size_t bstride = static_cast<size_t>(NBF) * S;       // doubles per boundary row
+    double* ring_all = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bars_all = reinterpret_cast<uint64_t*>(ring_all + W * kWaveDepth * BLK);
+    double* inb_all = reinterpret_cast<double*>(bars_all + W * kWaveDepth);  // [W][S][NBF], 16-byte aligned
     if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1ull);
-    if (lane == 0) {
+    if (warp < W && lane == 0) {
 #pragma unroll
-        for (int d = 0; d < kWaveDepth; ++d) ptx::mbar_init(bars + d, 1);
+        for (int d = 0; d < kWaveDepth; ++d) ptx::mbar_init(bars_all + warp * kWaveDepth + d, 1);
         ptx::fence_mbar_init();
     }
-    if (W > 1 && warp > 0) {
-        double* mine = sh_bnd + (warp - 1) * bstride;
-        for (size_t k = lane; k < bstride; k += 32) mine[k] = __longlong_as_double(static_cast<long long>(kSent));
+    // inbound rows: the sentinel where a value will arrive, 0 past the row's end
+    const int valid = a.bcols;  // slots that receive a value (5-point nx; MAC m + 1)
+    for (size_t k = threadIdx.x; k < static_cast<size_t>(W) * bstride; k += blockDim.x) {
+        const int slot = static_cast<int>((k % bstride) / NBF);
+        inb_all[k] = slot < valid ? __longlong_as_double(static_cast<long long>(kSent)) : 0.0;
     }
     __syncthreads();
     const unsigned long long t = s_ticket;
     const unsigned long long nctas = static_cast<unsigned long long>((a.nbands + W - 1) / W);
-    const int band = static_cast<int>(t % nctas) * W + warp;
+    const int band0 = static_cast<int>(t % nctas) * W;
     const int par = static_cast<int>((t / nctas) & 1ull);
+    const size_t pstride = static_cast<size_t>(a.nbands - 1) * bstride;  // one parity of the L2 buffer
+
+    if (warp == W) {  // ---- the poller
+        if (band0 == 0 || band0 >= a.nbands) return;
+        pdl_wait();  // the previous launch has read its parity; this launch may reset it
+        {   // reset this boundary's slots of the other parity for the next launch
+            double* rs = a.bnd + (par ^ 1) * pstride + static_cast<size_t>(band0 - 1) * bstride;
+            for (size_t k = lane; k < static_cast<size_t>(valid) * NBF; k += 32)
+                rs[k] = __longlong_as_double(static_cast<long long>(kSent));
+        }
+        const double* srcb = a.bnd + par * pstride + static_cast<size_t>(band0 - 1) * bstride;
+        double* dst = inb_all;  // inbound row of warp 0
+        const int nslots = valid * NBF;
+        for (int base = 0; base < nslots; base += 32) {
+            const int k = base + lane;
+            if (k < nslots) {
+                for (;;) {
+                    double v;
+                    asm volatile("ld.relaxed.gpu.f64 %0, [%1];" : "=d"(v) : "l"(srcb + k) : "memory");
+                    if (!is_sent_hi(v)) {
+                        asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(ptx::smem_addr(dst + k)), "d"(v)
+                                     : "memory");
+                        break;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    const int band = band0 + warp;
     if (band >= a.nbands) return;
+    double* ring = ring_all + warp * (kWaveDepth * BLK);
+    uint64_t* bars = bars_all + warp * kWaveDepth;
     pdl_wait();  // b is written by the prep kernel before this launch; the previous launch is done
     pdl_trigger();
     const double* src = a.rec + static_cast<size_t>(band) * a.nblocks * BLK;
@@ -182,73 +257,103 @@ __global__ void __launch_bounds__(32 * W, 1) k_gs_wave(WaveArgs a) {
         tma_block_if(ring + d * BLK, src + static_cast<size_t>(d) * BLK, BLK * 8, bars + d, lane == 0);
     const int j = band * 32 + lane;
     const bool has_src = band > 0, has_dst = band + 1 < a.nbands;
-    const bool src_sh = W > 1 && warp > 0, dst_sh = W > 1 && warp + 1 < W && has_dst;
-    unsigned long long wait_ns = 0, t_start = a.tl ? gtimer() : 0, t_first = 0, tma_cyc = 0, comp_cyc = 0;
-    const size_t pstride = static_cast<size_t>(a.nbands - 1) * bstride;         // one parity
-    const double* sb_in = src_sh    ? sh_bnd + (warp - 1) * bstride
-                          : has_src ? a.bnd + par * pstride + (band - 1) * bstride
-                                    : a.bnd;                                                 // read (lane 0)
-    double* sb_out = dst_sh ? sh_bnd + warp * bstride
-                            : a.bnd + par * pstride + (has_dst ? band : 0) * bstride;        // written (lane 31)
-    if (has_src && !src_sh) {  // reset the input slots of the other parity for the next launch
-        double* rs = a.bnd + (par ^ 1) * pstride + (band - 1) * bstride;
-        for (size_t k = lane; k < bstride; k += 32) rs[k] = __longlong_as_double(static_cast<long long>(kSent));
-    }
+    const bool dst_sh = warp + 1 < W && has_dst;
+    const double* inb = inb_all + warp * bstride;                                         // read (all lanes, same address)
+    double* sb_out = dst_sh ? inb_all + (warp + 1) * bstride
+                            : a.bnd + par * pstride + static_cast<size_t>(has_dst ? band : 0) * bstride;  // written (lane 31)
+    unsigned long long t_start = a.tl ? gtimer() : 0, t_first = 0, t_b4 = 0, t_b12 = 0;
+    long long wait_cyc = 0, comp_cyc = 0;
+    const bool pub = has_dst && lane == 31;
+
+    // the records of a step pair are loaded one pair ahead (R: this pair, Rn:
+    // the next one, across block boundaries too), so the shared-memory latency
+    // of the loads hides behind the previous pair's arithmetic
+    double2 R[F];
+    auto load_pair = [&](int slot, int u2, double2 (&dst)[F]) {
+        const double2* B = reinterpret_cast<const double2*>(ring + slot * BLK) + lane;
+#pragma unroll
+        for (int f = 0; f < F; ++f) dst[f] = B[(f * KU / 2 + u2) * 32];
+    };
+    // The inbound values of block q: loaded early (from the middle of block
+    // q - 1, into bn) and tested when block q starts; only if one is still the
+    // sentinel the band spins on reloads.  Every lane reads the same
+    // addresses, so the test is warp-uniform.  A band that is not right behind
+    // the band below pays no load latency for its inbound values.
+    double bz[NBF * KU], bn[NBF * KU];
+    const unsigned inb_addr = ptx::smem_addr(inb);
+    auto load_bnd = [&](int q, double (&o)[NBF * KU]) {
+        const unsigned p = inb_addr + static_cast<unsigned>(q) * (KU * NBF * 8);
+#pragma unroll
+        for (int k = 0; k < NBF * KU / 2; ++k) {
+            const double2 v = lds_v2(p + 16 * k);
+            o[2 * k] = v.x;
+            o[2 * k + 1] = v.y;
+        }
+    };
+    auto take_bnd = [&](int q) {  // bz = the inbound values of block q
+        if (!has_src) return;
+        const long long c0 = a.tl ? clock64() : 0;
+        for (;;) {
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < NBF * KU; ++k) ok = ok && !is_sent_hi(bn[k]);
+            if (__all_sync(0xffffffffu, ok)) break;
+            load_bnd(q, bn);
+        }
+#pragma unroll
+        for (int k = 0; k < NBF * KU; ++k) bz[k] = bn[k];
+        if (a.tl) wait_cyc += clock64() - c0;
+    };
+#pragma unroll
+    for (int k = 0; k < NBF * KU; ++k) bz[k] = bn[k] = 0.0;
+    if (has_src) load_bnd(0, bn);
 
     if constexpr (KIND == 1) {
         const int nx = a.nx;
-        // block q, step s = q KU + u: lane 0 reads z(s, j - 1) = sb[u]
-        double sb[KU], nsb[KU];
-        auto load_bnd = [&](int q, double (&o)[KU]) {
-            const bool on = has_src && lane == 0 && q < a.nblocks;
-#pragma unroll
-            for (int u = 0; u < KU; ++u) {
-                const int c = q * KU + u;
-                o[u] = ld_relaxed_if(sb_in + c, on && c < nx);
-            }
-        };
-        // warp-uniform wait until every value of the block has been stored
-        auto settle = [&](int q, double (&o)[KU]) {
-            const unsigned long long t0 = a.tl ? gtimer() : 0;
-            for (;;) {
-                bool ok = true;
-#pragma unroll
-                for (int u = 0; u < KU; ++u) ok = ok && not_sent(o[u]);
-                if (__all_sync(0xffffffffu, ok)) break;
-                load_bnd(q, o);
-            }
-            if (a.tl) wait_ns += gtimer() - t0;
-        };
-        load_bnd(0, sb);
-        settle(0, sb);
-        if (a.tl) t_first = gtimer();
         double last = 0.0;
         double* zrow = a.z + static_cast<size_t>(j) * nx;
         const bool row_ok = j < a.ny;
-        const bool pub = has_dst && lane == 31;
+        take_bnd(0);
+        if (a.tl) t_first = gtimer();
+        ptx::mbar_wait(bars + 0, 0);
+        load_pair(0, 0, R);
         for (int q = 0; q < a.nblocks; ++q) {
-            load_bnd(q + 1, nsb);  // in flight during this block
-            const int slot = q % kWaveDepth;
-            ptx::mbar_wait(bars + slot, (q / kWaveDepth) & 1);
-            const double2* B = reinterpret_cast<const double2*>(ring + slot * BLK) + lane;
+            if (q > 0) take_bnd(q);
+            if (a.tl && lane == 0 && q < 128) a.tl[8 * 1024 + band * 128 + q] = gtimer();
+            const int slot = q % kWaveDepth, nslot = (q + 1) % kWaveDepth;
+            const unsigned npar = ((q + 1) / kWaveDepth) & 1;
+            const bool more = q + 1 < a.nblocks;
+            const long long c1 = a.tl ? clock64() : 0;
             auto run_block = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
+            bool landed = true;
 #pragma unroll
             for (int u2 = 0; u2 < KU / 2; ++u2) {
-                const double2 b2 = B[(0 * KU / 2 + u2) * 32], cs2 = B[(1 * KU / 2 + u2) * 32],
-                              cw2 = B[(2 * KU / 2 + u2) * 32];
+                double2 Rn[F];
+                if (u2 == 0 && more) landed = mbar_try(bars + nslot, npar);
+                if (u2 == KU / 4 && has_src && more) load_bnd(q + 1, bn);
+                if (u2 + 1 < KU / 2) {
+                    load_pair(slot, u2 + 1, Rn);
+                } else if (more) {  // the next block's first pair
+                    if (!__all_sync(0xffffffffu, landed)) ptx::mbar_wait(bars + nslot, npar);
+                    load_pair(nslot, 0, Rn);
+                }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int u = 2 * u2 + h;
                     double south = __shfl_up_sync(0xffffffffu, last, 1);
-                    if (lane == 0) south = sb[u];
+                    if (lane == 0) south = bz[u];
                     // padding slots (before a lane's first column, after its
                     // last) hold zero records, so they compute 0: no select
-                    last = fma(h ? cw2.y : cw2.x, last, fma(h ? cs2.y : cs2.x, south, h ? b2.y : b2.x));
+                    last = fma(h ? R[2].y : R[2].x, last, fma(h ? R[1].y : R[1].x, south, h ? R[0].y : R[0].x));
                     const int i = q * KU + u - lane;
                     const bool act = FULL ? row_ok : (row_ok && i >= 0 && i < nx);
                     st_global_if(zrow + i, last, act);
                     st_relaxed_if(sb_out + i, last, act && pub);
+                }
+                if (u2 + 1 < KU / 2 || more) {
+#pragma unroll
+                    for (int f = 0; f < F; ++f) R[f] = Rn[f];
                 }
             }
             };
@@ -256,82 +361,64 @@ __global__ void __launch_bounds__(32 * W, 1) k_gs_wave(WaveArgs a) {
                 run_block(std::true_type{});
             else
                 run_block(std::false_type{});
+            if (a.tl) {
+                comp_cyc += clock64() - c1;
+                if (q == 2) t_b4 = gtimer();
+                if (q == 6) t_b12 = gtimer();
+            }
             __syncwarp();  // every lane has read the slot
             tma_block_if(ring + slot * BLK, src + static_cast<size_t>(q + kWaveDepth) * BLK, BLK * 8, bars + slot,
                          lane == 0 && q + kWaveDepth < a.nblocks);
-            settle(q + 1, nsb);
-#pragma unroll
-            for (int u = 0; u < KU; ++u) sb[u] = nsb[u];
         }
     } else {
         const int m = a.nx;
-        const double* su_in = sb_in;              // u(., j-1), m + 1 slots
-        const double* sv_in = sb_in + a.bcols;    // v(., j-1), m slots
-        double* su_out = sb_out;
-        double* sv_out = sb_out + a.bcols;
-        double bu[KU + 1], bv[KU], nbu[KU + 1], nbv[KU];
-        // block q, step s = q KU + u (lane 0: u column s, v column s - 1) reads
-        // u(s, j-1) = bu[u + 1], u(s - 1, j-1) = bu[u], v(s - 1, j-1) = bv[u]
-        auto load_bnd = [&](int q, double (&ou)[KU + 1], double (&ov)[KU]) {
-            const bool on = has_src && lane == 0 && q < a.nblocks;
-#pragma unroll
-            for (int k = 0; k <= KU; ++k) {
-                const int c = q * KU - 1 + k;
-                ou[k] = ld_relaxed_if(su_in + c, on && c >= 0 && c <= m);
-            }
-#pragma unroll
-            for (int k = 0; k < KU; ++k) {
-                const int c = q * KU - 1 + k;
-                ov[k] = ld_relaxed_if(sv_in + c, on && c >= 0 && c < m);
-            }
-        };
-        auto settle = [&](int q, double (&ou)[KU + 1], double (&ov)[KU]) {
-            const unsigned long long t0 = a.tl ? gtimer() : 0;
-            for (;;) {
-                bool ok = not_sent(ou[KU]);
-#pragma unroll
-                for (int k = 0; k < KU; ++k) ok = ok && not_sent(ou[k]) && not_sent(ov[k]);
-                if (__all_sync(0xffffffffu, ok)) break;
-                load_bnd(q, ou, ov);
-            }
-            if (a.tl) wait_ns += gtimer() - t0;
-        };
-        load_bnd(0, bu, bv);
-        settle(0, bu, bv);
-        if (a.tl) t_first = gtimer();
-        double u_last = 0.0, u_last2 = 0.0, v_last = 0.0;
+        // step s = q KU + u of lane 0 (u column s, v column s - 1) reads the
+        // pair {u(s, j-1), v(s-1, j-1)} = bz[2u], bz[2u + 1]; u(s-1, j-1) is
+        // the previous step's u(s, j-1) (su_prev: what a shuffle of the lane's
+        // own previous u would return, lane 0 included)
+        double u_last = 0.0, su_prev = 0.0, v_last = 0.0;
         double* zu = a.z + static_cast<size_t>(j) * (m + 1);
         double* zv = a.z + a.n_u + static_cast<size_t>(j) * m - 1;  // indexed by u column i = v column + 1
         const bool u_row = j < m, v_row = j <= m;
-        const bool pub = has_dst && lane == 31;
+        take_bnd(0);
+        if (a.tl) t_first = gtimer();
+        ptx::mbar_wait(bars + 0, 0);
+        load_pair(0, 0, R);
         for (int q = 0; q < a.nblocks; ++q) {
-            load_bnd(q + 1, nbu, nbv);  // in flight during this block
-            const int slot = q % kWaveDepth;
-            const long long c0 = a.tl ? clock64() : 0;
-            ptx::mbar_wait(bars + slot, (q / kWaveDepth) & 1);
+            if (q > 0) take_bnd(q);
+            if (a.tl && lane == 0 && q < 128) a.tl[8 * 1024 + band * 128 + q] = gtimer();
+            const int slot = q % kWaveDepth, nslot = (q + 1) % kWaveDepth;
+            const unsigned npar = ((q + 1) / kWaveDepth) & 1;
+            const bool more = q + 1 < a.nblocks;
             const long long c1 = a.tl ? clock64() : 0;
-            const double2* B = reinterpret_cast<const double2*>(ring + slot * BLK) + lane;
-            // every lane inside its u and v rows for the whole block: no
+            // FULL: every lane inside its u and v rows for the whole block, no
             // per-step column tests (the interior blocks, most of the sweep)
             auto run_block = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
+            bool landed = true;
 #pragma unroll
             for (int u2 = 0; u2 < KU / 2; ++u2) {
-                double2 R[F];
-#pragma unroll
-                for (int f = 0; f < F; ++f) R[f] = B[(f * KU / 2 + u2) * 32];
+                double2 Rn[F];
+                if (u2 == 0 && more) landed = mbar_try(bars + nslot, npar);
+                if (u2 == KU / 4 && has_src && more) load_bnd(q + 1, bn);
+                if (u2 + 1 < KU / 2) {
+                    load_pair(slot, u2 + 1, Rn);
+                } else if (more) {  // the next block's first pair
+                    if (!__all_sync(0xffffffffu, landed)) ptx::mbar_wait(bars + nslot, npar);
+                    load_pair(nslot, 0, Rn);
+                }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int u = 2 * u2 + h;
                     auto r = [&](int f) { return h ? R[f].y : R[f].x; };
                     double su1 = __shfl_up_sync(0xffffffffu, u_last, 1);   // u(i, j-1)
-                    double su2 = __shfl_up_sync(0xffffffffu, u_last2, 1);  // u(i-1, j-1)
+                    const double su2 = su_prev;                            // u(i-1, j-1)
                     double sv1 = __shfl_up_sync(0xffffffffu, v_last, 1);   // v(i-1, j-1)
                     if (lane == 0) {
-                        su1 = bu[u + 1];
-                        su2 = bu[u];
-                        sv1 = bv[u];
+                        su1 = bz[2 * u];
+                        sv1 = bz[2 * u + 1];
                     }
+                    su_prev = su1;
                     // u(i, j); padding slots hold zero records and compute 0
                     const double un = fma(r(2), u_last, fma(r(1), su1, r(0)));
                     // v(i' = i - 1, j): u neighbours in column order
@@ -345,11 +432,15 @@ __global__ void __launch_bounds__(32 * W, 1) k_gs_wave(WaveArgs a) {
                     const bool va = FULL ? v_row : (v_row && i >= 1 && i <= m);
                     st_global_if(zu + i, un, ua);
                     st_global_if(zv + i, vn, va);
-                    st_relaxed_if(su_out + i, un, ua && pub);
-                    st_relaxed_if(sv_out + i - 1, vn, va && pub);
-                    u_last2 = u_last;
+                    // one 16-byte store for the band above: at i = 0 the v
+                    // half is the 0 of a padding record, which is what it reads
+                    st_pair_if(sb_out + 2 * i, un, vn, ua && pub);
                     u_last = un;
                     v_last = vn;
+                }
+                if (u2 + 1 < KU / 2 || more) {
+#pragma unroll
+                    for (int f = 0; f < F; ++f) R[f] = Rn[f];
                 }
             }
             };
@@ -358,38 +449,36 @@ __global__ void __launch_bounds__(32 * W, 1) k_gs_wave(WaveArgs a) {
             else
                 run_block(std::false_type{});
             if (a.tl) {
-                const long long c2 = clock64();
-                tma_cyc += c1 - c0;
-                comp_cyc += c2 - c1;
+                comp_cyc += clock64() - c1;
+                if (q == 4) t_b4 = gtimer();
+                if (q == 12) t_b12 = gtimer();
             }
             __syncwarp();  // every lane has read the slot
             tma_block_if(ring + slot * BLK, src + static_cast<size_t>(q + kWaveDepth) * BLK, BLK * 8, bars + slot,
                          lane == 0 && q + kWaveDepth < a.nblocks);
-            settle(q + 1, nbu, nbv);
-#pragma unroll
-            for (int k = 0; k <= KU; ++k) bu[k] = nbu[k];
-#pragma unroll
-            for (int k = 0; k < KU; ++k) bv[k] = nbv[k];
         }
     }
     if (a.tl && lane == 0) {
         unsigned long long* o = a.tl + 8 * band;
-        o[4] = tma_cyc;
-        o[5] = comp_cyc;
         o[0] = t_start;
         o[1] = t_first;
         o[2] = gtimer();
-        o[3] = wait_ns;
+        o[3] = static_cast<unsigned long long>(wait_cyc);
+        o[4] = 0;
+        o[5] = static_cast<unsigned long long>(comp_cyc);
+        o[6] = t_b4;
+        o[7] = t_b12;
     }
 }
 
+// slots (steps) of a boundary row and shared memory of a CTA of w bands
 template <int KIND>
-size_t wave_smem_bytes(int w, int bcols) {
+size_t wave_smem_bytes(int w, int nblocks) {
     const size_t nbf = KIND == 1 ? 1 : 2;
     return static_cast<size_t>(w) * (static_cast<size_t>(kWaveDepth) * WaveShape<KIND>::F * WaveShape<KIND>::KU * 32 *
                                          sizeof(double) +
-                                     kWaveDepth * sizeof(uint64_t)) +
-           static_cast<size_t>(w - 1) * nbf * bcols * sizeof(double);
+                                     kWaveDepth * sizeof(uint64_t) +
+                                     nbf * nblocks * WaveShape<KIND>::KU * sizeof(double));
 }
 
 }  // namespace
@@ -490,16 +579,36 @@ bool GsPlan::build_wave(const HostCsr& a, const std::vector<int>& comps, const s
             rec[slot(field[hit], j, step)] = -(a.v[k] * dinv_h[r]);
         }
     }
+    int pick_w = 1;
+    size_t pick_smem = 0;
+    // warps (bands) per CTA: as many as shared memory holds, at most one per
+    // SM sub-partition; the MAC ring is 80 KB per band (SDG_WAVE_W overrides)
+    {
+        constexpr size_t kSmemMax = 226 * 1024;  // 227 KB per CTA minus the static words
+        int w = kind == 1 ? 4 : 2;
+        if (const char* e = std::getenv("SDG_WAVE_W")) w = std::max(1, std::min(w, std::atoi(e)));
+        auto bytes = [&](int ww) { return kind == 1 ? wave_smem_bytes<1>(ww, nblocks) : wave_smem_bytes<2>(ww, nblocks); };
+        while (w > 1 && bytes(w) > kSmemMax) w /= 2;
+        if (bytes(w) > kSmemMax) return false;  // a row too long for one inbound row: the walks run
+        w = std::min(w, nb >= 4 ? 4 : nb >= 2 ? 2 : 1);
+        pick_w = w;
+        pick_smem = bytes(w);
+    }
     if (rec.size() > static_cast<size_t>(INT32_MAX)) return false;  // bidx is int
     packed.upload(rec, s);
     bidx.upload(bx, s);
     wave_ticket.resize(1);
     SDG_CUDA(cudaMemsetAsync(wave_ticket.get(), 0, sizeof(unsigned long long), s));
-    {   // boundary slots, both parities, all holding the sentinel
-        const size_t nbnd = static_cast<size_t>(2) * std::max(nb - 1, 1) * (kind == 1 ? 1 : 2) * cols;
+    {   // L2 boundary rows [2 parities][nb - 1][S slots][NBF]: the sentinel where a value
+        // will arrive, 0 past the row's end (see the kernel's hand-off comment)
+        const size_t nbf = kind == 1 ? 1 : 2, S = static_cast<size_t>(nblocks) * KU;
         double sent;
         std::memcpy(&sent, &kSent, sizeof sent);
-        wave_bnd.upload(std::vector<double>(nbnd, sent), s);
+        std::vector<double> row(nbf * S, 0.0);
+        std::fill(row.begin(), row.begin() + nbf * cols, sent);
+        std::vector<double> all;
+        for (int k = 0; k < 2 * std::max(nb - 1, 1); ++k) all.insert(all.end(), row.begin(), row.end());
+        wave_bnd.upload(all, s);
     }
     wave = true;
     wave_kind = kind;
@@ -507,18 +616,8 @@ bool GsPlan::build_wave(const HostCsr& a, const std::vector<int>& comps, const s
     wave_ny = ny;
     wave_bands = nb;
     wave_blocks = nblocks;
-    // warps (bands) per CTA: as many as shared memory holds, at most one per
-    // SM sub-partition; the MAC ring is 80 KB per band (SDG_WAVE_W overrides)
-    {
-        const int bc = kind == 1 ? nx : nx + 1;
-        constexpr size_t kSmemMax = 226 * 1024;  // 227 KB per CTA minus the static words
-        int w = kind == 1 ? 4 : 2;
-        if (const char* e = std::getenv("SDG_WAVE_W")) w = std::max(1, std::min(w, std::atoi(e)));
-        while (w > 1 && (kind == 1 ? wave_smem_bytes<1>(w, bc) : wave_smem_bytes<2>(w, bc)) > kSmemMax) w /= 2;
-        w = std::min(w, nb >= 4 ? 4 : nb >= 2 ? 2 : 1);
-        wave_w = w;
-        wave_smem = kind == 1 ? wave_smem_bytes<1>(w, bc) : wave_smem_bytes<2>(w, bc);
-    }
+    wave_w = pick_w;
+    wave_smem = pick_smem;
     walk = false;
     usable = true;
     if (std::getenv("SDG_DEBUG"))
@@ -540,11 +639,19 @@ unsigned long long* wave_timeline(int bands) {
         return e && e[0] == '1';
     }();
     if (!on) return nullptr;
-    if (!g_wave_tl) SDG_CUDA(cudaMalloc(&g_wave_tl, 8 * 1024 * sizeof(unsigned long long)));
+    if (!g_wave_tl) SDG_CUDA(cudaMalloc(&g_wave_tl, (8 + 128) * 1024 * sizeof(unsigned long long)));
     g_wave_tl_bands = std::min(bands, 1024);
     return g_wave_tl;
 }
 }  // namespace
+
+int wave_blocks_copy(unsigned long long* out, int max_bands) {  // [band][128] block start times
+    if (!g_wave_tl) return 0;
+    const int nb = std::min(max_bands, g_wave_tl_bands);
+    SDG_CUDA(cudaDeviceSynchronize());
+    SDG_CUDA(cudaMemcpy(out, g_wave_tl + 8 * 1024, 128 * nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    return nb;
+}
 
 int wave_timeline_copy(unsigned long long* out, int max_bands) {
     if (!g_wave_tl) return 0;
@@ -565,7 +672,7 @@ void launch_gs_wave(Context& c, const GsPlan& g, double* z_new) {
         return true;
     }();
     (void)attr;
-    auto go = [&](void (*kernel)(WaveArgs)) { launch_k(c, kernel, ctas, 32 * g.wave_w, g.wave_smem, a); };
+    auto go = [&](void (*kernel)(WaveArgs)) { launch_k(c, kernel, ctas, 32 * (g.wave_w + 1), g.wave_smem, a); };
     if (g.wave_kind == 1) {
         if (g.wave_w == 4) go(k_gs_wave<1, 4>);
         else if (g.wave_w == 2) go(k_gs_wave<1, 2>);

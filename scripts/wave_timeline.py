@@ -28,5 +28,18 @@ t0 = t[:, 0].min()
 print(f"{cfg.name} {which}: {nb} bands, last wave launch (the post-smoother), ns from the first band start")
 for b in range(nb):
     print(f"band {b:3d}: start {t[b,0]-t0:9.0f} first {t[b,1]-t0:9.0f} end {t[b,2]-t0:9.0f} "
-          f"run {t[b,2]-t[b,1]:9.0f} wait {t[b,3]:9.0f} tma-wait cyc {t[b,4]:9.0f} compute cyc {t[b,5]:9.0f}")
+          f"run {t[b,2]-t[b,1]:9.0f} wait cyc {t[b,3]:9.0f} tma-wait cyc {t[b,4]:9.0f} compute cyc {t[b,5]:9.0f} "
+          f"first->blk4 {t[b,6]-t[b,1]:7.0f} blk4->blk12 {t[b,7]-t[b,6]:7.0f}")
 print(f"total {t[:,2].max()-t0:.0f} ns")
+
+if os.environ.get("SDG_WAVE_TL_BLOCKS"):
+    bb = (C.c_ulonglong * (128 * 1024))()
+    nb2 = L.sdg_debug_wave_blocks(bb, 1024)
+    B = np.array(bb[: 128 * nb2], dtype=np.float64).reshape(nb2, 128) - t0
+    nq = int((B[0] > -1e17).sum()) if False else int(os.environ["SDG_WAVE_TL_BLOCKS"])
+    np.save(os.path.join("gpurun_out", "s5e", f"blocks_{which}_w{os.environ.get('SDG_WAVE_W', 'd')}.npy"), B[:, :nq])
+    print("block start times (us), rows = bands, every 4th block; then lag to the band below")
+    for b in range(min(nb2, 6)):
+        print(f"band {b}: " + " ".join(f"{B[b, q] / 1e3:6.1f}" for q in range(0, nq, 4)))
+    for b in range(1, min(nb2, 6)):
+        print(f"lag {b}-{b-1}: " + " ".join(f"{(B[b, q] - B[b - 1, q]) / 1e3:6.1f}" for q in range(0, nq, 4)))
