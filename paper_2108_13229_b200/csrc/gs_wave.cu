@@ -172,11 +172,11 @@ __device__ __forceinline__ bool is_sent_hi(double v) {
     // the sentinel's high word belongs to a NaN that arithmetic never produces
     return static_cast<unsigned>(__double2hiint(v)) == static_cast<unsigned>(kSent >> 32);
 }
-// weak shared load the compiler may not cache or merge (shared memory has no
-// cache in front of it, so a weak load always sees the latest store)
+// relaxed (strong) shared load: ptxas may hoist a weak load out of the spin
+// loop that re-reads the same addresses
 __device__ __forceinline__ double2 lds_v2(unsigned addr) {
     double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    asm volatile("ld.relaxed.cta.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_pair_if(double* p, double x, double y, bool pred) {
@@ -185,7 +185,9 @@ __device__ __forceinline__ void st_pair_if(double* p, double x, double y, bool p
 }
 
 // W compute warps per CTA, one band each (consecutive bands), plus the poller.
-template <int KIND, int W>
+// TL: the dev timeline (SDG_WAVE_TL=1) is a separate instantiation, so the
+// product kernel carries no test of it in its loops
+template <int KIND, int W, bool TL>
 __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
     constexpr int F = WaveShape<KIND>::F, KU = WaveShape<KIND>::KU;
     constexpr int NBF = KIND == 1 ? 1 : 2;  // doubles per boundary slot: z, or {u, v}
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
     const double* inb = inb_all + warp * bstride;                                         // read (all lanes, same address)
     double* sb_out = dst_sh ? inb_all + (warp + 1) * bstride
                             : a.bnd + par * pstride + static_cast<size_t>(has_dst ? band : 0) * bstride;  // written (lane 31)
-    unsigned long long t_start = a.tl ? gtimer() : 0, t_first = 0, t_b4 = 0, t_b12 = 0;
+    unsigned long long t_start = TL ? gtimer() : 0, t_first = 0, t_b4 = 0, t_b12 = 0;
     long long wait_cyc = 0, comp_cyc = 0;
     const bool pub = has_dst && lane == 31;
 
@@ -292,17 +294,23 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
     };
     auto take_bnd = [&](int q) {  // bz = the inbound values of block q
         if (!has_src) return;
-        const long long c0 = a.tl ? clock64() : 0;
+        const long long c0 = TL ? clock64() : 0;
         for (;;) {
-            bool ok = true;
+            // four independent chains of compares, not one of NBF * KU
+            bool ok0 = true, ok1 = true, ok2 = true, ok3 = true;
 #pragma unroll
-            for (int k = 0; k < NBF * KU; ++k) ok = ok && !is_sent_hi(bn[k]);
-            if (__all_sync(0xffffffffu, ok)) break;
+            for (int k = 0; k < NBF * KU; k += 4) {
+                ok0 &= !is_sent_hi(bn[k]);
+                ok1 &= !is_sent_hi(bn[k + 1]);
+                ok2 &= !is_sent_hi(bn[k + 2]);
+                ok3 &= !is_sent_hi(bn[k + 3]);
+            }
+            if (__all_sync(0xffffffffu, (ok0 && ok1) && (ok2 && ok3))) break;
             load_bnd(q, bn);
         }
 #pragma unroll
         for (int k = 0; k < NBF * KU; ++k) bz[k] = bn[k];
-        if (a.tl) wait_cyc += clock64() - c0;
+        if (TL) wait_cyc += clock64() - c0;
     };
 #pragma unroll
     for (int k = 0; k < NBF * KU; ++k) bz[k] = bn[k] = 0.0;
@@ -314,16 +322,16 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
         double* zrow = a.z + static_cast<size_t>(j) * nx;
         const bool row_ok = j < a.ny;
         take_bnd(0);
-        if (a.tl) t_first = gtimer();
+        if (TL) t_first = gtimer();
         ptx::mbar_wait(bars + 0, 0);
         load_pair(0, 0, R);
         for (int q = 0; q < a.nblocks; ++q) {
             if (q > 0) take_bnd(q);
-            if (a.tl && lane == 0 && q < 128) a.tl[8 * 1024 + band * 128 + q] = gtimer();
+            if (TL && lane == 0 && q < 128) a.tl[8 * 1024 + band * 128 + q] = gtimer();
             const int slot = q % kWaveDepth, nslot = (q + 1) % kWaveDepth;
             const unsigned npar = ((q + 1) / kWaveDepth) & 1;
             const bool more = q + 1 < a.nblocks;
-            const long long c1 = a.tl ? clock64() : 0;
+            const long long c1 = TL ? clock64() : 0;
             auto run_block = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
             bool landed = true;
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
                 run_block(std::true_type{});
             else
                 run_block(std::false_type{});
-            if (a.tl) {
+            if (TL) {
                 comp_cyc += clock64() - c1;
                 if (q == 2) t_b4 = gtimer();
                 if (q == 6) t_b12 = gtimer();
@@ -381,16 +389,16 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
         double* zv = a.z + a.n_u + static_cast<size_t>(j) * m - 1;  // indexed by u column i = v column + 1
         const bool u_row = j < m, v_row = j <= m;
         take_bnd(0);
-        if (a.tl) t_first = gtimer();
+        if (TL) t_first = gtimer();
         ptx::mbar_wait(bars + 0, 0);
         load_pair(0, 0, R);
         for (int q = 0; q < a.nblocks; ++q) {
             if (q > 0) take_bnd(q);
-            if (a.tl && lane == 0 && q < 128) a.tl[8 * 1024 + band * 128 + q] = gtimer();
+            if (TL && lane == 0 && q < 128) a.tl[8 * 1024 + band * 128 + q] = gtimer();
             const int slot = q % kWaveDepth, nslot = (q + 1) % kWaveDepth;
             const unsigned npar = ((q + 1) / kWaveDepth) & 1;
             const bool more = q + 1 < a.nblocks;
-            const long long c1 = a.tl ? clock64() : 0;
+            const long long c1 = TL ? clock64() : 0;
             // FULL: every lane inside its u and v rows for the whole block, no
             // per-step column tests (the interior blocks, most of the sweep)
             auto run_block = [&](auto full_tag) {
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
                 run_block(std::true_type{});
             else
                 run_block(std::false_type{});
-            if (a.tl) {
+            if (TL) {
                 comp_cyc += clock64() - c1;
                 if (q == 4) t_b4 = gtimer();
                 if (q == 12) t_b12 = gtimer();
@@ -458,7 +466,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
                          lane == 0 && q + kWaveDepth < a.nblocks);
         }
     }
-    if (a.tl && lane == 0) {
+    if (TL && lane == 0) {
         unsigned long long* o = a.tl + 8 * band;
         o[0] = t_start;
         o[1] = t_first;
@@ -666,20 +674,25 @@ void launch_gs_wave(Context& c, const GsPlan& g, double* z_new) {
                g.wave_nx, g.wave_ny, g.wave_kind == 2 ? g.wave_nx * (g.wave_nx + 1) : 0,
                g.wave_kind == 1 ? g.wave_nx : g.wave_nx + 1, wave_timeline(g.wave_bands)};
     const int ctas = (g.wave_bands + g.wave_w - 1) / g.wave_w;
+    const bool tl = a.tl != nullptr;
     static const bool attr = [] {  // every instantiation may use the whole shared memory of an SM
-        for (auto k : {k_gs_wave<1, 1>, k_gs_wave<1, 2>, k_gs_wave<1, 4>, k_gs_wave<2, 1>, k_gs_wave<2, 2>})
+        for (auto k : {k_gs_wave<1, 1, false>, k_gs_wave<1, 2, false>, k_gs_wave<1, 4, false>, k_gs_wave<2, 1, false>,
+                       k_gs_wave<2, 2, false>, k_gs_wave<1, 1, true>, k_gs_wave<1, 2, true>, k_gs_wave<1, 4, true>,
+                       k_gs_wave<2, 1, true>, k_gs_wave<2, 2, true>})
             SDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
         return true;
     }();
     (void)attr;
-    auto go = [&](void (*kernel)(WaveArgs)) { launch_k(c, kernel, ctas, 32 * (g.wave_w + 1), g.wave_smem, a); };
+    auto go = [&](void (*kernel)(WaveArgs), void (*kernel_tl)(WaveArgs)) {
+        launch_k(c, tl ? kernel_tl : kernel, ctas, 32 * (g.wave_w + 1), g.wave_smem, a);
+    };
     if (g.wave_kind == 1) {
-        if (g.wave_w == 4) go(k_gs_wave<1, 4>);
-        else if (g.wave_w == 2) go(k_gs_wave<1, 2>);
-        else go(k_gs_wave<1, 1>);
+        if (g.wave_w == 4) go(k_gs_wave<1, 4, false>, k_gs_wave<1, 4, true>);
+        else if (g.wave_w == 2) go(k_gs_wave<1, 2, false>, k_gs_wave<1, 2, true>);
+        else go(k_gs_wave<1, 1, false>, k_gs_wave<1, 1, true>);
     } else {
-        if (g.wave_w == 2) go(k_gs_wave<2, 2>);
-        else go(k_gs_wave<2, 1>);
+        if (g.wave_w == 2) go(k_gs_wave<2, 2, false>, k_gs_wave<2, 2, true>);
+        else go(k_gs_wave<2, 1, false>, k_gs_wave<2, 1, true>);
     }
 }
 
