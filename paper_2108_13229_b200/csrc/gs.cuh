@@ -93,6 +93,7 @@ struct GsPlan {
     int wave_nx = 0, wave_ny = 0;        // grid columns (m for MAC) / grid rows
     int wave_bands = 0, wave_blocks = 0, wave_w = 1;  // wave_w: bands (warps) per CTA
     size_t wave_smem = 0;
+    bool wave_split = false;             // MAC: u and v recurrences on separate warps (k_gs_wave_mac)
     DevBuf<unsigned long long> wave_ticket;  // band tickets handed out (gs_wave.cu)
     DevBuf<double> wave_bnd;                 // band boundary rows, two parities, sentinel until written
     // multi-SM lattice lower solve of an aggregated coarse level (gs_lattice.cu);

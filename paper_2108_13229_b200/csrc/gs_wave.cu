@@ -126,13 +126,15 @@ __device__ __forceinline__ void st_global_if(double* p, double v, bool pred) {
     asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.f64 [%0], %1;\n}" ::"l"(p), "d"(v),
                  "r"(static_cast<int>(pred)));
 }
-// refill a ring slot: order the slot's shared loads before the async-proxy
-// write, arm the slot's mbarrier and issue the 1-D bulk copy (one lane)
+// refill a ring slot: arm the slot's mbarrier and issue the 1-D bulk copy (one
+// lane).  No proxy fence: the slot's shared loads have delivered their values
+// (the steps that used them are done, every lane has passed __syncwarp), and a
+// fence.proxy.async here also waits for the warp's outstanding global stores,
+// several hundred cycles on every block (measured: see DESIGN.md).
 __device__ __forceinline__ void tma_block_if(double* dst, const double* src, unsigned bytes, uint64_t* bar,
                                              bool pred) {
     asm volatile(
         "{\n.reg .pred q;\nsetp.ne.b32 q, %4, 0;\n"
-        "@q fence.proxy.async.shared::cta;\n"
         "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n"
         "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}" ::"r"(
             ptx::smem_addr(dst)),
@@ -479,6 +481,323 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// MAC wavefront with the u and v recurrences on separate warps ("split").
+//
+// The u rows of the MAC block never read a v value (assembly.cpp:134-170), so
+// a band's u recurrence can run ahead of its v recurrence, and everything a v
+// row takes from u rows can be summed where the u values are.  Each band gets
+// two warps on two SM sub-partitions:
+//   * the U warp walks u(i, j) like the 5-point kernel and, with the values it
+//     holds anyway (u(i, j), u(i-1, j), and the row below from its shuffle),
+//     also forms t = b_v + (the four u neighbours of v(i-1, j) in column
+//     order) - off its own dependent chain - and drops t into an exchange ring
+//     in shared memory, X[XD blocks][KU steps][32 lanes] (record fields 0-7);
+//   * the V warp follows at least one block behind, takes t from the ring and
+//     runs the v recurrence v = fma(c_W, v_W, fma(c_S, v_S, t)) (fields 8-9).
+// Same operations on the same operands in the same order as the fused kernel,
+// hence the same bits.  Per block the U warp arrives on xfull[slot] after its
+// stores and waits on xempty[slot] before it reuses a ring slot; the V warp
+// does the opposite (mbarriers, one arrive by lane 0 after __syncwarp).
+// Boundary rows are separate for u and v ([U row S | V row S], v indexed by
+// the u column i = v column + 1, slot 0 of the V row is a constant 0), each
+// polled by its own poller warp, so the u chain across bands never waits for
+// the v chain.  Threads: 2 W compute warps + 2 pollers.
+template <int W, bool TL>
+__global__ void __launch_bounds__(32 * (2 * W + 2), 1) k_gs_wave_mac(WaveArgs a) {
+    constexpr int KU = WaveShape<2>::KU, FU = 8, FV = 2, D = kWaveDepth, XD = 4;
+    constexpr int UBLK = FU * KU * 32, VBLK = FV * KU * 32, BLK = UBLK + VBLK, XBLK = KU * 32;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ unsigned long long s_ticket;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int S = a.nblocks * KU;
+    const size_t bstride = 2 * static_cast<size_t>(S);  // [U row | V row]
+    double* uring_all = reinterpret_cast<double*>(smem_raw);
+    double* vring_all = uring_all + W * D * UBLK;
+    double* x_all = vring_all + W * D * VBLK;
+    double* inb_all = x_all + W * XD * XBLK;                                  // [W][2][S]
+    uint64_t* bars_all = reinterpret_cast<uint64_t*>(inb_all + W * bstride);  // per band: U ring D, V ring D, xfull XD, xempty XD
+    constexpr int NBAR = 2 * D + 2 * XD;
+    const int m = a.nx, valid = a.bcols;  // valid = m + 1 u columns
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1ull);
+    if (warp < W && lane == 0) {
+        for (int d = 0; d < NBAR; ++d) ptx::mbar_init(bars_all + warp * NBAR + d, 1);
+        ptx::fence_mbar_init();
+    }
+    auto expects = [&](size_t k) {  // does slot k of a boundary row pair receive a value?
+        const size_t r = k % bstride;
+        const int slot = static_cast<int>(r % S);
+        return r < static_cast<size_t>(S) ? slot < valid : (slot >= 1 && slot < valid);
+    };
+    for (size_t k = threadIdx.x; k < static_cast<size_t>(W) * bstride; k += blockDim.x)
+        inb_all[k] = expects(k) ? __longlong_as_double(static_cast<long long>(kSent)) : 0.0;
+    __syncthreads();
+    const unsigned long long t = s_ticket;
+    const unsigned long long nctas = static_cast<unsigned long long>((a.nbands + W - 1) / W);
+    const int band0 = static_cast<int>(t % nctas) * W;
+    const int par = static_cast<int>((t / nctas) & 1ull);
+    const size_t pstride = static_cast<size_t>(a.nbands - 1) * bstride;
+
+    if (warp >= 2 * W) {  // ---- the pollers: warp 2W the U row, warp 2W + 1 the V row
+        if (band0 == 0 || band0 >= a.nbands) return;
+        const int row = warp - 2 * W;
+        pdl_wait();
+        const size_t off = static_cast<size_t>(band0 - 1) * bstride + static_cast<size_t>(row) * S;
+        {   // reset this row of the other parity for the next launch
+            double* rs = a.bnd + (par ^ 1) * pstride + off;
+            for (int k = lane + row; k < valid; k += 32) rs[k] = __longlong_as_double(static_cast<long long>(kSent));
+        }
+        const double* srcb = a.bnd + par * pstride + off;
+        double* dst = inb_all + static_cast<size_t>(row) * S;  // inbound rows of band 0 of the CTA
+        for (int base = row; base < valid; base += 32) {
+            const int k = base + lane;
+            if (k < valid) {
+                for (;;) {
+                    double v;
+                    asm volatile("ld.relaxed.gpu.f64 %0, [%1];" : "=d"(v) : "l"(srcb + k) : "memory");
+                    if (!is_sent_hi(v)) {
+                        asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(ptx::smem_addr(dst + k)), "d"(v)
+                                     : "memory");
+                        break;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    const int w = warp >> 1;
+    const bool is_v = warp & 1;
+    const int band = band0 + w;
+    if (band >= a.nbands) return;
+    uint64_t* bars = bars_all + w * NBAR + (is_v ? D : 0);
+    uint64_t* xfull = bars_all + w * NBAR + 2 * D;
+    uint64_t* xempty = xfull + XD;
+    double* X = x_all + w * XD * XBLK;
+    pdl_wait();
+    pdl_trigger();
+    const int j = band * 32 + lane;
+    const bool has_src = band > 0, has_dst = band + 1 < a.nbands;
+    const bool dst_sh = w + 1 < W && has_dst;
+    const bool pub = has_dst && lane == 31;
+    const unsigned inb_u = ptx::smem_addr(inb_all + w * bstride), inb_v = inb_u + static_cast<unsigned>(S) * 8;
+    double* out = dst_sh ? inb_all + (w + 1) * bstride
+                         : a.bnd + par * pstride + static_cast<size_t>(has_dst ? band : 0) * bstride;
+    unsigned long long t_start = TL ? gtimer() : 0, t_first = 0;
+    const double* src = a.rec + static_cast<size_t>(band) * a.nblocks * BLK + (is_v ? UBLK : 0);
+
+    if (!is_v) {
+        // ------------------------------------------------------------- U warp
+        double* ring = uring_all + w * D * UBLK;
+        for (int d = 0; d < D && d < a.nblocks; ++d)
+            tma_block_if(ring + d * UBLK, src + static_cast<size_t>(d) * BLK, UBLK * 8, bars + d, lane == 0);
+        double bz[KU], bn[KU];
+        auto load_bnd = [&](int q, double (&o)[KU]) {
+            const unsigned p = inb_u + static_cast<unsigned>(q) * (KU * 8);
+#pragma unroll
+            for (int k = 0; k < KU / 2; ++k) {
+                const double2 v = lds_v2(p + 16 * k);
+                o[2 * k] = v.x;
+                o[2 * k + 1] = v.y;
+            }
+        };
+        auto take_bnd = [&](int q) {
+            if (!has_src) return;
+            for (;;) {
+                bool ok = true;
+#pragma unroll
+                for (int k = 0; k < KU; ++k) ok &= !is_sent_hi(bn[k]);
+                if (__all_sync(0xffffffffu, ok)) break;
+                load_bnd(q, bn);
+            }
+#pragma unroll
+            for (int k = 0; k < KU; ++k) bz[k] = bn[k];
+        };
+#pragma unroll
+        for (int k = 0; k < KU; ++k) bz[k] = bn[k] = 0.0;
+        if (has_src) load_bnd(0, bn);
+        double2 R[FU];
+        auto load_pair = [&](int slot, int u2, double2 (&dst)[FU]) {
+            const double2* B = reinterpret_cast<const double2*>(ring + slot * UBLK) + lane;
+#pragma unroll
+            for (int f = 0; f < FU; ++f) dst[f] = B[(f * KU / 2 + u2) * 32];
+        };
+        double u_last = 0.0, su_prev = 0.0;
+        double* zu = a.z + static_cast<size_t>(j) * (m + 1);
+        const bool u_row = j < m;
+        take_bnd(0);
+        if (TL) t_first = gtimer();
+        ptx::mbar_wait(bars + 0, 0);
+        load_pair(0, 0, R);
+        for (int q = 0; q < a.nblocks; ++q) {
+            if (q > 0) take_bnd(q);
+            const int slot = q % D, nslot = (q + 1) % D, xs = q % XD;
+            const unsigned npar = ((q + 1) / D) & 1;
+            const bool more = q + 1 < a.nblocks;
+            if (q >= XD) ptx::mbar_wait(xempty + xs, ((q / XD) - 1) & 1);  // the V warp is done with this ring slot
+            double* Xq = X + xs * XBLK + lane;
+            auto run_block = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
+            bool landed = true;
+#pragma unroll
+            for (int u2 = 0; u2 < KU / 2; ++u2) {
+                double2 Rn[FU];
+                if (u2 == 0 && more) landed = mbar_try(bars + nslot, npar);
+                if (u2 == KU / 4 && has_src && more) load_bnd(q + 1, bn);
+                if (u2 + 1 < KU / 2) {
+                    load_pair(slot, u2 + 1, Rn);
+                } else if (more) {
+                    if (!__all_sync(0xffffffffu, landed)) ptx::mbar_wait(bars + nslot, npar);
+                    load_pair(nslot, 0, Rn);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int u = 2 * u2 + h;
+                    auto r = [&](int f) { return h ? R[f].y : R[f].x; };
+                    double su1 = __shfl_up_sync(0xffffffffu, u_last, 1);  // u(i, j-1)
+                    if (lane == 0) su1 = bz[u];
+                    const double su2 = su_prev;                           // u(i-1, j-1)
+                    su_prev = su1;
+                    const double un = fma(r(2), u_last, fma(r(1), su1, r(0)));
+                    // for v(i' = i - 1, j): its u neighbours in column order, then b_v
+                    double acc = fma(r(4), su2, 0.0);   // u(i', j-1)
+                    acc = fma(r(5), su1, acc);          // u(i'+1, j-1)
+                    acc = fma(r(6), u_last, acc);       // u(i', j)
+                    acc = fma(r(7), un, acc);           // u(i'+1, j)
+                    const double tv = r(3) + acc;
+                    const int i = q * KU + u - lane;
+                    const bool ua = FULL ? u_row : (u_row && i >= 0 && i <= m);
+                    Xq[u * 32] = tv;
+                    st_global_if(zu + i, un, ua);
+                    st_relaxed_if(out + i, un, ua && pub);
+                    u_last = un;
+                }
+                if (u2 + 1 < KU / 2 || more) {
+#pragma unroll
+                    for (int f = 0; f < FU; ++f) R[f] = Rn[f];
+                }
+            }
+            };
+            if (q * KU - 31 >= 1 && q * KU + KU - 1 <= m)
+                run_block(std::true_type{});
+            else
+                run_block(std::false_type{});
+            __syncwarp();  // every lane has stored its X values and read the record slot
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ptx::smem_addr(xfull + xs)) : "memory");
+            tma_block_if(ring + slot * UBLK, src + static_cast<size_t>(q + D) * BLK, UBLK * 8, bars + slot,
+                         lane == 0 && q + D < a.nblocks);
+        }
+        if (TL && lane == 0) {
+            unsigned long long* o = a.tl + 8 * band;
+            o[0] = t_start;
+            o[1] = t_first;
+            o[2] = gtimer();
+        }
+    } else {
+        // ------------------------------------------------------------- V warp
+        double* ring = vring_all + w * D * VBLK;
+        for (int d = 0; d < D && d < a.nblocks; ++d)
+            tma_block_if(ring + d * VBLK, src + static_cast<size_t>(d) * BLK, VBLK * 8, bars + d, lane == 0);
+        double bz[KU], bn[KU];  // v(s-1, j-1)
+        auto load_bnd = [&](int q, double (&o)[KU]) {
+            const unsigned pv = inb_v + static_cast<unsigned>(q) * (KU * 8);
+#pragma unroll
+            for (int k = 0; k < KU / 2; ++k) {
+                const double2 b2 = lds_v2(pv + 16 * k);
+                o[2 * k] = b2.x;
+                o[2 * k + 1] = b2.y;
+            }
+        };
+        auto take_bnd = [&](int q) {
+            if (!has_src) return;
+            for (;;) {
+                bool ok = true;
+#pragma unroll
+                for (int k = 0; k < KU; ++k) ok &= !is_sent_hi(bn[k]);
+                if (__all_sync(0xffffffffu, ok)) break;
+                load_bnd(q, bn);
+            }
+#pragma unroll
+            for (int k = 0; k < KU; ++k) bz[k] = bn[k];
+        };
+#pragma unroll
+        for (int k = 0; k < KU; ++k) bz[k] = bn[k] = 0.0;
+        if (has_src) load_bnd(0, bn);
+        double2 R[FV];  // cv_S, cv_W
+        auto load_pair = [&](int slot, int u2, double2 (&dst)[FV]) {
+            const double2* B = reinterpret_cast<const double2*>(ring + slot * VBLK) + lane;
+#pragma unroll
+            for (int f = 0; f < FV; ++f) dst[f] = B[(f * KU / 2 + u2) * 32];
+        };
+        double v_last = 0.0;
+        double* zv = a.z + a.n_u + static_cast<size_t>(j) * m - 1;  // indexed by u column i = v column + 1
+        const bool v_row = j <= m;
+        double* outv = out + S;
+        take_bnd(0);
+        ptx::mbar_wait(bars + 0, 0);
+        load_pair(0, 0, R);
+        for (int q = 0; q < a.nblocks; ++q) {
+            if (q > 0) take_bnd(q);
+            const int slot = q % D, nslot = (q + 1) % D, xs = q % XD;
+            const unsigned npar = ((q + 1) / D) & 1;
+            const bool more = q + 1 < a.nblocks;
+            ptx::mbar_wait(xfull + xs, (q / XD) & 1);  // the U warp has stored this block's values
+            const double* Xq = X + xs * XBLK + lane;
+            auto run_block = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
+            bool landed = true;
+#pragma unroll
+            for (int u2 = 0; u2 < KU / 2; ++u2) {
+                double2 Rn[FV];
+                if (u2 == 0 && more) landed = mbar_try(bars + nslot, npar);
+                if (u2 == KU / 4 && has_src && more) load_bnd(q + 1, bn);
+                if (u2 + 1 < KU / 2) {
+                    load_pair(slot, u2 + 1, Rn);
+                } else if (more) {
+                    if (!__all_sync(0xffffffffu, landed)) ptx::mbar_wait(bars + nslot, npar);
+                    load_pair(nslot, 0, Rn);
+                }
+                const double t0 = Xq[(2 * u2) * 32], t1 = Xq[(2 * u2 + 1) * 32];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int u = 2 * u2 + h;
+                    double sv1 = __shfl_up_sync(0xffffffffu, v_last, 1);   // v(i-1, j-1)
+                    if (lane == 0) sv1 = bz[u];
+                    const double vn = fma(h ? R[1].y : R[1].x, v_last, fma(h ? R[0].y : R[0].x, sv1, h ? t1 : t0));
+                    const int i = q * KU + u - lane;
+                    const bool va = FULL ? v_row : (v_row && i >= 1 && i <= m);
+                    st_global_if(zv + i, vn, va);
+                    st_relaxed_if(outv + i, vn, va && pub);
+                    v_last = vn;
+                }
+                if (u2 + 1 < KU / 2 || more) {
+#pragma unroll
+                    for (int f = 0; f < FV; ++f) R[f] = Rn[f];
+                }
+            }
+            };
+            if (q * KU - 31 >= 1 && q * KU + KU - 1 <= m)
+                run_block(std::true_type{});
+            else
+                run_block(std::false_type{});
+            __syncwarp();  // every lane has read the X values and the record slot
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ptx::smem_addr(xempty + xs)) : "memory");
+            tma_block_if(ring + slot * VBLK, src + static_cast<size_t>(q + D) * BLK, VBLK * 8, bars + slot,
+                         lane == 0 && q + D < a.nblocks);
+        }
+        if (TL && lane == 0) a.tl[8 * band + 3] = gtimer();
+    }
+}
+
+size_t wave_mac_smem_bytes(int w, int nblocks) {
+    constexpr int KU = WaveShape<2>::KU;
+    return static_cast<size_t>(w) * (static_cast<size_t>(kWaveDepth) * 10 * KU * 32 * sizeof(double) +  // record rings
+                                     4 * KU * 32 * sizeof(double) +                                     // exchange ring
+                                     2 * static_cast<size_t>(nblocks) * KU * sizeof(double) +           // inbound rows
+                                     (2 * kWaveDepth + 8) * sizeof(uint64_t));
+}
+
 // slots (steps) of a boundary row and shared memory of a CTA of w bands
 template <int KIND>
 size_t wave_smem_bytes(int w, int nblocks) {
@@ -589,13 +908,21 @@ bool GsPlan::build_wave(const HostCsr& a, const std::vector<int>& comps, const s
     }
     int pick_w = 1;
     size_t pick_smem = 0;
-    // warps (bands) per CTA: as many as shared memory holds, at most one per
-    // SM sub-partition; the MAC ring is 80 KB per band (SDG_WAVE_W overrides)
+    // MAC: the split kernel (u and v on separate warps) unless SDG_WAVE_SPLIT=0
+    bool split = kind == 2;
+    if (const char* e = std::getenv("SDG_WAVE_SPLIT")) split = split && e[0] != '0';
+    // warps (bands) per CTA: as many as shared memory holds, at most two (the
+    // MAC rings are 80 KB per band; four 5-point bands on one SM measured
+    // slower than two); SDG_WAVE_W overrides
     {
         constexpr size_t kSmemMax = 226 * 1024;  // 227 KB per CTA minus the static words
-        int w = kind == 1 ? 4 : 2;
-        if (const char* e = std::getenv("SDG_WAVE_W")) w = std::max(1, std::min(w, std::atoi(e)));
-        auto bytes = [&](int ww) { return kind == 1 ? wave_smem_bytes<1>(ww, nblocks) : wave_smem_bytes<2>(ww, nblocks); };
+        int w = 2;
+        if (const char* e = std::getenv("SDG_WAVE_W")) w = std::max(1, std::min(kind == 1 ? 4 : 2, std::atoi(e)));
+        auto bytes = [&](int ww) {
+            return kind == 1 ? wave_smem_bytes<1>(ww, nblocks)
+                   : split   ? wave_mac_smem_bytes(ww, nblocks)
+                             : wave_smem_bytes<2>(ww, nblocks);
+        };
         while (w > 1 && bytes(w) > kSmemMax) w /= 2;
         if (bytes(w) > kSmemMax) return false;  // a row too long for one inbound row: the walks run
         w = std::min(w, nb >= 4 ? 4 : nb >= 2 ? 2 : 1);
@@ -607,13 +934,20 @@ bool GsPlan::build_wave(const HostCsr& a, const std::vector<int>& comps, const s
     bidx.upload(bx, s);
     wave_ticket.resize(1);
     SDG_CUDA(cudaMemsetAsync(wave_ticket.get(), 0, sizeof(unsigned long long), s));
-    {   // L2 boundary rows [2 parities][nb - 1][S slots][NBF]: the sentinel where a value
-        // will arrive, 0 past the row's end (see the kernel's hand-off comment)
+    {   // L2 boundary rows [2 parities][nb - 1][row]: the sentinel where a value will arrive,
+        // 0 elsewhere (see the kernels' hand-off comments).  A row is [S slots][NBF] for the
+        // 5-point and the fused MAC kernel, [U row S | V row S] for the split MAC kernel
+        // (slot 0 of the V row never receives a value)
         const size_t nbf = kind == 1 ? 1 : 2, S = static_cast<size_t>(nblocks) * KU;
         double sent;
         std::memcpy(&sent, &kSent, sizeof sent);
         std::vector<double> row(nbf * S, 0.0);
-        std::fill(row.begin(), row.begin() + nbf * cols, sent);
+        if (split) {
+            std::fill(row.begin(), row.begin() + cols, sent);
+            std::fill(row.begin() + S + 1, row.begin() + S + cols, sent);
+        } else {
+            std::fill(row.begin(), row.begin() + nbf * cols, sent);
+        }
         std::vector<double> all;
         for (int k = 0; k < 2 * std::max(nb - 1, 1); ++k) all.insert(all.end(), row.begin(), row.end());
         wave_bnd.upload(all, s);
@@ -626,12 +960,13 @@ bool GsPlan::build_wave(const HostCsr& a, const std::vector<int>& comps, const s
     wave_blocks = nblocks;
     wave_w = pick_w;
     wave_smem = pick_smem;
+    wave_split = split;
     walk = false;
     usable = true;
     if (std::getenv("SDG_DEBUG"))
         std::fprintf(stderr,
-                     "[sdg] gs wave: kind %d, %d x %d grid, %d bands (%d per CTA), %d blocks of %d steps, %zu B smem\n",
-                     kind, nx, ny, nb, wave_w, nblocks, KU, wave_smem);
+                     "[sdg] gs wave: kind %d%s, %d x %d grid, %d bands (%d per CTA), %d blocks of %d steps, %zu B smem\n",
+                     kind, wave_split ? " (u/v split)" : "", nx, ny, nb, wave_w, nblocks, KU, wave_smem);
     return true;
 }
 
@@ -686,6 +1021,18 @@ void launch_gs_wave(Context& c, const GsPlan& g, double* z_new) {
     auto go = [&](void (*kernel)(WaveArgs), void (*kernel_tl)(WaveArgs)) {
         launch_k(c, tl ? kernel_tl : kernel, ctas, 32 * (g.wave_w + 1), g.wave_smem, a);
     };
+    if (g.wave_split) {
+        static const bool attr2 = [] {
+            for (auto k : {k_gs_wave_mac<1, false>, k_gs_wave_mac<2, false>, k_gs_wave_mac<1, true>, k_gs_wave_mac<2, true>})
+                SDG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+            return true;
+        }();
+        (void)attr2;
+        auto kern = g.wave_w == 2 ? (tl ? k_gs_wave_mac<2, true> : k_gs_wave_mac<2, false>)
+                                  : (tl ? k_gs_wave_mac<1, true> : k_gs_wave_mac<1, false>);
+        launch_k(c, kern, ctas, 32 * (2 * g.wave_w + 2), g.wave_smem, a);
+        return;
+    }
     if (g.wave_kind == 1) {
         if (g.wave_w == 4) go(k_gs_wave<1, 4, false>, k_gs_wave<1, 4, true>);
         else if (g.wave_w == 2) go(k_gs_wave<1, 2, false>, k_gs_wave<1, 2, true>);
