@@ -11,23 +11,31 @@
 //     west to east, one cell per step, one step behind lane L - 1: the west
 //     value stays in a register, the south values come from lane L - 1's
 //     previous step by warp shuffle;
-//   * bands are separate CTAs (one warp each) on separate SMs.  Lane 31 of a
-//     band also stores each value of its row into a boundary buffer whose
-//     slots hold a sentinel until written, and lane 0 of the band above polls
-//     those slots (L2, relaxed loads, one block of KU columns ahead): the
-//     value is its own ready flag, so the hand-off needs no fence, no flag
-//     and no acquire.  Bands run as a pipeline whose depth is the wavefront's
-//     own (columns + rows steps) plus about one block and one L2 round trip
-//     per band;
+//   * bands run as a pipeline over SMs, W bands (warps) per CTA.  A band reads
+//     the top row of the band below from an *inbound row* in its CTA's shared
+//     memory, one block of KU steps at a time; the values are loaded early
+//     (from the middle of the previous block) and tested when the block
+//     starts, so a band that is not right behind the band below never waits.
+//     The inbound row is filled by the band below itself when it is a warp of
+//     the same CTA, otherwise by a *poller warp* that copies the band below's
+//     L2 boundary buffer (st.relaxed.gpu by its lane 31) into shared memory
+//     slot by slot.  Every slot - in L2 and in shared memory - holds a
+//     sentinel until written: the value is its own ready flag, so the
+//     hand-off needs no fence, no flag and no acquire, and the compute warps
+//     never wait on an L2 round trip.  The pipeline's depth is the wavefront's
+//     own (columns + rows steps) plus about KU steps per band;
 //   * band ids come from a ticket counter (atomicAdd), so the band a CTA waits
 //     for always belongs to a CTA that started earlier (no co-residency
-//     assumption); the boundary buffer has two parities (launch e uses e % 2
-//     and resets the other), so a captured CUDA graph replays the kernel
+//     assumption); the L2 boundary buffer has two parities (launch e uses
+//     e % 2 and resets the other), so a captured CUDA graph replays the kernel
 //     unchanged;
-//   * the records of a band, [block][field][KU/2 step pairs][32 lanes][2], are streamed
-//     into a shared-memory ring by 1-D TMA bulk copies (cp.async.bulk +
-//     mbarrier), one copy per block, so every step reads its coefficients
-//     from shared memory with conflict-free 8-byte loads.
+//   * the records of a band, [block][field][KU/2 step pairs][32 lanes][2], are
+//     streamed into a shared-memory ring by 1-D TMA bulk copies (cp.async.bulk
+//     + mbarrier), one copy per block, and read with 16-byte shared loads one
+//     step pair ahead of their use;
+//   * the MAC block runs its u and v recurrences on two warps per band
+//     (k_gs_wave_mac below); k_gs_wave<2> is the same sweep on one warp
+//     (SDG_WAVE_SPLIT=0), kept as the bitwise cross-check.
 //
 // b (the prep kernels' output, gs.cu) lives in the same record array: the
 // plan's bidx points each row at its b slot, so the prep kernels are shared
@@ -97,21 +105,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // use; launches of one plan are ordered (each starts with griddepcontrol.wait).
 constexpr unsigned long long kSent = 0x7ff4deadbeefcafeull;  // a signalling-NaN payload arithmetic never makes
 
-__device__ __forceinline__ bool not_sent(double v) {
-    return static_cast<unsigned long long>(__double_as_longlong(v)) != kSent;
-}
 // Everything inside the step loop is warp-uniform control flow; per-lane work
-// (lane 0's boundary loads, lane 31's boundary stores, the elected bulk copy)
-// is predicated, never branched: a lane-divergent branch there makes the
-// compiler's divergent-warp fallback (collective shuffles) run the block.
-__device__ __forceinline__ double ld_relaxed_if(const double* p, bool pred) {
-    double v;
-    asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\nmov.b64 %0, 0;\n@q ld.relaxed.gpu.f64 %0, [%1];\n}"
-                 : "=d"(v)
-                 : "l"(p), "r"(static_cast<int>(pred))
-                 : "memory");
-    return v;
-}
+// (lane 31's boundary stores, the elected bulk copy) is predicated, never
+// branched: a lane-divergent branch there makes the compiler's divergent-warp
+// fallback (collective shuffles) run the block.
 __device__ __forceinline__ void st_relaxed_if(double* p, double v, bool pred) {
     // every stored value is the result of an fma, which never returns a
     // signalling NaN, so a stored value is never the sentinel

@@ -206,6 +206,34 @@ def test_wave_bands_per_cta_bitwise(monkeypatch, wave_w):
         assert np.array_equal(z0[0], z1[0]) and np.array_equal(z0[1], z1[1]) and np.array_equal(z0[0], z0[1])
 
 
+@pytest.mark.parametrize("cfg_name", ["c1", "c2"])
+def test_wave_mac_split_bitwise_vs_fused(monkeypatch, cfg_name):
+    """The MAC wavefront with the u and v recurrences on two warps per band
+    (k_gs_wave_mac, the default) against the same sweep on one warp
+    (SDG_WAVE_SPLIT=0): the velocity V-cycle gives the same bits, with one and
+    with two bands per CTA, and repeated applies are bitwise reproducible."""
+    from paper_2108_13229_b200 import scenarios
+    cfg = scenarios.CONFIGS[cfg_name]
+    s = scenarios.build_system(cfg)
+    V = sdc.submatrix(s.matrix, 0, s.n_vel, 0, s.n_vel)
+    opts = sdc.AmgOptions(components=[0] * s.n_u + [1] * (s.n_vel - s.n_u), max_levels=cfg.v_max_levels)
+    rng = np.random.default_rng(11)
+    r = [rng.standard_normal(V.n_rows) for _ in range(2)]
+    monkeypatch.setenv("SDG_WAVE_SPLIT", "0")
+    fused = sdc.AmgPreconditioner(V, opts)
+    assert "wave_v" in fused.features()
+    z0 = [fused.apply(x) for x in r]
+    del fused
+    for w in ("1", "2"):
+        monkeypatch.setenv("SDG_WAVE_SPLIT", "1")
+        monkeypatch.setenv("SDG_WAVE_W", w)
+        split = sdc.AmgPreconditioner(V, opts)
+        assert "wave_v" in split.features()
+        z1 = [split.apply(x) for x in r] + [split.apply(r[0])]
+        del split
+        assert np.array_equal(z0[0], z1[0]) and np.array_equal(z0[1], z1[1]) and np.array_equal(z1[0], z1[2])
+
+
 @pytest.mark.parametrize("cfg_name", ["c3"])
 def test_lattice_smoother_matches_walks(monkeypatch, cfg_name):
     """The multi-SM lattice lower solve (gs_lattice.cu, opt-in SDG_GS_LATTICE=1)
