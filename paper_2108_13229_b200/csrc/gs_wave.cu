@@ -66,6 +66,18 @@ namespace sdg {
 namespace {
 
 constexpr int kWaveDepth = 4;  // blocks of records in flight per band
+// MAC block: steps per block and ring depth of the two-warp kernel.  Measured
+// at c3 (velocity V-cycle): 8 steps x 4 blocks, two bands per CTA 820 us;
+// 16 x 2, two bands per CTA 823 us (refills arrive late); 16 x 3, one band per
+// CTA 765 us: the per-block work (inbound test, mbarrier probes, ring refill)
+// is a third of a block of 8 steps.
+#ifndef SDG_WAVE_MAC_KU
+#define SDG_WAVE_MAC_KU 16
+#endif
+#ifndef SDG_WAVE_MAC_DEPTH
+#define SDG_WAVE_MAC_DEPTH 3
+#endif
+constexpr int kMacDepth = SDG_WAVE_MAC_DEPTH;  // the same for the two-warp MAC kernel
 
 template <int KIND>
 struct WaveShape;
@@ -75,7 +87,7 @@ struct WaveShape<1> {  // 5-point: b, c_S, c_W
 };
 template <>
 struct WaveShape<2> {  // MAC: bu, cu_S, cu_W, bv, c_u(i',j-1), c_u(i'+1,j-1), c_u(i',j), c_u(i'+1,j), cv_S, cv_W
-    static constexpr int F = 10, KU = 8;
+    static constexpr int F = 10, KU = SDG_WAVE_MAC_KU;
 };
 
 struct WaveArgs {
@@ -502,7 +514,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_gs_wave(WaveArgs a) {
 // the v chain.  Threads: 2 W compute warps + 2 pollers.
 template <int W, bool TL>
 __global__ void __launch_bounds__(32 * (2 * W + 2), 1) k_gs_wave_mac(WaveArgs a) {
-    constexpr int KU = WaveShape<2>::KU, FU = 8, FV = 2, D = kWaveDepth, XD = 4;
+    constexpr int KU = WaveShape<2>::KU, FU = 8, FV = 2, D = kMacDepth, XD = 4;
     constexpr int UBLK = FU * KU * 32, VBLK = FV * KU * 32, BLK = UBLK + VBLK, XBLK = KU * 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ unsigned long long s_ticket;
@@ -621,6 +633,7 @@ __global__ void __launch_bounds__(32 * (2 * W + 2), 1) k_gs_wave_mac(WaveArgs a)
             for (int f = 0; f < FU; ++f) dst[f] = B[(f * KU / 2 + u2) * 32];
         };
         double u_last = 0.0, su_prev = 0.0;
+        bool x_free = false;
         double* zu = a.z + static_cast<size_t>(j) * (m + 1);
         const bool u_row = j < m;
         take_bnd(0);
@@ -632,7 +645,8 @@ __global__ void __launch_bounds__(32 * (2 * W + 2), 1) k_gs_wave_mac(WaveArgs a)
             const int slot = q % D, nslot = (q + 1) % D, xs = q % XD;
             const unsigned npar = ((q + 1) / D) & 1;
             const bool more = q + 1 < a.nblocks;
-            if (q >= XD) ptx::mbar_wait(xempty + xs, ((q / XD) - 1) & 1);  // the V warp is done with this ring slot
+            // the V warp is done with this ring slot (probed during the previous block)
+            if (q >= XD && !__all_sync(0xffffffffu, x_free)) ptx::mbar_wait(xempty + xs, ((q / XD) - 1) & 1);
             double* Xq = X + xs * XBLK + lane;
             auto run_block = [&](auto full_tag) {
             constexpr bool FULL = decltype(full_tag)::value;
@@ -642,6 +656,8 @@ __global__ void __launch_bounds__(32 * (2 * W + 2), 1) k_gs_wave_mac(WaveArgs a)
                 double2 Rn[FU];
                 if (u2 == 0 && more) landed = mbar_try(bars + nslot, npar);
                 if (u2 == KU / 4 && has_src && more) load_bnd(q + 1, bn);
+                if (u2 == KU / 4 && q + 1 >= XD && more)
+                    x_free = mbar_try(xempty + (q + 1) % XD, (((q + 1) / XD) - 1) & 1);
                 if (u2 + 1 < KU / 2) {
                     load_pair(slot, u2 + 1, Rn);
                 } else if (more) {
@@ -789,10 +805,10 @@ __global__ void __launch_bounds__(32 * (2 * W + 2), 1) k_gs_wave_mac(WaveArgs a)
 
 size_t wave_mac_smem_bytes(int w, int nblocks) {
     constexpr int KU = WaveShape<2>::KU;
-    return static_cast<size_t>(w) * (static_cast<size_t>(kWaveDepth) * 10 * KU * 32 * sizeof(double) +  // record rings
+    return static_cast<size_t>(w) * (static_cast<size_t>(kMacDepth) * 10 * KU * 32 * sizeof(double) +   // record rings
                                      4 * KU * 32 * sizeof(double) +                                     // exchange ring
                                      2 * static_cast<size_t>(nblocks) * KU * sizeof(double) +           // inbound rows
-                                     (2 * kWaveDepth + 8) * sizeof(uint64_t));
+                                     (2 * kMacDepth + 8) * sizeof(uint64_t));
 }
 
 // slots (steps) of a boundary row and shared memory of a CTA of w bands
