@@ -312,6 +312,17 @@ int sdg_assemble_monolithic(const sdg_scenario* sc, const double* k_cell, const 
  * Replaces the per-step assemble_monolithic call of MonolithicDriver::advance
  * (bench.cpp:187, assembly.cpp:327-380). */
 int sdg_assemble_rhs_device(sdg_context* ctx, const sdg_scenario* sc, const double* v_prev_dev, double* rhs_dev);
+/* The matrix of assemble_monolithic on the device (StokesAssembler / DarcyAssembler /
+ * coupling rows, assembly.cpp:17-286 and 327-380), CSR with int32 offsets, bitwise the
+ * host assembly (sdg_assemble_monolithic), with the per-cell permeability extension
+ * (k_cell_dev: n*n device doubles, or NULL for the scenario's uniform K).  One thread per
+ * row emits the row's contributions in the reference's order with explicitly rounded
+ * operations; a count pass and a device scan give the row offsets.
+ * rowptr_dev: n_total + 1 device ints, always written; *nnz receives the number of
+ * entries.  col_dev / val_dev (capacity entries) are written when capacity >= *nnz; with
+ * NULL col_dev / val_dev the call only counts (then size the arrays and call again). */
+int sdg_assemble_matrix_device(sdg_context* ctx, const sdg_scenario* sc, const double* k_cell_dev, int* rowptr_dev,
+                               int* col_dev, double* val_dev, int64_t capacity, int64_t* nnz);
 int sdg_assemble_stokes(const sdg_scenario* sc, const double* v_prev, const double* v_gamma, int* n,
                         int64_t* nnz, int* rowptr, int* col, double* val, double* rhs);
 int sdg_assemble_darcy(const sdg_scenario* sc, const double* p_gamma, int* n, int64_t* nnz, int* rowptr,

@@ -604,6 +604,19 @@ int sdg_assemble_rhs_device(sdg_context* ctx, const sdg_scenario* sc, const doub
     });
 }
 
+int sdg_assemble_matrix_device(sdg_context* ctx, const sdg_scenario* sc, const double* k_cell_dev, int* rowptr_dev,
+                               int* col_dev, double* val_dev, int64_t capacity, int64_t* nnz) {
+    return guard([&] {
+        need(ctx, "sdg_assemble_matrix_device");
+        need(sc, "sdg_assemble_matrix_device");
+        need(rowptr_dev, "sdg_assemble_matrix_device");
+        need(nnz, "sdg_assemble_matrix_device");
+        *nnz = sdg::assemble_matrix_device(*ctx->p, *sc, k_cell_dev, rowptr_dev, col_dev, val_dev, capacity);
+        if (col_dev && val_dev && capacity < *nnz)
+            sdg::fail(SDG_EDIM, "sdg_assemble_matrix_device: capacity below the number of entries");
+    });
+}
+
 // ---- partitioned subproblems (host) --------------------------------------------
 namespace {
 int copy_system(const sdg::LinearSystem& s, int* n, int64_t* nnz, int* rowptr, int* col, double* val, double* rhs) {

@@ -18,6 +18,8 @@ namespace sdg {
 
 // device right-hand side of the monolithic system (assemble.cu), bitwise setup.cpp's
 void launch_assemble_rhs(Context& c, const sdg_scenario& sc, const double* v_prev, double* rhs);
+int64_t assemble_matrix_device(Context& c, const sdg_scenario& sc, const double* k_cell_dev, int* rowptr_dev,
+                               int* col_dev, double* val_dev, int64_t capacity);
 
 struct BiWork;     // krylov.cu: cached BiCGSTAB workspace + captured iteration graph
 struct GmresWork;  // krylov.cu: cached GMRES basis / workspace + captured Arnoldi-step graphs

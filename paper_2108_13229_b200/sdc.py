@@ -164,6 +164,7 @@ def lib():
         p("sdg_bicgstab_device", _i, [_vp, _vp, _vp, _vp, _d, _i, P(_Report)])
         p("sdg_power_iteration", _i, [_vp, _d, _i, C.c_uint, P(_d), P(_i), P(_i)])
         p("sdg_assemble_rhs_device", _i, [_vp, P(_Scenario), _vp, _vp])
+        p("sdg_assemble_matrix_device", _i, [_vp, P(_Scenario), _vp, _vp, _vp, _vp, _i64, P(_i64)])
         p("sdg_assemble_monolithic", _i, [P(_Scenario), _vp, _vp, P(_i), P(_i64), P(_i), P(_i), P(_i),
                                           P(_i), _vp, _vp, _vp, _vp])
         p("sdg_assemble_stokes", _i, [P(_Scenario), _vp, _vp, P(_i), P(_i64), _vp, _vp, _vp, _vp])
@@ -1014,6 +1015,32 @@ def assemble_rhs_device(cfg: ScenarioConfig, rhs_ptr: int, v_prev_ptr: Optional[
     sc = _scenario_c(cfg, t)
     _check(lib().sdg_assemble_rhs_device(ctx.h, C.byref(sc), None if v_prev_ptr is None else C.c_void_p(v_prev_ptr),
                                          C.c_void_p(rhs_ptr)))
+
+
+def assemble_matrix_device(cfg: ScenarioConfig, k_cell=None, t: Optional[float] = None,
+                           ctx: Optional[Context] = None) -> SparseMatrix:
+    """The matrix of assemble_monolithic assembled on the device (sdg_assemble_matrix_device:
+    count pass, device scan, fill pass) and copied back as a SparseMatrix; bitwise the
+    host assembly, per-cell permeability included."""
+    import torch
+    ctx = ctx or default_context()
+    sc = _scenario_c(cfg, t)
+    n = cfg.cells_per_unit_square
+    n_total = 2 * n * (n + 1) + 2 * n * n
+    dev = torch.device("cuda")
+    kd = None if k_cell is None else torch.from_numpy(np.ascontiguousarray(k_cell, dtype=np.float64)).to(dev)
+    rp = torch.empty(n_total + 1, dtype=torch.int32, device=dev)
+    nnz = _i64()
+    kp = None if kd is None else C.c_void_p(kd.data_ptr())
+    _check(lib().sdg_assemble_matrix_device(ctx.h, C.byref(sc), kp, C.c_void_p(rp.data_ptr()), None, None, 0,
+                                            C.byref(nnz)))
+    ci = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)
+    vv = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=dev)
+    _check(lib().sdg_assemble_matrix_device(ctx.h, C.byref(sc), kp, C.c_void_p(rp.data_ptr()),
+                                            C.c_void_p(ci.data_ptr()), C.c_void_p(vv.data_ptr()), nnz.value,
+                                            C.byref(nnz)))
+    return SparseMatrix(n_total, n_total, rp.cpu().numpy(), ci.cpu().numpy()[:nnz.value],
+                        vv.cpu().numpy()[:nnz.value])
 
 
 def _scenario_c(cfg: "ScenarioConfig", t: Optional[float]) -> _Scenario:

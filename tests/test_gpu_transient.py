@@ -148,3 +148,26 @@ def test_device_rhs_assembly_bitwise(n):
             ctx.synchronize()
             dev = out.cpu().numpy()
             assert np.array_equal(dev.view(np.uint64), host.view(np.uint64)), (n, dt, t, v_prev is None)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3, 7, 16, 50, 160])
+def test_device_matrix_assembly_bitwise(n):
+    """sdg_assemble_matrix_device (assemble.cu: one thread per row, count pass,
+    device scan, fill pass) equals the host assembly's CSR (setup.cpp, itself
+    bitwise the reference's assemble_monolithic for a uniform K) bit for bit:
+    offsets, columns and values, stationary and transient, uniform and per-cell
+    (log-normal) permeability."""
+    rng = np.random.default_rng(100 + n)
+    for dt in (float("inf"), 0.1):
+        for perm in (1.0, 1e-2, 1e-4):
+            cfg = sdc.ScenarioConfig(cells_per_unit_square=n, permeability=perm, alpha_bj=1.0, kinematic_viscosity=1.0,
+                                     density=1.0, dt=dt, t_end=1.0, dp_max=1.0)
+            for k_cell in (None, 10.0 ** rng.standard_normal(n * n)):
+                host = sdc.assemble_monolithic(cfg, k_cell=k_cell).matrix
+                dev = sdc.assemble_matrix_device(cfg, k_cell=k_cell)
+                assert dev.n_rows == host.n_rows
+                assert np.array_equal(dev.row_offsets, host.row_offsets), (n, dt, perm, k_cell is None)
+                assert np.array_equal(dev.col_indices, host.col_indices), (n, dt, perm, k_cell is None)
+                assert np.array_equal(dev.values.view(np.uint64), host.values.view(np.uint64)), \
+                    (n, dt, perm, k_cell is None)
