@@ -59,7 +59,7 @@ if os.path.exists(ll):
     with open(os.path.join(DST, "launches_c3_summary.csv"), "w") as f:
         f.write("kernel,launches,total_ms,mean_us,share_of_kernel_time\n")
         for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-            f.write(f"{k},{c},{t / 1e6:.3f},{t / c / 1e3:.2f},{t / tot:.4f}\n")
+            f.write(f"\"{k}\",{c},{t / 1e6:.3f},{t / c / 1e3:.2f},{t / tot:.4f}\n")
 
 # DRAM bytes per launch of one td_bgs apply (ncu, caches cold per launch)
 traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
