@@ -468,7 +468,8 @@ int sdg_pd_gmres_warm(sdg_matrix* a, sdg_precond* precond, const double* b_host,
         need(a, "sdg_pd_gmres_warm");
         auto& c = *a->p->ctx;
         const int n = a->p->host.n_rows;
-        sdg::DevBuf<double> b(std::max(n, 1)), x(std::max(n, 1));
+        c.stage(static_cast<std::size_t>(std::max(n, 1)));
+        sdg::DevBuf<double>&b = c.stage_b, &x = c.stage_x;
         b.upload(b_host, n, c.stream);
         x.upload(x_host, n, c.stream);
         const int rc = sdg_pd_gmres_warm_device(a, precond, b.get(), x.get(), tol_abs, max_restarts, ctrl, rep);
@@ -502,7 +503,8 @@ int sdg_bicgstab_warm(sdg_matrix* a, sdg_precond* precond, const double* b_host,
         need(a, "sdg_bicgstab_warm");
         auto& c = *a->p->ctx;
         const int n = a->p->host.n_rows;
-        sdg::DevBuf<double> b(std::max(n, 1)), x(std::max(n, 1));
+        c.stage(static_cast<std::size_t>(std::max(n, 1)));
+        sdg::DevBuf<double>&b = c.stage_b, &x = c.stage_x;
         b.upload(b_host, n, c.stream);
         x.upload(x_host, n, c.stream);
         const int rc = sdg_bicgstab_warm_device(a, precond, b.get(), x.get(), tol_abs, max_iters, rep);
@@ -519,7 +521,8 @@ int sdg_pd_gmres(sdg_matrix* a, sdg_precond* precond, const double* b_host, doub
         auto t0 = std::chrono::steady_clock::now();
         auto& c = *a->p->ctx;
         const int n = a->p->host.n_rows;
-        sdg::DevBuf<double> b(n), x(n);
+        c.stage(static_cast<std::size_t>(std::max(n, 1)));
+        sdg::DevBuf<double>&b = c.stage_b, &x = c.stage_x;
         b.upload(b_host, n, c.stream);
         const int64_t apps0 = precond ? precond->p->applications() : 0;
         sdg::SolveOut o = sdg::pd_gmres(*a->p, precond ? precond->p.get() : nullptr, b.get(),
@@ -550,7 +553,8 @@ int sdg_bicgstab(sdg_matrix* a, sdg_precond* precond, const double* b_host, doub
         auto t0 = std::chrono::steady_clock::now();
         auto& c = *a->p->ctx;
         const int n = a->p->host.n_rows;
-        sdg::DevBuf<double> b(n), x(n);
+        c.stage(static_cast<std::size_t>(std::max(n, 1)));
+        sdg::DevBuf<double>&b = c.stage_b, &x = c.stage_x;
         b.upload(b_host, n, c.stream);
         const int64_t apps0 = precond ? precond->p->applications() : 0;
         sdg::SolveOut o = sdg::bicgstab(*a->p, precond ? precond->p.get() : nullptr, b.get(),

@@ -154,6 +154,16 @@ struct Context {
     void side_end();
     void side_join();
 
+    // Device staging of the host-pointer solve entry points (b and x), kept
+    // across calls: a cudaMalloc / cudaFree pair per call cost up to 130 ms on
+    // the GPU box (cudaFree synchronises the device and unmaps; measured with
+    // scripts/e2e_probe.py), which is end-to-end time of every host-pointer solve.
+    DevBuf<double> stage_b, stage_x;
+    void stage(std::size_t n) {
+        if (stage_b.size() < n) stage_b.resize(n);
+        if (stage_x.size() < n) stage_x.resize(n);
+    }
+
     explicit Context(int dev);
     ~Context();
     void sync() { SDG_CUDA(cudaStreamSynchronize(stream)); }

@@ -352,6 +352,60 @@ BlockPrecond::BlockPrecond(CtxPtr c, int kind, const HostCsr& matrix, int n_v, i
     }
     tmp_.resize(std::max(n_ppm_, 1));
     cx.sync();
+    if (early_ev_) tune_early();
+}
+
+// Early or late interface correction?  Both are the same arithmetic (bitwise);
+// which is faster depends on what the GEMV's stream of K does to the
+// post-smoother it overlaps: at c2 (K = 33 MB, in L2) and c4 (K = 8 GB, the
+// GEMV far longer than the smoother) early wins, at c3 (K = 1 GB, GEMV and
+// wavefront about equally long) the GEMV's CTAs fill the SMs before the
+// wavefront's CTAs find room and late wins (c3 solve 208.6 ms early, 203.4 ms
+// late; c4 55.9 s early, 57.8 s late; c2 76.5 ms early, 79.6 ms late).  So, like
+// the smoother plans, the choice is timed at setup: ten applies each way.
+// SDG_TD_EARLY=1 keeps early without timing, =0 never sets it up.
+void BlockPrecond::tune_early() {
+    const char* e = std::getenv("SDG_TD_EARLY");
+    if (e && e[0] == '1') return;
+    auto* uz = dynamic_cast<UzawaPrecond*>(first_.get());
+    if (!uz) return;
+    Context& cx = *ctx_;
+    const int n = n_v_ + n_pff_ + n_ppm_;
+    DevBuf<double> r(n), z(n);
+    launch_fill(cx, r.get(), 1.0, n);
+    cudaEvent_t a, b;
+    SDG_CUDA(cudaEventCreate(&a));
+    SDG_CUDA(cudaEventCreate(&b));
+    auto timed = [&] {
+        for (int k = 0; k < 3; ++k) do_apply(r.get(), z.get());
+        SDG_CUDA(cudaEventRecord(a, cx.stream));
+        for (int k = 0; k < 10; ++k) do_apply(r.get(), z.get());
+        SDG_CUDA(cudaEventRecord(b, cx.stream));
+        SDG_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        return ms / 10.f;
+    };
+    const float t_early = timed();
+    cudaEvent_t ev = early_ev_;
+    const GsPlan* plan = early_plan_;
+    uz->inner_mut().post_mark = nullptr;
+    early_ev_ = nullptr;
+    early_plan_ = nullptr;
+    const float t_late = timed();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const bool keep = t_early <= t_late;
+    if (keep) {
+        early_ev_ = ev;
+        early_plan_ = plan;
+        uz->inner_mut().post_mark = ev;
+    } else {
+        cudaEventDestroy(ev);
+    }
+    if (std::getenv("SDG_DEBUG"))
+        std::fprintf(stderr, "[sdg td_bgs] interface correction: early %.1f us, late %.1f us per apply -> %s\n",
+                     1e3 * t_early, 1e3 * t_late, keep ? "early" : "late");
 }
 
 // td_bgs: z_pm = P_D'(r_pm - C' z_ff).  P_D' (one AMG V-cycle from zero:

@@ -225,6 +225,7 @@ private:
     // early correction: w and z_pm -= K w on the side stream as soon as the
     // Uzawa V-cycle's finest post-smoother has its packed b (setup_early_w)
     void setup_early_w(const HostCsr& matrix);
+    void tune_early();  // early or late, timed at setup
     cudaEvent_t early_ev_ = nullptr;
     const GsPlan* early_plan_ = nullptr;
 

@@ -381,13 +381,14 @@ def test_c2_walk_roles_bitwise(monkeypatch):
 @pytest.mark.parametrize("split", ["0", "1"], ids=["v0-wave", "label-block-walks"])
 def test_c2_early_interface_correction_bitwise(monkeypatch, split):
     """td_bgs with the interface GEMV started on the side stream from the
-    Uzawa post-smoother's mark (the default) against the GEMV after the join:
+    Uzawa post-smoother's mark (SDG_TD_EARLY=1) against the GEMV after the join:
     bitwise equal, for the V0 wavefront and for label-block walks."""
     from paper_2108_13229_b200 import scenarios
     monkeypatch.setenv("SDG_GS_SPLIT", split)
     cfg = scenarios.CONFIGS["c2"]
     s = scenarios.build_system(cfg)
     r = np.random.default_rng(5).standard_normal(s.n_total())
+    monkeypatch.setenv("SDG_TD_EARLY", "1")  # unset, the faster of early and late is timed at setup
     early = sdc.TdPreconditioner(s, "td_bgs", cfg.v_max_levels, cfg.d_max_levels)
     assert {"split", "early"} <= early.features()
     assert ("wave_v" in early.features()) == (split == "0")
