@@ -371,10 +371,13 @@ __global__ void __launch_bounds__(kDotThreads) k_multidot(int64_t n, int k, cons
                                                           double* __restrict__ out) {
     pdl_begin();
     __shared__ bool am_last;
-    __shared__ double red[kDotThreads / 32][kDotGroup];
+    __shared__ double red[kDotThreads / 32][kMaxDotVecs];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int64_t b0 = blockIdx.x * chunk;
     const int64_t b1 = min(n, b0 + chunk);
+    // no block barrier between groups: a warp that has finished a group's rows
+    // folds its accumulators and starts the next group's loads while the other
+    // warps are still streaming (one barrier at the end, same fold order)
     for (int g0 = 0; g0 < k; g0 += kDotGroup) {
         double acc[kDotGroup];
 #pragma unroll
@@ -401,16 +404,16 @@ __global__ void __launch_bounds__(kDotThreads) k_multidot(int64_t n, int k, cons
 #pragma unroll
         for (int g = 0; g < kDotGroup; ++g) {
             const double t = warp_sum(acc[g]);
-            if (lane == 0) red[warp][g] = t;
+            if (lane == 0 && g < ng) red[warp][g0 + g] = t;
         }
-        __syncthreads();
-        if (threadIdx.x < ng) {
-            double t = 0.0;
-            for (int w = 0; w < nwarps; ++w) t += red[w][threadIdx.x];
-            partials[blockIdx.x * kMaxDotVecs + g0 + threadIdx.x] = t;
-        }
-        __syncthreads();
     }
+    __syncthreads();
+    if (threadIdx.x < k) {
+        double t = 0.0;
+        for (int w = 0; w < nwarps; ++w) t += red[w][threadIdx.x];
+        partials[blockIdx.x * kMaxDotVecs + threadIdx.x] = t;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned t = atomicAdd(ticket, 1u);
